@@ -1,0 +1,220 @@
+/*
+ * spfd_b200 — C-ABI of the B200-native SPFD Poisson hot path.
+ *
+ * The reference (`/root/reference/pkg/src/spfd`) is pure Python and has no
+ * FFI; its "operator API" is the Python functions each entry point below
+ * replaces (cited per function).  The Python package
+ * `paper_2010_12879_b200` binds this header with ctypes; INTEGRATION.md shows
+ * the binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - every data pointer is a DEVICE pointer (CUDA global memory) unless the
+ *     parameter name starts with `h_`; sizes are int64_t; every call that
+ *     launches work takes a `cudaStream_t` passed as `void *` (NULL = legacy
+ *     default stream) and is asynchronous unless stated otherwise;
+ *   - multi-RHS vectors ("nrhs" = 1 or 2, e.g. the real/imag parts of a
+ *     phasor) are PLANAR at the boundary: rhs k occupies
+ *     [k*len, (k+1)*len);
+ *   - node / edge / voxel orderings are exactly the reference's:
+ *     x-fastest linear indices, edges in three blocks x, y, z
+ *     (fit_operators.py:1-16); DOF vectors are in ascending node order
+ *     (fit_operators.py:406-407);
+ *   - all arithmetic is IEEE binary64;
+ *   - status codes map onto the reference exceptions in Python
+ *     (see SPFD_E* below); spfd_last_error() returns a thread-local message.
+ */
+#ifndef SPFD_B200_H
+#define SPFD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define SPFD_OK         0
+#define SPFD_EINVAL     1 /* ValueError   (bad shape / argument)                     */
+#define SPFD_ENONFINITE 2 /* SolverError  (linsolve.py:218-219, 267-268, 293-294)    */
+#define SPFD_ENOTPOS    3 /* SolverError  (linsolve.py:172-176 non-positive diagonal) */
+#define SPFD_EEMPTY     4 /* EmptySystemError (fit_operators.py:396-397, 443-444)     */
+#define SPFD_ENOCONV    5 /* never returned as an error: report flag only            */
+#define SPFD_ECUDA      6 /* RuntimeError (CUDA failure)                             */
+#define SPFD_ENCCL      7 /* RuntimeError (NCCL failure)                             */
+#define SPFD_ENOMEM     8 /* MemoryError                                             */
+
+const char *spfd_last_error(void);
+/* Library version string and the SM architecture the kernels were built for. */
+const char *spfd_version(void);
+
+/* ---- opaque handles ---------------------------------------------------- */
+typedef struct spfd_op_s  *spfd_op_t;   /* assembled voxel operator            */
+typedef struct spfd_amg_s *spfd_amg_t;  /* AMG hierarchy (+ solve workspace)   */
+
+/* ---- operator (fit_operators.py:311-457, voxel_model.py:153-159,470-511) */
+
+typedef struct {
+    int64_t dims[3];          /* voxels nx, ny, nz                              */
+    int64_t n_nodes;          /* (nx+1)(ny+1)(nz+1)                             */
+    int64_t n_edges;          /* three edge blocks                              */
+    int64_t n_dofs;           /* free conductive nodes                          */
+    int64_t n_conductive;     /* conductive nodes                               */
+    int64_t n_components;     /* conductive components (= pinned nodes if pin)  */
+    int64_t n_cond_voxels;    /* voxels with kappa > 0                          */
+    int64_t nnz;              /* nonzeros of the reduced 7-point matrix         */
+    int64_t span_len;         /* internal row-span layout length (>= n_dofs)    */
+    int64_t n_rows;           /* (ny+1)(nz+1) x-rows of the node box           */
+    int64_t device_bytes;     /* device memory owned by the handle             */
+} spfd_op_info;
+
+/* Build the operator from tissue ids and a conductivity LUT.
+ * Replaces assemble_poisson()'s operator half (fit_operators.py:367-436):
+ * kappa = lut[ids] (voxel_model.py:153-159), edge conductances
+ * (fit_operators.py:289-324), conductive components and pinning of the
+ * lowest-index node per component (voxel_model.py:470-511,
+ * fit_operators.py:394-408), DOF numbering, and the matrix-free stencil.
+ *   ids   : uint16[nx*ny*nz], x-fastest                (device)
+ *   lut   : double[lut_len], kappa per tissue id      (device)
+ *   pin   : 1 = pin one node per component (reference default)
+ * Errors: SPFD_EINVAL (id >= lut_len, bad dims), SPFD_EEMPTY (no conductive
+ * voxel).  Synchronises `stream` before returning. */
+int spfd_op_create(const int64_t *h_dims, const double *h_spacing,
+                   const uint16_t *ids, const double *lut, int64_t lut_len,
+                   int pin, void *stream, spfd_op_t *out);
+int spfd_op_destroy(spfd_op_t op);
+int spfd_op_info_get(spfd_op_t op, spfd_op_info *h_info);
+
+/* Exports (device destinations, sizes from spfd_op_info):
+ *   SPFD_EXPORT_EDGE_CONDUCTANCE  double[n_edges]   (fit_operators.py:311)
+ *   SPFD_EXPORT_DOF_TO_NODE       int64[n_dofs]     (PoissonSystem.dof_to_node)
+ *   SPFD_EXPORT_NODE_TO_DOF       int64[n_nodes]    (-1 = not a DOF)
+ *   SPFD_EXPORT_PINNED            int64[n_components]
+ *   SPFD_EXPORT_VOXEL_INDICES     int64[n_cond_voxels] (dosimetry.py:101-104)
+ *   SPFD_EXPORT_DIAGONAL          double[n_dofs]    (matrix diagonal)          */
+#define SPFD_EXPORT_EDGE_CONDUCTANCE 0
+#define SPFD_EXPORT_DOF_TO_NODE      1
+#define SPFD_EXPORT_NODE_TO_DOF      2
+#define SPFD_EXPORT_PINNED           3
+#define SPFD_EXPORT_VOXEL_INDICES    4
+#define SPFD_EXPORT_DIAGONAL         5
+int spfd_op_export(spfd_op_t op, int what, void *dst, void *stream);
+
+/* Materialise the reduced matrix as CSR (sorted columns) — the reference's
+ * PoissonSystem.matrix, bit-identical values (fit_operators.py:421-436).
+ *   indptr int64[n_dofs+1], indices int32[nnz], data double[nnz]          */
+int spfd_op_csr(spfd_op_t op, int64_t *indptr, int32_t *indices, double *data,
+                void *stream);
+
+/* y = A x with the matrix-free 7-point stencil (DOF-ordered, planar nrhs).
+ * Same products, same order as the reference csr_matvec. */
+int spfd_stencil_apply(spfd_op_t op, const double *x, double *y, int nrhs,
+                       void *stream);
+
+/* rhs = -G^T M_kappa a restricted to DOFs (fit_operators.py:438-441).
+ *   a   : double[nrhs][n_edges]  edge vector potential(s)
+ *   rhs : double[nrhs][n_dofs]                                            */
+int spfd_rhs_assemble(spfd_op_t op, const double *a, double *rhs, int nrhs,
+                      void *stream);
+
+/* ---- E-field chain (dosimetry.py:27-116) ------------------------------- */
+
+/* v = omega*(a + psi[head] - psi[tail]) on every edge (dosimetry.py:27-47).
+ *   a double[nrhs][n_edges], psi double[nrhs][n_dofs], v double[nrhs][n_edges] */
+int spfd_edge_voltages(spfd_op_t op, const double *a, const double *psi,
+                       double omega, double *v, int nrhs, void *stream);
+/* per-node |E| from edge voltages (dosimetry.py:50-85); node double[nrhs][n_nodes] */
+int spfd_node_field(spfd_op_t op, const double *v, double *node, int nrhs,
+                    void *stream);
+/* 8-corner mean on conductive voxels (dosimetry.py:88-116); vox double[nrhs][n_cond_voxels] */
+int spfd_voxel_average(spfd_op_t op, const double *node, double *vox, int nrhs,
+                       void *stream);
+/* Fused chain a, psi -> voxel |E| without materialising edge voltages or the
+ * node box: bit-identical to the three calls above.  node_out may be NULL. */
+int spfd_efield_voxavg(spfd_op_t op, const double *a, const double *psi,
+                       double omega, double *vox, int nrhs, void *stream);
+
+/* ---- AMG + Krylov (linsolve.py:26-298) ---------------------------------- */
+
+typedef struct {
+    double  rel_tol;             /* 1e-12 reference default                  */
+    int32_t max_iters;           /* 1000                                     */
+    int32_t restart;             /* 30 (FGMRES)                              */
+    int32_t pre_sweeps;          /* 1                                        */
+    int32_t post_sweeps;         /* 1                                        */
+    double  jacobi_damping;      /* 2/3                                      */
+    double  strength_threshold;  /* 0.08, halved per level                   */
+    int32_t coarse_cap;          /* 500                                      */
+    int32_t max_levels;          /* 20                                       */
+    int32_t method;              /* SPFD_METHOD_PCG | SPFD_METHOD_FGMRES     */
+    int32_t max_nrhs;            /* workspace sizing: 1 or 2                 */
+} spfd_config;
+#define SPFD_METHOD_PCG    0
+#define SPFD_METHOD_FGMRES 1
+
+typedef struct {
+    int32_t n_levels;
+    int64_t level_rows[32];
+    int64_t level_nnz[32];       /* nnz of A_l (level 0: stencil matrix nnz) */
+    int64_t prolong_nnz[32];     /* nnz of P_l (0 on the coarsest level)     */
+    double  setup_seconds;       /* device-timed                             */
+    int64_t device_bytes;
+    int32_t structured;          /* 1 = level 0 is the matrix-free stencil   */
+} spfd_amg_info;
+
+/* Hierarchy on the operator (level 0 = matrix-free stencil) or on a
+ * generic CSR (device arrays, sorted or unsorted columns).
+ * Replaces amg_setup() (linsolve.py:120-169) including plain_aggregation
+ * (_kernels.py:79-120) with identical aggregates.
+ * Errors: SPFD_ENOTPOS (non-positive diagonal), SPFD_EINVAL.
+ * Synchronises `stream`. */
+int spfd_amg_setup_op(spfd_op_t op, const spfd_config *h_cfg, void *stream,
+                      spfd_amg_t *out);
+int spfd_amg_setup_csr(int64_t n, int64_t nnz, const int64_t *indptr,
+                       const int32_t *indices, const double *data,
+                       const spfd_config *h_cfg, void *stream, spfd_amg_t *out);
+int spfd_amg_destroy(spfd_amg_t amg);
+int spfd_amg_info_get(spfd_amg_t amg, spfd_amg_info *h_info);
+
+/* Level export (device destinations; sizes from spfd_amg_info):
+ *   which = 0: A_l, 1: P_l, 2: R_l as CSR (indptr int64[rows+1], indices
+ *   int32[nnz], data double[nnz]); level 0 A is the operator CSR.
+ *   spfd_amg_level_agg: int32[rows_l] aggregate id per row of level l.    */
+int spfd_amg_level_csr(spfd_amg_t amg, int level, int which, int64_t *indptr,
+                       int32_t *indices, double *data, void *stream);
+int spfd_amg_level_agg(spfd_amg_t amg, int level, int32_t *agg, void *stream);
+
+/* z = V-cycle(r) (linsolve.py:179-197), planar nrhs, level-0 ordering
+ * (DOF order for an operator hierarchy, row order for a CSR one). */
+int spfd_vcycle(spfd_amg_t amg, const double *r, double *z, int nrhs,
+                void *stream);
+
+typedef struct {
+    int32_t iterations;          /* Krylov iterations (max over rhs)         */
+    int32_t converged;           /* all rhs at rel_residual <= rel_tol       */
+    double  rel_residual[2];     /* true ||b - A x|| / ||b|| per rhs          */
+    double  solve_seconds;       /* device-timed                             */
+    int32_t status;              /* SPFD_OK or the error code                */
+} spfd_report;
+
+/* Solve A x = b (x starts at 0).  method from cfg (PCG default; FGMRES(m)
+ * with the reference semantics, linsolve.py:200-298).  Non-convergence is
+ * a report flag, not an error.  h_trace (may be NULL) receives
+ * max_iters*nrhs residual estimates (iteration-major).
+ * Synchronises `stream` (the report is host data). */
+int spfd_solve(spfd_amg_t amg, const double *b, double *x, int nrhs,
+               const spfd_config *h_cfg, spfd_report *h_rep, double *h_trace,
+               void *stream);
+
+/* ---- device-resident snapshot pipeline (pipeline.py:158-175, C5) ------- */
+
+/* One snapshot on a resident operator + hierarchy: rhs assembly, solve and
+ * fused E-field/voxel average, all on `stream`.  vox double[nrhs][n_cond_voxels];
+ * psi (may be NULL) double[nrhs][n_dofs]. */
+int spfd_snapshot(spfd_op_t op, spfd_amg_t amg, const double *a, double omega,
+                  double *psi, double *vox, int nrhs, const spfd_config *h_cfg,
+                  spfd_report *h_rep, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPFD_B200_H */

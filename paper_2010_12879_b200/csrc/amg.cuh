@@ -1,0 +1,76 @@
+// Smoothed-aggregation AMG hierarchy and Krylov solvers (device).
+#pragma once
+#include <vector>
+
+#include "op.cuh"
+
+namespace spfd {
+
+struct Csr {
+    int64_t rows = 0, cols = 0, nnz = 0;
+    DevBuf<int64_t> ptr;   // rows + 1
+    DevBuf<int32_t> col;   // nnz (sorted per row)
+    DevBuf<double> val;    // nnz
+    void alloc(int64_t r, int64_t c, int64_t z) {
+        rows = r; cols = c; nnz = z;
+        ptr.alloc(r + 1); col.alloc(z); val.alloc(z);
+    }
+    int64_t bytes() const { return ptr.bytes() + col.bytes() + val.bytes(); }
+};
+
+struct CsrView {
+    const int64_t *ptr;
+    const int32_t *col;
+    const double *val;
+    int64_t rows;
+};
+inline CsrView view(const Csr &m) { return CsrView{m.ptr.get(), m.col.get(), m.val.get(), m.rows}; }
+
+struct Level {
+    int64_t n = 0;            // unknowns on this level
+    int64_t nvec = 0;         // vector length (span L on a structured level 0)
+    int64_t a_nnz = 0;        // nnz(A_l) (reference CSR count)
+    Csr A;                    // CSR (absent on a structured level 0 after setup)
+    Csr P, R;                 // solve-layout prolongation / restriction
+    Csr P_dof, R_dof;         // DOF-numbered copies (structured level 0 only; exports)
+    DevBuf<int32_t> agg;      // aggregate per row (DOF numbering)
+    DevBuf<double> dinv;      // [nvec]
+    DevBuf<double> odinv;     // [nvec] omega * dinv
+    DevBuf<double> vr, vx, vd, vt;  // workspaces [nvec * max_nrhs]
+    int p_group = 4, r_group = 32, a_group = 32;  // lanes per row in CSR kernels
+};
+
+struct Amg {
+    std::vector<Level> lv;
+    Operator *op = nullptr;   // structured level 0 (not owned)
+    bool structured = false;
+    int64_t nc = 0;           // coarsest size
+    DevBuf<double> cinv;      // dense inverse of the coarsest matrix (nc x nc)
+    double omega = 2.0 / 3.0;
+    int pre = 1, post = 1;
+    int max_nrhs = 2;
+    double setup_seconds = 0.0;
+    // Krylov workspace (level-0 layout, interleaved nrhs)
+    DevBuf<double> kx, kr, kz, kp, kq, kb;
+    DevBuf<double> partials;  // per-CTA dot partials
+    DevBuf<double> scal;      // device scalars
+    DevBuf<double> fg_basis, fg_prec;  // FGMRES basis (allocated on demand)
+    int64_t fg_m = 0;
+    int64_t device_bytes() const;
+};
+
+Amg *amg_setup_op(Operator *op, const spfd_config &cfg, cudaStream_t s);
+Amg *amg_setup_csr(int64_t n, int64_t nnz, const int64_t *ptr, const int32_t *col, const double *val,
+                   const spfd_config &cfg, cudaStream_t s);
+void amg_vcycle(Amg &h, const double *r, double *z, int nrhs, cudaStream_t s);  // level-0 layout, interleaved
+void amg_level_csr(Amg &h, int level, int which, int64_t *ptr, int32_t *col, double *val, cudaStream_t s);
+void amg_level_agg(Amg &h, int level, int32_t *agg, cudaStream_t s);
+
+// level-0 layout helpers (span for structured, identity for CSR)
+void amg_to_level0(Amg &h, const double *planar, double *inter, int nrhs, cudaStream_t s);
+void amg_from_level0(Amg &h, const double *inter, double *planar, int nrhs, cudaStream_t s);
+
+spfd_report krylov_solve(Amg &h, const double *b_inter, double *x_inter, int nrhs, const spfd_config &cfg,
+                         double *h_trace, cudaStream_t s);
+
+}  // namespace spfd

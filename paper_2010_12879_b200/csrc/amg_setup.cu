@@ -1,0 +1,948 @@
+// Device AMG setup: strength graph, exact greedy aggregation, smoothed
+// prolongation and Galerkin products (linsolve.py:106-176, _kernels.py:79-120).
+//
+// Parity contract: given the reference's fine matrix, the aggregates are
+// identical and P, R = P^T and every coarse operator are bit-identical to the
+// scipy results (products are formed without FMA and each output entry is
+// summed sequentially in the order scipy's csr_matmat accumulates it).
+#include <cub/cub.cuh>
+
+#include <chrono>
+
+#include "amg.cuh"
+
+namespace spfd {
+
+namespace {
+
+template <class T>
+T read1(const T *dev, cudaStream_t s) {
+    T h;
+    SPFD_CUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+template <class In, class Out>
+void scan_excl(In in, Out *out, int64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    SPFD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+    DevBuf<uint8_t> tmp;
+    tmp.alloc(bytes);
+    SPFD_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, in, out, n, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+}
+
+inline int bits_for(uint64_t v) {
+    int b = 1;
+    while (b < 64 && (v >> b) != 0) ++b;
+    return b;
+}
+
+// ---------------------------------------------------------------- diag --
+__global__ void k_diag_dinv(CsrView a, double omega, double *dinv, double *odinv, double *diag_out,
+                            int *bad) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < a.rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double d = 0.0;
+        for (int64_t q = a.ptr[r]; q < a.ptr[r + 1]; ++q)
+            if (a.col[q] == r) d = add_rn(d, a.val[q]);
+        if (!(d > 0.0)) *bad = 1;
+        double di = 1.0 / d;
+        dinv[r] = di;
+        odinv[r] = mul_rn(omega, di);
+        if (diag_out) diag_out[r] = d;
+    }
+}
+
+// ------------------------------------------------------------ strength --
+// strong(i,j): i != j and |a_ij| >= (theta*sd_i)*sd_j, sd = sqrt|a_ii|
+// (linsolve.py:106-117)
+__global__ void k_strength_count(CsrView a, const double *diag, double theta, int64_t *cnt) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < a.rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double sr = __dsqrt_rn(fabs(diag[r]));
+        double tr = mul_rn(theta, sr);
+        int64_t c = 0;
+        for (int64_t q = a.ptr[r]; q < a.ptr[r + 1]; ++q) {
+            int j = a.col[q];
+            if (j == r) continue;
+            c += fabs(a.val[q]) >= mul_rn(tr, __dsqrt_rn(fabs(diag[j])));
+        }
+        cnt[r] = c;
+    }
+}
+
+__global__ void k_strength_fill(CsrView a, const double *diag, double theta, const int64_t *sptr,
+                                int32_t *scol, double *sval) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < a.rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double tr = mul_rn(theta, __dsqrt_rn(fabs(diag[r])));
+        int64_t o = sptr[r];
+        for (int64_t q = a.ptr[r]; q < a.ptr[r + 1]; ++q) {
+            int j = a.col[q];
+            if (j == r) continue;
+            double m = fabs(a.val[q]);
+            if (m >= mul_rn(tr, __dsqrt_rn(fabs(diag[j])))) { scol[o] = j; sval[o] = m; ++o; }
+        }
+    }
+}
+
+// pattern transpose (order within a row irrelevant for its users)
+__global__ void k_count_cols(const int32_t *col, int64_t nnz, int64_t *cnt) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+         q += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd((unsigned long long *)&cnt[col[q]], 1ull);
+}
+
+__global__ void k_scatter_t(const int64_t *ptr, const int32_t *col, int64_t rows, int64_t *cursor,
+                            int32_t *tcol) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+         r += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t q = ptr[r]; q < ptr[r + 1]; ++q) {
+            unsigned long long o = atomicAdd((unsigned long long *)&cursor[col[q]], 1ull);
+            tcol[o] = (int32_t)r;
+        }
+}
+
+// --------------------------------------------------------- aggregation --
+// Pass 1 of _kernels.py:79-120 is the greedy (index-order) selection of
+// roots such that no two roots "claim" (root + strong neighbours) a common
+// node.  i becomes a root iff every lower-index node r that could claim a
+// node of {i} U S(i) is decided non-root; i is non-root as soon as a root
+// claims a node of {i} U S(i).  Both rules are monotone, so they can be
+// applied asynchronously in rounds; the fixed point is exactly the serial
+// result.  Work is event driven: a decided node re-queues its dependants.
+struct Graph {
+    const int64_t *sp;  // strong graph S
+    const int32_t *sc;
+    const int64_t *tp;  // transpose S^T (claimers)
+    const int32_t *tc;
+};
+
+__device__ __forceinline__ void notify_dependants(Graph g, int i, int8_t *state, int *queued, int round,
+                                                  int *next, int *n_next) {
+    // dependants: j > i with j in {x} U ST(x) for x in {i} U S(i)
+    for (int64_t a = g.sp[i] - 1; a < g.sp[i + 1]; ++a) {
+        int x = a < g.sp[i] ? i : g.sc[a];
+        for (int64_t b = g.tp[x] - 1; b < g.tp[x + 1]; ++b) {
+            int j = b < g.tp[x] ? x : g.tc[b];
+            if (j <= i) continue;
+            if (*(volatile int8_t *)&state[j] != 0) continue;
+            if (atomicExch(&queued[j], round) != round) {
+                int slot = atomicAdd(n_next, 1);
+                next[slot] = j;
+            }
+        }
+    }
+}
+
+__global__ void k_agg_round(Graph g, int8_t *state, int32_t *claimed, int *queued, int round,
+                            const int *cur, const int *n_cur_p, int *next, int *n_next, int full_n) {
+    int n_cur = full_n > 0 ? full_n : *n_cur_p;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n_cur; idx += gridDim.x * blockDim.x) {
+        int i = full_n > 0 ? idx : cur[idx];
+        if (*(volatile int8_t *)&state[i] != 0) continue;
+        bool blocked = false, waiting = false;
+        for (int64_t a = g.sp[i] - 1; a < g.sp[i + 1] && !blocked; ++a) {
+            int x = a < g.sp[i] ? i : g.sc[a];
+            for (int64_t b = g.tp[x] - 1; b < g.tp[x + 1]; ++b) {
+                int r = b < g.tp[x] ? x : g.tc[b];
+                int8_t st = *(volatile int8_t *)&state[r];
+                if (st == 1) { blocked = true; break; }
+                if (st == 0 && r < i) waiting = true;
+            }
+        }
+        if (blocked) {
+            state[i] = 2;
+        } else if (!waiting) {
+            claimed[i] = i;
+            for (int64_t a = g.sp[i]; a < g.sp[i + 1]; ++a) claimed[g.sc[a]] = i;
+            __threadfence();
+            state[i] = 1;
+        } else {
+            continue;
+        }
+        notify_dependants(g, i, state, queued, round + 1, next, n_next);
+    }
+}
+
+__global__ void k_swap_counts(int *n_cur, int *n_next) {
+    *n_cur = *n_next;
+    *n_next = 0;
+}
+
+// Pass 2: strongest already-assigned strong neighbour (strict '>', first
+// maximum in CSR order); j < i always counts as assigned in the serial scan.
+__global__ void k_agg_best(const int64_t *sp, const int32_t *sc, const double *sv, const int32_t *claimed,
+                           int64_t n, int32_t *best, int32_t *single) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (claimed[i] >= 0) { best[i] = -2; single[i] = 0; continue; }
+        int b = -1;
+        double top = 0.0;
+        for (int64_t q = sp[i]; q < sp[i + 1]; ++q) {
+            int j = sc[q];
+            if ((j < i || claimed[j] >= 0) && sv[q] > top) { top = sv[q]; b = j; }
+        }
+        best[i] = b;
+        single[i] = b < 0 ? 1 : 0;
+    }
+}
+
+__global__ void k_root_flags(const int8_t *state, int64_t n, int32_t *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = state[i] == 1 ? 1 : 0;
+}
+
+__global__ void k_agg_final(const int32_t *claimed, const int32_t *best, const int32_t *root_rank,
+                            const int32_t *single_rank, int32_t n_roots, int64_t n, int32_t *agg) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t j = i;
+        while (true) {
+            if (claimed[j] >= 0) { agg[i] = root_rank[claimed[j]]; break; }
+            int b = best[j];
+            if (b < 0) { agg[i] = n_roots + single_rank[j]; break; }
+            j = b;
+        }
+    }
+}
+
+// ------------------------------------------------------------ ESC SpGEMM --
+__global__ void k_prod_count(CsrView a, CsrView b, int64_t *cnt) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < a.rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t c = 0;
+        for (int64_t q = a.ptr[r]; q < a.ptr[r + 1]; ++q) {
+            int k = a.col[q];
+            c += b.ptr[k + 1] - b.ptr[k];
+        }
+        cnt[r] = c;
+    }
+}
+
+// expansion in scipy csr_matmat order: A's row order, then B's row order
+__global__ void k_prod_expand(CsrView a, CsrView b, int64_t row0, int64_t row1, const int64_t *off,
+                              int64_t base, uint64_t ncols, uint64_t *keys, double *vals) {
+    for (int64_t r = row0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < row1;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t o = off[r] - base;
+        for (int64_t q = a.ptr[r]; q < a.ptr[r + 1]; ++q) {
+            int k = a.col[q];
+            double av = a.val[q];
+            for (int64_t t = b.ptr[k]; t < b.ptr[k + 1]; ++t) {
+                keys[o] = (uint64_t)r * ncols + (uint64_t)b.col[t];
+                vals[o] = mul_rn(av, b.val[t]);
+                ++o;
+            }
+        }
+    }
+}
+
+__global__ void k_heads(const uint64_t *keys, int64_t m, int32_t *head) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m;
+         q += (int64_t)gridDim.x * blockDim.x)
+        head[q] = (q == 0 || keys[q] != keys[q - 1]) ? 1 : 0;
+}
+
+__global__ void k_seg_starts(const int32_t *head, const int64_t *segid, int64_t m, int64_t *start) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m;
+         q += (int64_t)gridDim.x * blockDim.x)
+        if (head[q]) start[segid[q]] = q;
+}
+
+// sequential per-segment sum (the order scipy accumulates sums[k])
+__global__ void k_seg_sum(const uint64_t *keys, const double *vals, const int64_t *start, int64_t nseg,
+                          int64_t m, bool drop_zero, uint64_t *okey, double *oval, int32_t *keep) {
+    for (int64_t sg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sg < nseg;
+         sg += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b = start[sg], e = sg + 1 < nseg ? start[sg + 1] : m;
+        double v = 0.0;
+        for (int64_t q = b; q < e; ++q) v = add_rn(v, vals[q]);
+        okey[sg] = keys[b];
+        oval[sg] = v;
+        keep[sg] = (!drop_zero || v != 0.0) ? 1 : 0;
+    }
+}
+
+__global__ void k_compact(const uint64_t *key, const double *val, const int32_t *keep, const int64_t *pos,
+                          int64_t nseg, uint64_t ncols, int64_t out_base, int32_t *col, double *oval,
+                          int64_t *rowcnt) {
+    for (int64_t sg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sg < nseg;
+         sg += (int64_t)gridDim.x * blockDim.x) {
+        if (!keep[sg]) continue;
+        int64_t o = out_base + pos[sg];
+        uint64_t k = key[sg];
+        col[o] = (int32_t)(k % ncols);
+        oval[o] = val[sg];
+        atomicAdd((unsigned long long *)&rowcnt[k / ncols], 1ull);
+    }
+}
+
+__global__ void k_find_chunk(const int64_t *off, int64_t rows, int64_t r0, int64_t budget, int64_t *out) {
+    // largest r1 in (r0, rows] with off[r1] - off[r0] <= budget (at least r0+1)
+    int64_t lo = r0 + 1, hi = rows;
+    int64_t base = off[r0];
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) / 2;
+        if (off[mid] - base <= budget) lo = mid; else hi = mid - 1;
+    }
+    *out = lo;
+}
+
+struct Pieces {
+    std::vector<DevBuf<int32_t>> cols;
+    std::vector<DevBuf<double>> vals;
+    std::vector<int64_t> counts;
+};
+
+constexpr int64_t kChunkProducts = 192ll << 20;  // products per ESC chunk
+
+// C = A * B (sorted columns, optional zero dropping).
+void spgemm(const CsrView &a, const CsrView &b, int64_t bcols, Csr &c, bool drop_zero, cudaStream_t s) {
+    const int T = 256;
+    int64_t rows = a.rows;
+    DevBuf<int64_t> cnt, off, rowcnt;
+    cnt.alloc(rows + 1);
+    off.alloc(rows + 1);
+    rowcnt.alloc(rows + 1);
+    SPFD_CUDA(cudaMemsetAsync(cnt.get() + rows, 0, sizeof(int64_t), s));
+    SPFD_CUDA(cudaMemsetAsync(rowcnt.get(), 0, rowcnt.bytes(), s));
+    if (rows > 0) k_prod_count<<<grid_for(rows, T), T, 0, s>>>(a, b, cnt.get());
+    SPFD_LAUNCH_CHECK();
+    scan_excl(cnt.get(), off.get(), rows + 1, s);
+    int64_t total = read1(off.get() + rows, s);
+    uint64_t ncols = (uint64_t)(bcols > 0 ? bcols : 1);
+    int end_bit = bits_for((uint64_t)rows * ncols);
+
+    Pieces pc;
+    DevBuf<int64_t> chunk_end;
+    chunk_end.alloc(1);
+    int64_t r0 = 0, out_total = 0;
+    while (r0 < rows) {
+        k_find_chunk<<<1, 1, 0, s>>>(off.get(), rows, r0, kChunkProducts, chunk_end.get());
+        int64_t r1 = read1(chunk_end.get(), s);
+        int64_t base = read1(off.get() + r0, s);
+        int64_t m = read1(off.get() + r1, s) - base;
+        if (m > 0) {
+            DevBuf<uint64_t> k0, k1, okey;
+            DevBuf<double> v0, v1, oval;
+            k0.alloc(m); k1.alloc(m); v0.alloc(m); v1.alloc(m);
+            k_prod_expand<<<grid_for(r1 - r0, T), T, 0, s>>>(a, b, r0, r1, off.get(), base, ncols, k0.get(),
+                                                             v0.get());
+            SPFD_LAUNCH_CHECK();
+            size_t bytes = 0;
+            SPFD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0.get(), k1.get(), v0.get(), v1.get(),
+                                                      m, 0, end_bit, s));
+            {
+                DevBuf<uint8_t> tmp;
+                tmp.alloc(bytes);
+                SPFD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, k0.get(), k1.get(), v0.get(),
+                                                          v1.get(), m, 0, end_bit, s));
+                SPFD_CUDA(cudaStreamSynchronize(s));
+            }
+            k0.release(); v0.release();
+            DevBuf<int32_t> head;
+            DevBuf<int64_t> segid;
+            head.alloc(m);
+            segid.alloc(m + 1);
+            k_heads<<<grid_for(m, T), T, 0, s>>>(k1.get(), m, head.get());
+            {
+                cub::TransformInputIterator<int64_t, WidenI32, const int32_t *> wi(head.get(), WidenI32());
+                // inclusive ids minus one -> exclusive scan then use directly
+                scan_excl(wi, segid.get(), m, s);
+            }
+            int64_t nseg = read1(segid.get() + (m - 1), s) + read1(head.get() + (m - 1), s);
+            DevBuf<int64_t> start;
+            start.alloc(nseg);
+            k_seg_starts<<<grid_for(m, T), T, 0, s>>>(head.get(), segid.get(), m, start.get());
+            head.release(); segid.release();
+            okey.alloc(nseg); oval.alloc(nseg);
+            DevBuf<int32_t> keep;
+            keep.alloc(nseg + 1);
+            SPFD_CUDA(cudaMemsetAsync(keep.get() + nseg, 0, sizeof(int32_t), s));
+            k_seg_sum<<<grid_for(nseg, T), T, 0, s>>>(k1.get(), v1.get(), start.get(), nseg, m, drop_zero,
+                                                      okey.get(), oval.get(), keep.get());
+            SPFD_LAUNCH_CHECK();
+            k1.release(); v1.release(); start.release();
+            DevBuf<int64_t> pos;
+            pos.alloc(nseg + 1);
+            {
+                cub::TransformInputIterator<int64_t, WidenI32, const int32_t *> wi(keep.get(), WidenI32());
+                scan_excl(wi, pos.get(), nseg + 1, s);
+            }
+            int64_t kept = read1(pos.get() + nseg, s);
+            DevBuf<int32_t> pcol;
+            DevBuf<double> pval;
+            pcol.alloc(kept); pval.alloc(kept);
+            k_compact<<<grid_for(nseg, T), T, 0, s>>>(okey.get(), oval.get(), keep.get(), pos.get(), nseg, ncols,
+                                                      0, pcol.get(), pval.get(), rowcnt.get());
+            SPFD_LAUNCH_CHECK();
+            SPFD_CUDA(cudaStreamSynchronize(s));
+            pc.cols.push_back(std::move(pcol));
+            pc.vals.push_back(std::move(pval));
+            pc.counts.push_back(kept);
+            out_total += kept;
+        }
+        r0 = r1;
+    }
+    c.alloc(rows, bcols, out_total);
+    int64_t o = 0;
+    for (size_t q = 0; q < pc.counts.size(); ++q) {
+        if (pc.counts[q] == 0) continue;
+        SPFD_CUDA(cudaMemcpyAsync(c.col.get() + o, pc.cols[q].get(), pc.counts[q] * sizeof(int32_t),
+                                  cudaMemcpyDeviceToDevice, s));
+        SPFD_CUDA(cudaMemcpyAsync(c.val.get() + o, pc.vals[q].get(), pc.counts[q] * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, s));
+        o += pc.counts[q];
+    }
+    scan_excl(rowcnt.get(), c.ptr.get(), rows + 1, s);
+}
+
+// transpose with (col, row)-sorted output: stable radix sort on col*rows+row
+__global__ void k_t_keys(CsrView a, uint64_t nrows, uint64_t *keys, double *vals) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < a.rows;
+         r += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t q = a.ptr[r]; q < a.ptr[r + 1]; ++q) {
+            keys[q] = (uint64_t)a.col[q] * nrows + (uint64_t)r;
+            vals[q] = a.val[q];
+        }
+}
+
+__global__ void k_t_out(const uint64_t *keys, const double *vals, int64_t nnz, uint64_t nrows, int32_t *col,
+                        double *val, int64_t *rowcnt) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        col[q] = (int32_t)(keys[q] % nrows);
+        val[q] = vals[q];
+        atomicAdd((unsigned long long *)&rowcnt[keys[q] / nrows], 1ull);
+    }
+}
+
+void transpose(const CsrView &a, int64_t acols, Csr &t, cudaStream_t s) {
+    const int T = 256;
+    int64_t nnz = read1(a.ptr + a.rows, s);
+    t.alloc(acols, a.rows, nnz);
+    DevBuf<int64_t> rowcnt;
+    rowcnt.alloc(acols + 1);
+    SPFD_CUDA(cudaMemsetAsync(rowcnt.get(), 0, rowcnt.bytes(), s));
+    if (nnz > 0) {
+        DevBuf<uint64_t> k0, k1;
+        DevBuf<double> v0, v1;
+        k0.alloc(nnz); k1.alloc(nnz); v0.alloc(nnz); v1.alloc(nnz);
+        uint64_t nrows = (uint64_t)(a.rows > 0 ? a.rows : 1);
+        k_t_keys<<<grid_for(a.rows, T), T, 0, s>>>(a, nrows, k0.get(), v0.get());
+        int end_bit = bits_for((uint64_t)acols * nrows);
+        size_t bytes = 0;
+        SPFD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0.get(), k1.get(), v0.get(), v1.get(), nnz, 0,
+                                                  end_bit, s));
+        DevBuf<uint8_t> tmp;
+        tmp.alloc(bytes);
+        SPFD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, k0.get(), k1.get(), v0.get(), v1.get(), nnz,
+                                                  0, end_bit, s));
+        k_t_out<<<grid_for(nnz, T), T, 0, s>>>(k1.get(), v1.get(), nnz, nrows, t.col.get(), t.val.get(),
+                                               rowcnt.get());
+        SPFD_LAUNCH_CHECK();
+        SPFD_CUDA(cudaStreamSynchronize(s));
+    }
+    scan_excl(rowcnt.get(), t.ptr.get(), acols + 1, s);
+}
+
+// P = T - (omega*dinv_i) * AT (entries of AT with zero results dropped;
+// scipy binop semantics of `tentative - smoothed`, linsolve.py:146-150)
+__global__ void k_make_p(CsrView at, const int32_t *agg, const double *dinv, double omega, int64_t *cnt,
+                         double *val_out, int32_t *keep) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < at.rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double scale = mul_rn(omega, dinv[r]);
+        int64_t c = 0;
+        for (int64_t q = at.ptr[r]; q < at.ptr[r + 1]; ++q) {
+            double sm = mul_rn(at.val[q], scale);
+            double v = at.col[q] == agg[r] ? sub_rn(1.0, sm) : sub_rn(0.0, sm);
+            val_out[q] = v;
+            keep[q] = v != 0.0;
+            c += v != 0.0;
+        }
+        cnt[r] = c;
+    }
+}
+
+__global__ void k_compact_rows(CsrView src, const double *vals, const int32_t *keep, const int64_t *optr,
+                               int32_t *ocol, double *oval) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < src.rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t o = optr[r];
+        for (int64_t q = src.ptr[r]; q < src.ptr[r + 1]; ++q)
+            if (keep[q]) { ocol[o] = src.col[q]; oval[o] = vals[q]; ++o; }
+    }
+}
+
+// ------------------------------------------------------ dense inverse ----
+__global__ void k_dense_from_csr(CsrView a, int64_t n, double *m) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t q = a.ptr[r]; q < a.ptr[r + 1]; ++q) m[r * n + a.col[q]] = add_rn(m[r * n + a.col[q]], a.val[q]);
+}
+
+__global__ void k_eye(int64_t n, double *m) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n * n;
+         q += (int64_t)gridDim.x * blockDim.x)
+        m[q] = (q / n == q % n) ? 1.0 : 0.0;
+}
+
+// Gauss-Jordan step k on [M | Inv] (SPD: no pivoting needed)
+__global__ void k_gj_save(const double *m, int64_t n, int64_t k, double *f, int *bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        f[i] = m[i * n + k];
+        if (i == k && !(f[i] > 0.0 && isfinite(f[i]))) *bad = 1;
+    }
+}
+
+__global__ void k_gj_norm(double *m, double *inv, int64_t n, int64_t k, const double *f) {
+    double piv = f[k];
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        m[k * n + c] /= piv;
+        inv[k * n + c] /= piv;
+    }
+}
+
+__global__ void k_gj_elim(double *m, double *inv, int64_t n, int64_t k, const double *f) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n * n;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = q / n, c = q % n;
+        if (i == k) continue;
+        double fi = f[i];
+        if (fi == 0.0) continue;
+        m[i * n + c] -= fi * m[k * n + c];
+        inv[i * n + c] -= fi * inv[k * n + c];
+    }
+}
+
+void dense_inverse(const Csr &a, DevBuf<double> &inv, cudaStream_t s) {
+    int64_t n = a.rows;
+    SPFD_CHECK(n <= 16384, SPFD_EINVAL, "coarsest level too large for a dense factorisation");
+    DevBuf<double> m, f;
+    DevBuf<int> bad;
+    m.alloc(n * n); f.alloc(n); bad.alloc(1);
+    inv.alloc(n * n);
+    SPFD_CUDA(cudaMemsetAsync(m.get(), 0, m.bytes(), s));
+    SPFD_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    const int T = 256;
+    k_dense_from_csr<<<grid_for(n, T), T, 0, s>>>(view(a), n, m.get());
+    k_eye<<<grid_for(n * n, T), T, 0, s>>>(n, inv.get());
+    for (int64_t k = 0; k < n; ++k) {
+        k_gj_save<<<grid_for(n, T), T, 0, s>>>(m.get(), n, k, f.get(), bad.get());
+        k_gj_norm<<<grid_for(n, T), T, 0, s>>>(m.get(), inv.get(), n, k, f.get());
+        k_gj_elim<<<grid_for(n * n, T), T, 0, s>>>(m.get(), inv.get(), n, k, f.get());
+    }
+    SPFD_LAUNCH_CHECK();
+    SPFD_CHECK(read1(bad.get(), s) == 0, SPFD_ENOTPOS, "coarsest matrix is not positive definite");
+}
+
+// ------------------------------------------------- structured level 0 ----
+__global__ void k_span_rowcnt(const int32_t *pos_to_dof, int64_t L, const int64_t *pptr, int64_t *cnt) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int d = pos_to_dof[p];
+        cnt[p] = d >= 0 ? pptr[d + 1] - pptr[d] : 0;
+    }
+}
+
+__global__ void k_map_cols(const int32_t *col, int64_t nnz, const int32_t *dof_to_pos, int32_t *out) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+         q += (int64_t)gridDim.x * blockDim.x)
+        out[q] = dof_to_pos[col[q]];
+}
+
+__global__ void k_dofs_to_span_1(const int32_t *pos_to_dof, int64_t L, const double *in, double *out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int d = pos_to_dof[p];
+        out[p] = d >= 0 ? in[d] : 0.0;
+    }
+}
+
+int pick_group(int64_t nnz, int64_t rows) {
+    double avg = rows > 0 ? (double)nnz / (double)rows : 1.0;
+    if (avg <= 6.0) return 4;
+    if (avg <= 14.0) return 8;
+    if (avg <= 28.0) return 16;
+    return 32;
+}
+
+// One coarsening step on level l (CSR A in level numbering).  Returns false
+// on stagnation.
+bool coarsen(Level &L, const Csr &A, double theta, double omega, Csr &Ac, Csr &P, Csr &R, DevBuf<int32_t> &agg,
+             cudaStream_t s) {
+    const int T = 256;
+    int64_t n = A.rows;
+    CsrView av = view(A);
+    DevBuf<double> diag;
+    diag.alloc(n);
+    {
+        DevBuf<double> d1, d2;
+        d1.alloc(n); d2.alloc(n);
+        DevBuf<int> bad;
+        bad.alloc(1);
+        SPFD_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+        k_diag_dinv<<<grid_for(n, T), T, 0, s>>>(av, omega, d1.get(), d2.get(), diag.get(), bad.get());
+        SPFD_CHECK(read1(bad.get(), s) == 0, SPFD_ENOTPOS, "matrix has a non-positive diagonal entry");
+    }
+    // strength graph
+    DevBuf<int64_t> scnt, sptr;
+    scnt.alloc(n + 1); sptr.alloc(n + 1);
+    SPFD_CUDA(cudaMemsetAsync(scnt.get() + n, 0, sizeof(int64_t), s));
+    k_strength_count<<<grid_for(n, T), T, 0, s>>>(av, diag.get(), theta, scnt.get());
+    scan_excl(scnt.get(), sptr.get(), n + 1, s);
+    int64_t snnz = read1(sptr.get() + n, s);
+    DevBuf<int32_t> scol;
+    DevBuf<double> sval;
+    scol.alloc(snnz); sval.alloc(snnz);
+    k_strength_fill<<<grid_for(n, T), T, 0, s>>>(av, diag.get(), theta, sptr.get(), scol.get(), sval.get());
+    // transpose pattern
+    DevBuf<int64_t> tcnt, tptr, cursor;
+    tcnt.alloc(n + 1); tptr.alloc(n + 1); cursor.alloc(n + 1);
+    SPFD_CUDA(cudaMemsetAsync(tcnt.get(), 0, tcnt.bytes(), s));
+    if (snnz) k_count_cols<<<grid_for(snnz, T), T, 0, s>>>(scol.get(), snnz, tcnt.get());
+    scan_excl(tcnt.get(), tptr.get(), n + 1, s);
+    SPFD_CUDA(cudaMemcpyAsync(cursor.get(), tptr.get(), (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    DevBuf<int32_t> tcol;
+    tcol.alloc(snnz);
+    k_scatter_t<<<grid_for(n, T), T, 0, s>>>(sptr.get(), scol.get(), n, cursor.get(), tcol.get());
+    SPFD_LAUNCH_CHECK();
+
+    // pass 1
+    DevBuf<int8_t> state;
+    DevBuf<int32_t> claimed;
+    DevBuf<int> queued, wl0, wl1, counts;
+    state.alloc(n); claimed.alloc(n); queued.alloc(n); wl0.alloc(n); wl1.alloc(n); counts.alloc(2);
+    SPFD_CUDA(cudaMemsetAsync(state.get(), 0, n, s));
+    SPFD_CUDA(cudaMemsetAsync(claimed.get(), 0xff, n * sizeof(int32_t), s));
+    SPFD_CUDA(cudaMemsetAsync(queued.get(), 0xff, n * sizeof(int), s));
+    SPFD_CUDA(cudaMemsetAsync(counts.get(), 0, 2 * sizeof(int), s));
+    Graph g{sptr.get(), scol.get(), tptr.get(), tcol.get()};
+    int *cur = wl0.get(), *nxt = wl1.get();
+    int *n_cur = counts.get(), *n_next = counts.get() + 1;
+    const int G = 148 * 8;
+    k_agg_round<<<grid_for(n, T, G), T, 0, s>>>(g, state.get(), claimed.get(), queued.get(), 0, cur, n_cur, nxt,
+                                               n_next, (int)n);
+    k_swap_counts<<<1, 1, 0, s>>>(n_cur, n_next);
+    std::swap(cur, nxt);
+    int round = 1;
+    while (true) {
+        for (int b = 0; b < 64; ++b, ++round) {
+            k_agg_round<<<G, T, 0, s>>>(g, state.get(), claimed.get(), queued.get(), round, cur, n_cur, nxt, n_next, 0);
+            k_swap_counts<<<1, 1, 0, s>>>(n_cur, n_next);
+            std::swap(cur, nxt);
+        }
+        SPFD_LAUNCH_CHECK();
+        if (read1(n_cur, s) == 0) break;
+        SPFD_CHECK(round < 4 * (int)n + 1000, SPFD_ECUDA, "aggregation did not terminate");
+    }
+    // pass 2 + numbering
+    DevBuf<int32_t> best, single, rootflag, root_rank, single_rank;
+    best.alloc(n); single.alloc(n + 1); rootflag.alloc(n + 1); root_rank.alloc(n + 1); single_rank.alloc(n + 1);
+    SPFD_CUDA(cudaMemsetAsync(single.get() + n, 0, sizeof(int32_t), s));
+    SPFD_CUDA(cudaMemsetAsync(rootflag.get() + n, 0, sizeof(int32_t), s));
+    k_agg_best<<<grid_for(n, T), T, 0, s>>>(sptr.get(), scol.get(), sval.get(), claimed.get(), n, best.get(),
+                                             single.get());
+    k_root_flags<<<grid_for(n, T), T, 0, s>>>(state.get(), n, rootflag.get());
+    scan_excl(rootflag.get(), root_rank.get(), n + 1, s);
+    scan_excl(single.get(), single_rank.get(), n + 1, s);
+    int32_t n_roots = read1(root_rank.get() + n, s);
+    int32_t n_single = read1(single_rank.get() + n, s);
+    int64_t n_agg = (int64_t)n_roots + n_single;
+    agg.alloc(n);
+    k_agg_final<<<grid_for(n, T), T, 0, s>>>(claimed.get(), best.get(), root_rank.get(), single_rank.get(),
+                                              n_roots, n, agg.get());
+    SPFD_LAUNCH_CHECK();
+    if (n_agg >= n) return false;
+
+    // tentative T (n x n_agg, ones) and AT = A * T (zeros kept)
+    Csr Tm;
+    Tm.alloc(n, n_agg, n);
+    {
+        std::vector<int64_t> hp(n + 1);
+        for (int64_t i = 0; i <= n; ++i) hp[i] = i;
+        SPFD_CUDA(cudaMemcpyAsync(Tm.ptr.get(), hp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        std::vector<double> hv((size_t)n, 1.0);
+        SPFD_CUDA(cudaMemcpyAsync(Tm.val.get(), hv.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+        SPFD_CUDA(cudaMemcpyAsync(Tm.col.get(), agg.get(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        SPFD_CUDA(cudaStreamSynchronize(s));
+    }
+    Csr AT;
+    spgemm(av, view(Tm), n_agg, AT, false, s);
+    Tm = Csr();
+    // P
+    {
+        DevBuf<double> dinv;
+        dinv.alloc(n);
+        DevBuf<double> od;
+        od.alloc(n);
+        DevBuf<int> bad;
+        bad.alloc(1);
+        SPFD_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+        k_diag_dinv<<<grid_for(n, T), T, 0, s>>>(av, omega, dinv.get(), od.get(), nullptr, bad.get());
+        DevBuf<int64_t> pcnt;
+        pcnt.alloc(n + 1);
+        SPFD_CUDA(cudaMemsetAsync(pcnt.get() + n, 0, sizeof(int64_t), s));
+        DevBuf<double> pv;
+        DevBuf<int32_t> keep;
+        pv.alloc(AT.nnz); keep.alloc(AT.nnz);
+        k_make_p<<<grid_for(n, T), T, 0, s>>>(view(AT), agg.get(), dinv.get(), omega, pcnt.get(), pv.get(),
+                                              keep.get());
+        DevBuf<int64_t> pptr;
+        pptr.alloc(n + 1);
+        scan_excl(pcnt.get(), pptr.get(), n + 1, s);
+        int64_t pnnz = read1(pptr.get() + n, s);
+        P.alloc(n, n_agg, pnnz);
+        SPFD_CUDA(cudaMemcpyAsync(P.ptr.get(), pptr.get(), (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+        k_compact_rows<<<grid_for(n, T), T, 0, s>>>(view(AT), pv.get(), keep.get(), pptr.get(), P.col.get(),
+                                                    P.val.get());
+        SPFD_LAUNCH_CHECK();
+        SPFD_CUDA(cudaStreamSynchronize(s));
+    }
+    AT = Csr();
+    transpose(view(P), n_agg, R, s);
+    Csr AP;
+    spgemm(av, view(P), n_agg, AP, true, s);
+    spgemm(view(R), view(AP), n_agg, Ac, true, s);
+    (void)L;
+    return true;
+}
+
+}  // namespace
+
+int64_t Amg::device_bytes() const {
+    int64_t b = cinv.bytes() + kx.bytes() + kr.bytes() + kz.bytes() + kp.bytes() + kq.bytes() + kb.bytes() +
+                partials.bytes() + scal.bytes() + fg_basis.bytes() + fg_prec.bytes();
+    for (auto &l : lv)
+        b += l.A.bytes() + l.P.bytes() + l.R.bytes() + l.P_dof.bytes() + l.R_dof.bytes() + l.agg.bytes() +
+             l.dinv.bytes() + l.odinv.bytes() + l.vr.bytes() + l.vx.bytes() + l.vd.bytes() + l.vt.bytes();
+    return b;
+}
+
+void alloc_krylov(Amg &h, int64_t nvec0, int max_nrhs);
+
+static void finish_level(Level &L, const Csr &A, double omega, cudaStream_t s) {
+    const int T = 256;
+    L.dinv.alloc(L.nvec);
+    L.odinv.alloc(L.nvec);
+    DevBuf<int> bad;
+    bad.alloc(1);
+    SPFD_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    k_diag_dinv<<<grid_for(A.rows, T), T, 0, s>>>(view(A), omega, L.dinv.get(), L.odinv.get(), nullptr, bad.get());
+    SPFD_LAUNCH_CHECK();
+    SPFD_CHECK(read1(bad.get(), s) == 0, SPFD_ENOTPOS, "matrix has a non-positive diagonal entry");
+}
+
+static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
+    const int T = 256;
+    cudaEvent_t e0, e1;
+    SPFD_CUDA(cudaEventCreate(&e0));
+    SPFD_CUDA(cudaEventCreate(&e1));
+    SPFD_CUDA(cudaEventRecord(e0, s));
+    auto wall0 = std::chrono::steady_clock::now();
+    h->omega = cfg.jacobi_damping;
+    h->pre = cfg.pre_sweeps;
+    h->post = cfg.post_sweeps;
+    h->max_nrhs = cfg.max_nrhs < 1 ? 1 : (cfg.max_nrhs > 2 ? 2 : cfg.max_nrhs);
+    int R = h->max_nrhs;
+
+    std::vector<Csr> mats;
+    mats.push_back(std::move(A0));
+    h->lv.emplace_back();
+    h->lv[0].n = mats[0].rows;
+    h->lv[0].a_nnz = mats[0].nnz;
+    int depth = 0;
+    while (mats.back().rows > cfg.coarse_cap && (int)h->lv.size() < cfg.max_levels) {
+        Csr Ac, P, Rm;
+        DevBuf<int32_t> agg;
+        double theta = cfg.strength_threshold * std::pow(0.5, depth);
+        bool ok = coarsen(h->lv.back(), mats.back(), theta, h->omega, Ac, P, Rm, agg, s);
+        h->lv.back().agg = std::move(agg);
+        if (!ok) break;
+        h->lv.back().P = std::move(P);
+        h->lv.back().R = std::move(Rm);
+        h->lv.emplace_back();
+        h->lv.back().n = Ac.rows;
+        h->lv.back().a_nnz = Ac.nnz;
+        mats.push_back(std::move(Ac));
+        ++depth;
+    }
+    int nl = (int)h->lv.size();
+    // per-level solve data
+    for (int l = 0; l < nl; ++l) {
+        Level &L = h->lv[l];
+        bool st0 = (l == 0 && h->structured);
+        L.nvec = st0 ? h->op->L : L.n;
+        if (st0) {
+            // dinv / odinv in span layout from the operator's exact diagonal
+            L.dinv.alloc(L.nvec);
+            L.odinv.alloc(L.nvec);
+            SPFD_CUDA(cudaMemcpyAsync(L.dinv.get(), h->op->dinv.get(), L.nvec * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, s));
+            // odinv = omega * dinv computed on the DOF CSR then mapped
+            DevBuf<double> d1, d2;
+            d1.alloc(L.n); d2.alloc(L.n);
+            DevBuf<int> bad;
+            bad.alloc(1);
+            SPFD_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+            k_diag_dinv<<<grid_for(L.n, T), T, 0, s>>>(view(mats[0]), h->omega, d1.get(), d2.get(), nullptr,
+                                                        bad.get());
+            k_dofs_to_span_1<<<grid_for(L.nvec, T), T, 0, s>>>(h->op->pos_to_dof.get(), L.nvec, d2.get(),
+                                                               L.odinv.get());
+            SPFD_LAUNCH_CHECK();
+            if (l < nl - 1) {
+                // P/R in span numbering; keep DOF copies for export
+                Csr &Pd = L.P;
+                Csr &Rd = L.R;
+                Csr Ps, Rs;
+                DevBuf<int64_t> cnt;
+                cnt.alloc(L.nvec + 1);
+                SPFD_CUDA(cudaMemsetAsync(cnt.get() + L.nvec, 0, sizeof(int64_t), s));
+                k_span_rowcnt<<<grid_for(L.nvec, T), T, 0, s>>>(h->op->pos_to_dof.get(), L.nvec, Pd.ptr.get(),
+                                                                cnt.get());
+                Ps.alloc(L.nvec, Pd.cols, Pd.nnz);
+                scan_excl(cnt.get(), Ps.ptr.get(), L.nvec + 1, s);
+                SPFD_CUDA(cudaMemcpyAsync(Ps.col.get(), Pd.col.get(), Pd.nnz * sizeof(int32_t),
+                                          cudaMemcpyDeviceToDevice, s));
+                SPFD_CUDA(cudaMemcpyAsync(Ps.val.get(), Pd.val.get(), Pd.nnz * sizeof(double),
+                                          cudaMemcpyDeviceToDevice, s));
+                Rs.alloc(Rd.rows, L.nvec, Rd.nnz);
+                SPFD_CUDA(cudaMemcpyAsync(Rs.ptr.get(), Rd.ptr.get(), (Rd.rows + 1) * sizeof(int64_t),
+                                          cudaMemcpyDeviceToDevice, s));
+                SPFD_CUDA(cudaMemcpyAsync(Rs.val.get(), Rd.val.get(), Rd.nnz * sizeof(double),
+                                          cudaMemcpyDeviceToDevice, s));
+                if (Rd.nnz)
+                    k_map_cols<<<grid_for(Rd.nnz, T), T, 0, s>>>(Rd.col.get(), Rd.nnz, h->op->dof_to_pos.get(),
+                                                                 Rs.col.get());
+                SPFD_LAUNCH_CHECK();
+                L.P_dof = std::move(L.P);
+                L.R_dof = std::move(L.R);
+                L.P = std::move(Ps);
+                L.R = std::move(Rs);
+            }
+        } else {
+            finish_level(L, mats[l], h->omega, s);
+            L.A = std::move(mats[l]);
+        }
+        if (l < nl - 1) {
+            L.p_group = pick_group(L.P.nnz, L.P.rows);
+            L.r_group = pick_group(L.R.nnz, L.R.rows);
+        }
+        if (!(l == 0 && h->structured)) L.a_group = pick_group(L.A.nnz, L.A.rows);
+        L.vr.alloc(L.nvec * R);
+        L.vx.alloc(L.nvec * R);
+        L.vd.alloc(L.nvec * R);
+        L.vt.alloc(L.nvec * R);
+    }
+    // coarsest dense inverse
+    {
+        Level &C = h->lv[nl - 1];
+        const Csr &Am = (nl - 1 == 0 && h->structured) ? mats[0] : C.A;
+        h->nc = C.n;
+        dense_inverse(Am, h->cinv, s);
+        if (nl - 1 == 0 && h->structured) {
+            // single-level structured hierarchy: keep the DOF CSR
+        }
+    }
+    alloc_krylov(*h, h->lv[0].nvec, R);
+    SPFD_CUDA(cudaEventRecord(e1, s));
+    SPFD_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    SPFD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    (void)wall0;
+    h->setup_seconds = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return h;
+}
+
+Amg *amg_setup_op(Operator *op, const spfd_config &cfg, cudaStream_t s) {
+    auto *h = new Amg();
+    try {
+        h->op = op;
+        h->structured = true;
+        Csr A0;
+        A0.alloc(op->n_dofs, op->n_dofs, op->nnz);
+        op_csr(*op, A0.ptr.get(), A0.col.get(), A0.val.get(), s);
+        return build(h, std::move(A0), cfg, s);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+}
+
+__global__ void k_copy_sorted_rows(int64_t n, const int64_t *ptr, const int32_t *col, const double *val,
+                                   int32_t *ocol, double *oval) {
+    // insertion sort per row (input may be unsorted); rows are short
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b = ptr[r], e = ptr[r + 1];
+        for (int64_t q = b; q < e; ++q) { ocol[q] = col[q]; oval[q] = val[q]; }
+        for (int64_t q = b + 1; q < e; ++q) {
+            int32_t c = ocol[q];
+            double v = oval[q];
+            int64_t t = q - 1;
+            while (t >= b && ocol[t] > c) { ocol[t + 1] = ocol[t]; oval[t + 1] = oval[t]; --t; }
+            ocol[t + 1] = c;
+            oval[t + 1] = v;
+        }
+    }
+}
+
+Amg *amg_setup_csr(int64_t n, int64_t nnz, const int64_t *ptr, const int32_t *col, const double *val,
+                   const spfd_config &cfg, cudaStream_t s) {
+    SPFD_CHECK(n >= 1, SPFD_EINVAL, "matrix must have at least one row");
+    auto *h = new Amg();
+    try {
+        Csr A0;
+        A0.alloc(n, n, nnz);
+        SPFD_CUDA(cudaMemcpyAsync(A0.ptr.get(), ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+        k_copy_sorted_rows<<<grid_for(n, 256), 256, 0, s>>>(n, ptr, col, val, A0.col.get(), A0.val.get());
+        SPFD_LAUNCH_CHECK();
+        return build(h, std::move(A0), cfg, s);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+}
+
+void amg_level_csr(Amg &h, int level, int which, int64_t *ptr, int32_t *col, double *val, cudaStream_t s) {
+    SPFD_CHECK(level >= 0 && level < (int)h.lv.size(), SPFD_EINVAL, "level out of range");
+    Level &L = h.lv[level];
+    const Csr *m = nullptr;
+    if (which == 0) {
+        if (level == 0 && h.structured) {
+            op_csr(*h.op, ptr, col, val, s);
+            return;
+        }
+        m = &L.A;
+    } else if (which == 1) {
+        m = (level == 0 && h.structured) ? &L.P_dof : &L.P;
+    } else if (which == 2) {
+        m = (level == 0 && h.structured) ? &L.R_dof : &L.R;
+    }
+    SPFD_CHECK(m != nullptr && m->rows > 0, SPFD_EINVAL, "no such matrix on this level");
+    SPFD_CUDA(cudaMemcpyAsync(ptr, m->ptr.get(), (m->rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    if (m->nnz) {
+        SPFD_CUDA(cudaMemcpyAsync(col, m->col.get(), m->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        SPFD_CUDA(cudaMemcpyAsync(val, m->val.get(), m->nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    SPFD_CUDA(cudaStreamSynchronize(s));
+}
+
+void amg_level_agg(Amg &h, int level, int32_t *agg, cudaStream_t s) {
+    SPFD_CHECK(level >= 0 && level < (int)h.lv.size(), SPFD_EINVAL, "level out of range");
+    Level &L = h.lv[level];
+    SPFD_CHECK(L.agg.get() != nullptr && L.agg.n >= (size_t)L.n, SPFD_EINVAL, "no aggregates on this level");
+    SPFD_CUDA(cudaMemcpyAsync(agg, L.agg.get(), L.n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace spfd

@@ -1,0 +1,264 @@
+// extern "C" boundary of libspfd_b200.so (include/spfd_b200.h).
+#include <cstring>
+#include <string>
+
+#include "amg.cuh"
+
+struct spfd_op_s {
+    spfd::Operator *op;
+};
+struct spfd_amg_s {
+    spfd::Amg *amg;
+    spfd::Operator *op;  // not owned
+};
+
+namespace spfd {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string &msg) { g_last_error = msg; }
+
+template <class F>
+static int guarded(F &&f) {
+    try {
+        f();
+        return SPFD_OK;
+    } catch (const Error &e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        set_last_error("host allocation failed");
+        return SPFD_ENOMEM;
+    } catch (const std::exception &e) {
+        set_last_error(e.what());
+        return SPFD_ECUDA;
+    }
+}
+
+static inline cudaStream_t S(void *p) { return (cudaStream_t)p; }
+
+}  // namespace spfd
+
+using namespace spfd;
+
+extern "C" {
+
+const char *spfd_last_error(void) { return g_last_error.c_str(); }
+
+const char *spfd_version(void) { return "spfd_b200 0.1 (sm_100a, fp64)"; }
+
+int spfd_op_create(const int64_t *h_dims, const double *h_spacing, const uint16_t *ids, const double *lut,
+                   int64_t lut_len, int pin, void *stream, spfd_op_t *out) {
+    return guarded([&] {
+        SPFD_CHECK(out != nullptr && h_dims != nullptr && h_spacing != nullptr, SPFD_EINVAL, "null argument");
+        Operator *op = op_create(h_dims, h_spacing, ids, lut, lut_len, pin, S(stream));
+        *out = new spfd_op_s{op};
+    });
+}
+
+int spfd_op_destroy(spfd_op_t op) {
+    return guarded([&] {
+        if (!op) return;
+        delete op->op;
+        delete op;
+    });
+}
+
+int spfd_op_info_get(spfd_op_t h, spfd_op_info *info) {
+    return guarded([&] {
+        SPFD_CHECK(h && info, SPFD_EINVAL, "null argument");
+        const Operator &op = *h->op;
+        info->dims[0] = op.nx; info->dims[1] = op.ny; info->dims[2] = op.nz;
+        info->n_nodes = op.n_nodes;
+        info->n_edges = op.n_edges;
+        info->n_dofs = op.n_dofs;
+        info->n_conductive = op.n_cond;
+        info->n_components = op.n_comp;
+        info->n_cond_voxels = op.n_cond_vox;
+        info->nnz = op.nnz;
+        info->span_len = op.L;
+        info->n_rows = op.n_rows;
+        info->device_bytes = op.device_bytes();
+    });
+}
+
+int spfd_op_export(spfd_op_t h, int what, void *dst, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && dst, SPFD_EINVAL, "null argument");
+        op_export(*h->op, what, dst, S(stream));
+    });
+}
+
+int spfd_op_csr(spfd_op_t h, int64_t *indptr, int32_t *indices, double *data, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && indptr && indices && data, SPFD_EINVAL, "null argument");
+        op_csr(*h->op, indptr, indices, data, S(stream));
+    });
+}
+
+int spfd_stencil_apply(spfd_op_t h, const double *x, double *y, int nrhs, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && x && y && (nrhs == 1 || nrhs == 2), SPFD_EINVAL, "bad argument");
+        Operator &op = *h->op;
+        op_dofs_to_span(op, x, op.ws_a.get(), nrhs, S(stream));
+        op_stencil_span(op, op.ws_a.get(), op.ws_b.get(), nrhs, S(stream));
+        op_span_to_dofs(op, op.ws_b.get(), y, nrhs, S(stream));
+    });
+}
+
+int spfd_rhs_assemble(spfd_op_t h, const double *a, double *rhs, int nrhs, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && a && rhs && (nrhs == 1 || nrhs == 2), SPFD_EINVAL, "bad argument");
+        Operator &op = *h->op;
+        op_rhs_span(op, a, op.ws_a.get(), nrhs, S(stream));
+        op_span_to_dofs(op, op.ws_a.get(), rhs, nrhs, S(stream));
+    });
+}
+
+int spfd_edge_voltages(spfd_op_t h, const double *a, const double *psi, double omega, double *v, int nrhs,
+                       void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && a && psi && v && (nrhs == 1 || nrhs == 2), SPFD_EINVAL, "bad argument");
+        Operator &op = *h->op;
+        op_dofs_to_span(op, psi, op.ws_a.get(), nrhs, S(stream));
+        op_edge_voltages(op, a, op.ws_a.get(), omega, v, nrhs, S(stream));
+    });
+}
+
+int spfd_node_field(spfd_op_t h, const double *v, double *node, int nrhs, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && v && node && (nrhs == 1 || nrhs == 2), SPFD_EINVAL, "bad argument");
+        op_node_field(*h->op, v, node, nrhs, S(stream));
+    });
+}
+
+int spfd_voxel_average(spfd_op_t h, const double *node, double *vox, int nrhs, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && node && vox && (nrhs == 1 || nrhs == 2), SPFD_EINVAL, "bad argument");
+        op_voxel_average(*h->op, node, vox, nrhs, S(stream));
+    });
+}
+
+int spfd_efield_voxavg(spfd_op_t h, const double *a, const double *psi, double omega, double *vox, int nrhs,
+                       void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && a && psi && vox && (nrhs == 1 || nrhs == 2), SPFD_EINVAL, "bad argument");
+        Operator &op = *h->op;
+        op_dofs_to_span(op, psi, op.ws_a.get(), nrhs, S(stream));
+        op_efield_voxavg_span(op, a, op.ws_a.get(), omega, vox, op.ws_b.get(), nrhs, S(stream));
+    });
+}
+
+static void check_cfg(const spfd_config *c) {
+    SPFD_CHECK(c != nullptr, SPFD_EINVAL, "null config");
+    SPFD_CHECK(c->rel_tol > 0.0, SPFD_EINVAL, "rel_tol must be positive");
+    SPFD_CHECK(c->restart >= 1, SPFD_EINVAL, "restart must be >= 1");
+    SPFD_CHECK(c->jacobi_damping > 0.0 && c->jacobi_damping <= 1.0, SPFD_EINVAL, "jacobi_damping must be in (0, 1]");
+    SPFD_CHECK(c->max_iters >= 1, SPFD_EINVAL, "max_iters must be >= 1");
+    SPFD_CHECK(c->coarse_cap >= 1 && c->max_levels >= 1, SPFD_EINVAL, "coarse_cap and max_levels must be >= 1");
+}
+
+int spfd_amg_setup_op(spfd_op_t h, const spfd_config *cfg, void *stream, spfd_amg_t *out) {
+    return guarded([&] {
+        SPFD_CHECK(h && out, SPFD_EINVAL, "null argument");
+        check_cfg(cfg);
+        SPFD_CHECK(h->op->n_dofs >= 1, SPFD_EEMPTY, "empty Poisson system");
+        Amg *a = amg_setup_op(h->op, *cfg, S(stream));
+        *out = new spfd_amg_s{a, h->op};
+    });
+}
+
+int spfd_amg_setup_csr(int64_t n, int64_t nnz, const int64_t *indptr, const int32_t *indices, const double *data,
+                       const spfd_config *cfg, void *stream, spfd_amg_t *out) {
+    return guarded([&] {
+        SPFD_CHECK(out && indptr && (nnz == 0 || (indices && data)), SPFD_EINVAL, "null argument");
+        check_cfg(cfg);
+        Amg *a = amg_setup_csr(n, nnz, indptr, indices, data, *cfg, S(stream));
+        *out = new spfd_amg_s{a, nullptr};
+    });
+}
+
+int spfd_amg_destroy(spfd_amg_t h) {
+    return guarded([&] {
+        if (!h) return;
+        delete h->amg;
+        delete h;
+    });
+}
+
+int spfd_amg_info_get(spfd_amg_t h, spfd_amg_info *info) {
+    return guarded([&] {
+        SPFD_CHECK(h && info, SPFD_EINVAL, "null argument");
+        Amg &a = *h->amg;
+        std::memset(info, 0, sizeof(*info));
+        info->n_levels = (int32_t)a.lv.size();
+        SPFD_CHECK(a.lv.size() <= 32, SPFD_EINVAL, "too many levels for the info struct");
+        for (size_t l = 0; l < a.lv.size(); ++l) {
+            info->level_rows[l] = a.lv[l].n;
+            info->level_nnz[l] = a.lv[l].a_nnz;
+            const Csr &P = (l == 0 && a.structured) ? a.lv[l].P_dof : a.lv[l].P;
+            info->prolong_nnz[l] = P.nnz;
+        }
+        info->setup_seconds = a.setup_seconds;
+        info->device_bytes = a.device_bytes();
+        info->structured = a.structured ? 1 : 0;
+    });
+}
+
+int spfd_amg_level_csr(spfd_amg_t h, int level, int which, int64_t *indptr, int32_t *indices, double *data,
+                       void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && indptr, SPFD_EINVAL, "null argument");
+        amg_level_csr(*h->amg, level, which, indptr, indices, data, S(stream));
+    });
+}
+
+int spfd_amg_level_agg(spfd_amg_t h, int level, int32_t *agg, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && agg, SPFD_EINVAL, "null argument");
+        amg_level_agg(*h->amg, level, agg, S(stream));
+    });
+}
+
+int spfd_vcycle(spfd_amg_t h, const double *r, double *z, int nrhs, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && r && z && nrhs >= 1 && nrhs <= h->amg->max_nrhs, SPFD_EINVAL, "bad argument");
+        Amg &a = *h->amg;
+        amg_to_level0(a, r, a.kb.get(), nrhs, S(stream));
+        amg_vcycle(a, a.kb.get(), a.kz.get(), nrhs, S(stream));
+        amg_from_level0(a, a.kz.get(), z, nrhs, S(stream));
+    });
+}
+
+int spfd_solve(spfd_amg_t h, const double *b, double *x, int nrhs, const spfd_config *cfg, spfd_report *rep,
+               double *h_trace, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && b && x && rep && nrhs >= 1 && nrhs <= h->amg->max_nrhs, SPFD_EINVAL, "bad argument");
+        check_cfg(cfg);
+        Amg &a = *h->amg;
+        amg_to_level0(a, b, a.kb.get(), nrhs, S(stream));
+        *rep = krylov_solve(a, a.kb.get(), a.kx.get(), nrhs, *cfg, h_trace, S(stream));
+        amg_from_level0(a, a.kx.get(), x, nrhs, S(stream));
+        SPFD_CUDA(cudaStreamSynchronize(S(stream)));
+        if (rep->status == SPFD_ENONFINITE) throw Error(SPFD_ENONFINITE, "non-finite value in the Krylov iteration");
+    });
+}
+
+int spfd_snapshot(spfd_op_t hop, spfd_amg_t h, const double *a, double omega, double *psi, double *vox, int nrhs,
+                  const spfd_config *cfg, spfd_report *rep, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(hop && h && a && vox && rep && h->op == hop->op, SPFD_EINVAL, "bad argument");
+        SPFD_CHECK(nrhs >= 1 && nrhs <= h->amg->max_nrhs, SPFD_EINVAL, "nrhs exceeds the hierarchy workspace");
+        check_cfg(cfg);
+        Amg &m = *h->amg;
+        Operator &op = *hop->op;
+        // rhs straight into the span layout, solve, fused E-field from the span iterate
+        op_rhs_span(op, a, m.kb.get(), nrhs, S(stream));
+        *rep = krylov_solve(m, m.kb.get(), m.kx.get(), nrhs, *cfg, nullptr, S(stream));
+        if (rep->status == SPFD_ENONFINITE) throw Error(SPFD_ENONFINITE, "non-finite value in the Krylov iteration");
+        op_efield_voxavg_span(op, a, m.kx.get(), omega, vox, op.ws_b.get(), nrhs, S(stream));
+        if (psi) op_span_to_dofs(op, m.kx.get(), psi, nrhs, S(stream));
+        SPFD_CUDA(cudaStreamSynchronize(S(stream)));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Shared helpers for the spfd_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/spfd_b200.h"
+
+namespace spfd {
+
+// ---------------------------------------------------------------- errors --
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string &msg);
+
+#define SPFD_CUDA(expr)                                                        \
+    do {                                                                       \
+        cudaError_t _e = (expr);                                               \
+        if (_e != cudaSuccess)                                                 \
+            throw ::spfd::Error(SPFD_ECUDA, std::string(#expr) + ": " +        \
+                                                cudaGetErrorString(_e));       \
+    } while (0)
+
+#define SPFD_CHECK(cond, code, msg)                                            \
+    do {                                                                       \
+        if (!(cond)) throw ::spfd::Error((code), (msg));                       \
+    } while (0)
+
+#define SPFD_LAUNCH_CHECK() SPFD_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------- device buffers --
+// RAII device allocation (stream-ordered).  Handles own their buffers; the
+// Python side owns every input/output tensor.
+template <class T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf &operator=(DevBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count == 0) count = 1;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e != cudaSuccess) {
+            p = nullptr;
+            throw Error(SPFD_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+        }
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+    T *get() const { return p; }
+};
+
+// int32 -> int64 widening functor for CUB scans over int32 counts
+struct WidenI32 {
+    __host__ __device__ int64_t operator()(int v) const { return (int64_t)v; }
+};
+struct RootFlag {  // operator construction: bit 2 marks a component root
+    __host__ __device__ uint8_t operator()(uint8_t f) const { return (f & 2) ? 1 : 0; }
+};
+
+inline int grid_for(int64_t n, int threads, int cap = 148 * 16) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+// ---------------------------------------------- exact (no-FMA) arithmetic --
+// The reference computes with numpy/scipy (no fused multiply-add); the bit-
+// exact kernels use explicitly rounded ops so nvcc cannot contract them.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+// ---------------------------------------------- deterministic reductions --
+// Block-level sum of K values per thread in a FIXED tree order (xor-shuffle
+// within warps, then warp 0 over the per-warp partials).  Result valid in
+// thread 0.  No atomics: the order depends only on blockDim.
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double *smem /* [32*K] */) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) smem[warp * K + k] = v[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double t = lane < nwarps ? smem[lane * K + k] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            v[k] = t;
+        }
+    }
+    __syncthreads();
+}
+
+}  // namespace spfd

@@ -1,0 +1,784 @@
+// V-cycle (linsolve.py:179-197), PCG and FGMRES(m) (linsolve.py:200-298)
+// on device.  Level 0 is either the matrix-free stencil in the span layout
+// or a CSR; coarse levels are CSR; the coarsest level applies the dense
+// inverse.  All reductions are two-stage with a fixed order (per-CTA
+// partials, then one CTA summing the partials in index order): repeated
+// solves are bitwise identical (test_linsolve.py:157-166).
+#include <chrono>
+#include <cmath>
+
+#include "amg.cuh"
+
+namespace spfd {
+
+namespace {
+
+constexpr int kDotGrid = 148 * 4;
+constexpr int kDotThreads = 256;
+
+// device scalar slots (per rhs k)
+enum {
+    S_RHO = 0, S_PQ = 2, S_RR = 4, S_ALPHA = 6, S_BETA = 8, S_BB = 10, S_RZ = 12, S_ACTIVE = 14,
+    S_TMP = 16, S_H = 32  // FGMRES Hessenberg column / scratch from S_H
+};
+
+__device__ __forceinline__ bool mbit(const uint32_t *m, int64_t p) { return (m[p >> 5] >> (p & 31)) & 1u; }
+
+__device__ __forceinline__ int spos(const int4 *rows, int r, int i) {
+    int4 q = rows[r];
+    return (i >= q.y && i < q.z) ? q.x + (i - q.y) : -1;
+}
+
+__device__ __forceinline__ int frow(const int4 *rows, int r0, int r1, int p) {
+    int lo = r0, hi = r1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (rows[mid].x <= p) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Stencil product at position p with the input given by a functor X(pos, c)
+// (so x = odinv*r or z + beta*p can be formed on the fly at the neighbours).
+// Sum order is the reference's sorted-column order.
+template <int R, class X>
+__device__ __forceinline__ void stencil_at(const SpanView &v, int p, int r, int i, int4 q, X xat, double (&s)[R]) {
+    int j = r % v.NY;
+    double wxp = v.wx[p], wyp = v.wy[p], wzp = v.wz[p];
+    double wxm = 0.0, wym = 0.0, wzm = 0.0;
+    int pxm = -1, pym = -1, pzm = -1, pxp = -1, pyp = -1, pzp = -1;
+    if (i > q.y) { pxm = p - 1; wxm = v.wx[pxm]; }
+    if (i + 1 < q.z) pxp = p + 1;
+    if (j > 0) { pym = spos(v.rows, r - 1, i); if (pym >= 0) wym = v.wy[pym]; }
+    if (j + 1 < v.NY) pyp = spos(v.rows, r + 1, i);
+    if (r >= v.NY) { pzm = spos(v.rows, r - v.NY, i); if (pzm >= 0) wzm = v.wz[pzm]; }
+    if (r + v.NY < v.n_rows) pzp = spos(v.rows, r + v.NY, i);
+    double d = add_rn(add_rn(add_rn(add_rn(add_rn(wxp, wyp), wzp), wxm), wym), wzm);
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+        double a = 0.0;
+        if (pzm >= 0) a = add_rn(a, mul_rn(-wzm, xat(pzm, c)));
+        if (pym >= 0) a = add_rn(a, mul_rn(-wym, xat(pym, c)));
+        if (pxm >= 0) a = add_rn(a, mul_rn(-wxm, xat(pxm, c)));
+        a = add_rn(a, mul_rn(d, xat(p, c)));
+        if (pxp >= 0) a = add_rn(a, mul_rn(-wxp, xat(pxp, c)));
+        if (pyp >= 0) a = add_rn(a, mul_rn(-wyp, xat(pyp, c)));
+        if (pzp >= 0) a = add_rn(a, mul_rn(-wzp, xat(pzp, c)));
+        s[c] = a;
+    }
+}
+
+struct ArrX {
+    const double *x;
+    int R;
+    __device__ double operator()(int p, int c) const { return x[(int64_t)p * R + c]; }
+};
+struct ScaledX {  // odinv * r
+    const double *od, *r;
+    int R;
+    __device__ double operator()(int p, int c) const { return od[p] * r[(int64_t)p * R + c]; }
+};
+
+// ---- span (structured level 0) kernels --------------------------------
+// MODE 0: y = A x (+ partial x.y if DOT)
+// MODE 1: y = r - A x
+// MODE 2: y = r - A (odinv r)
+// MODE 3: y = x + odinv (r - A x) (+ partial r.y if DOT)
+template <int R, int MODE, bool DOT>
+__global__ void __launch_bounds__(kSpanThreads) k_span(SpanView v, const double *__restrict__ x,
+                                                       const double *__restrict__ r,
+                                                       const double *__restrict__ od, double *__restrict__ y,
+                                                       double *__restrict__ partials) {
+    __shared__ double red[32 * R];
+    int t = blockIdx.x;
+    int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
+    double dot[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) dot[c] = 0.0;
+#pragma unroll
+    for (int u = 0; u < kTile / kSpanThreads; ++u) {
+        int p = t * kTile + u * kSpanThreads + threadIdx.x;
+        if (p < v.L) {
+            int row = frow(v.rows, r0, r1, p);
+            int4 q = v.rows[row];
+            int i = q.y + (p - q.x);
+            double s[R];
+            if (MODE == 2) stencil_at<R>(v, p, row, i, q, ScaledX{od, r, R}, s);
+            else stencil_at<R>(v, p, row, i, q, ArrX{x, R}, s);
+            bool dof = mbit(v.mask, p);
+#pragma unroll
+            for (int c = 0; c < R; ++c) {
+                double out;
+                int64_t e = (int64_t)p * R + c;
+                if (MODE == 0) out = s[c];
+                else if (MODE == 1 || MODE == 2) out = r[e] - s[c];
+                else out = x[e] + od[p] * (r[e] - s[c]);
+                out = dof ? out : 0.0;
+                y[e] = out;
+                if (DOT) {
+                    if (MODE == 0) dot[c] += x[e] * out;
+                    else if (MODE == 3) dot[c] += r[e] * out;
+                    else dot[c] += out * out;
+                }
+            }
+        }
+    }
+    if (DOT) {
+        block_sum<R>(dot, red);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int c = 0; c < R; ++c) partials[blockIdx.x * R + c] = dot[c];
+    }
+}
+
+// ---- CSR kernels (G lanes per row) ------------------------------------
+// MODE 0: y = M x;  1: y = r - M x;  2: y = r - M(odinv r);
+// MODE 3: y = x + odinv (r - M x);  4: y = odinv r + M e (prolongation, x=e)
+// MODE 5: y = base + M e (prolongation on a materialised smoother iterate)
+template <int G, int R, int MODE, bool DOT>
+__global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__restrict__ r,
+                      const double *__restrict__ od, const double *__restrict__ base, double *__restrict__ y,
+                      double *__restrict__ partials) {
+    __shared__ double red[32 * R];
+    const int lane = threadIdx.x % G;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int GPW = 32 / G;  // row groups per warp
+    double dot[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) dot[c] = 0.0;
+    // warp-uniform trip count so the full-mask shuffles below are safe
+    for (int64_t rbase = warp * GPW; rbase < m.rows; rbase += nwarp * GPW) {
+        const int64_t row = rbase + (threadIdx.x & 31) / G;
+        const bool valid = row < m.rows;
+        double acc[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) acc[c] = 0.0;
+        if (valid) {
+            for (int64_t q = m.ptr[row] + lane; q < m.ptr[row + 1]; q += G) {
+                int col = m.col[q];
+                double a = m.val[q];
+#pragma unroll
+                for (int c = 0; c < R; ++c) {
+                    double xv = MODE == 2 ? od[col] * r[(int64_t)col * R + c] : x[(int64_t)col * R + c];
+                    acc[c] = fma(a, xv, acc[c]);
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < R; ++c)
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o, G);
+        if (valid && lane == 0) {
+#pragma unroll
+            for (int c = 0; c < R; ++c) {
+                int64_t e = row * R + c;
+                double out;
+                if (MODE == 0) out = acc[c];
+                else if (MODE == 1 || MODE == 2) out = r[e] - acc[c];
+                else if (MODE == 3) out = x[e] + od[row] * (r[e] - acc[c]);
+                else if (MODE == 4) out = od[row] * r[e] + acc[c];
+                else out = base[e] + acc[c];
+                y[e] = out;
+                if (DOT) {
+                    if (MODE == 0) dot[c] += x[e] * out;
+                    else if (MODE == 3) dot[c] += r[e] * out;
+                    else dot[c] += out * out;
+                }
+            }
+        }
+    }
+    if (DOT) {
+        block_sum<R>(dot, red);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int c = 0; c < R; ++c) partials[blockIdx.x * R + c] = dot[c];
+    }
+}
+
+constexpr int kCsrThreads = 256;
+inline int csr_grid(int64_t rows, int G) {
+    int64_t groups = (int64_t)kCsrThreads / G;
+    int64_t g = (rows + groups - 1) / groups;
+    if (g < 1) g = 1;
+    if (g > 148 * 16) g = 148 * 16;
+    return (int)g;
+}
+
+template <int G, int R, int MODE, bool DOT>
+void launch_csr_g(const Csr &m, const double *x, const double *r, const double *od, const double *base, double *y,
+                  double *partials, cudaStream_t s, int grid) {
+    k_csr<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials);
+}
+
+template <int R, int MODE, bool DOT>
+int launch_csr(const Csr &m, int G, const double *x, const double *r, const double *od, const double *base,
+               double *y, double *partials, cudaStream_t s) {
+    int grid = csr_grid(m.rows, G);
+    switch (G) {
+        case 4: launch_csr_g<4, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid); break;
+        case 8: launch_csr_g<8, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid); break;
+        case 16: launch_csr_g<16, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid); break;
+        default: launch_csr_g<32, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid); break;
+    }
+    SPFD_LAUNCH_CHECK();
+    return grid;
+}
+
+// dense coarsest solve z = Cinv r (one warp per row)
+template <int R>
+__global__ void k_dense_mv(const double *cinv, int64_t n, const double *r, double *z) {
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    for (int64_t row = warp; row < n; row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double acc[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) acc[c] = 0.0;
+        for (int64_t j = lane; j < n; j += 32) {
+            double a = cinv[row * n + j];
+#pragma unroll
+            for (int c = 0; c < R; ++c) acc[c] = fma(a, r[j * R + c], acc[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < R; ++c)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+        if (lane == 0)
+#pragma unroll
+            for (int c = 0; c < R; ++c) z[row * R + c] = acc[c];
+    }
+}
+
+// ---- elementwise / BLAS-1 ----------------------------------------------
+template <int R>
+__global__ void k_odinv_r(int64_t n, const double *od, const double *r, double *x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int c = 0; c < R; ++c) x[i * R + c] = od[i] * r[i * R + c];
+}
+
+// partial a.b per rhs (fixed grid)
+template <int R>
+__global__ void k_dot(int64_t n, const double *a, const double *b, double *partials) {
+    __shared__ double red[32 * R];
+    double d[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) d[c] = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int c = 0; c < R; ++c) d[c] = fma(a[i * R + c], b[i * R + c], d[c]);
+    block_sum<R>(d, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int c = 0; c < R; ++c) partials[blockIdx.x * R + c] = d[c];
+}
+
+// x += alpha p ; r -= alpha q ; partial r.r
+template <int R>
+__global__ void k_update_xr(int64_t n, const double *scal, double *x, double *r, const double *p, const double *q,
+                            double *partials) {
+    __shared__ double red[32 * R];
+    double a[R], d[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) { a[c] = scal[S_ALPHA + c]; d[c] = 0.0; }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            int64_t e = i * R + c;
+            x[e] = fma(a[c], p[e], x[e]);
+            double rv = fma(-a[c], q[e], r[e]);
+            r[e] = rv;
+            d[c] = fma(rv, rv, d[c]);
+        }
+    block_sum<R>(d, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int c = 0; c < R; ++c) partials[blockIdx.x * R + c] = d[c];
+}
+
+// p = z + beta p
+template <int R>
+__global__ void k_xpby(int64_t n, const double *scal, const double *z, double *p) {
+    double b[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) b[c] = scal[S_BETA + c];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int c = 0; c < R; ++c) p[i * R + c] = fma(b[c], p[i * R + c], z[i * R + c]);
+}
+
+// Sum per-CTA partials in index order; then apply `what`.
+enum { F_STORE = 0, F_ALPHA = 1, F_BETA_INIT = 2, F_BETA = 3 };
+template <int R>
+__global__ void k_finalize(const double *partials, int nblocks, double *scal, int slot, int what, double tol) {
+    __shared__ double red[32 * R];
+    double s[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) s[c] = 0.0;
+    // each thread sums a contiguous stripe sequentially, then a fixed tree
+    int per = (nblocks + blockDim.x - 1) / blockDim.x;
+    int b0 = threadIdx.x * per, b1 = min(nblocks, b0 + per);
+    for (int b = b0; b < b1; ++b)
+#pragma unroll
+        for (int c = 0; c < R; ++c) s[c] += partials[b * R + c];
+    block_sum<R>(s, red);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            scal[slot + c] = s[c];
+            bool active = scal[S_ACTIVE + c] != 0.0;
+            if (what == F_ALPHA) {
+                double pq = s[c];
+                scal[S_ALPHA + c] = (active && pq != 0.0) ? scal[S_RHO + c] / pq : 0.0;
+            } else if (what == F_BETA_INIT) {
+                scal[S_RHO + c] = s[c];
+                scal[S_BETA + c] = 0.0;
+            } else if (what == F_BETA) {
+                double old = scal[S_RHO + c];
+                scal[S_BETA + c] = (active && old != 0.0) ? s[c] / old : 0.0;
+                scal[S_RHO + c] = s[c];
+            }
+        }
+        (void)tol;
+    }
+}
+
+__global__ void k_set_active(double *scal, int R, double tol) {
+    for (int c = 0; c < R; ++c) {
+        double bb = scal[S_BB + c], rr = scal[S_RR + c];
+        bool conv = bb == 0.0 || sqrt(rr) <= tol * sqrt(bb);
+        scal[S_ACTIVE + c] = conv ? 0.0 : 1.0;
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------
+// level-0 layout conversions
+// ------------------------------------------------------------------------
+
+__global__ void k_interleave(int64_t n, int R, const double *planar, double *inter) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        for (int c = 0; c < R; ++c) inter[i * R + c] = planar[c * n + i];
+}
+__global__ void k_deinterleave(int64_t n, int R, const double *inter, double *planar) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        for (int c = 0; c < R; ++c) planar[c * n + i] = inter[i * R + c];
+}
+
+void amg_to_level0(Amg &h, const double *planar, double *inter, int nrhs, cudaStream_t s) {
+    if (h.structured) op_dofs_to_span(*h.op, planar, inter, nrhs, s);
+    else {
+        k_interleave<<<grid_for(h.lv[0].n, 256, 148 * 16), 256, 0, s>>>(h.lv[0].n, nrhs, planar, inter);
+        SPFD_LAUNCH_CHECK();
+    }
+}
+
+void amg_from_level0(Amg &h, const double *inter, double *planar, int nrhs, cudaStream_t s) {
+    if (h.structured) op_span_to_dofs(*h.op, inter, planar, nrhs, s);
+    else {
+        k_deinterleave<<<grid_for(h.lv[0].n, 256, 148 * 16), 256, 0, s>>>(h.lv[0].n, nrhs, inter, planar);
+        SPFD_LAUNCH_CHECK();
+    }
+}
+
+void alloc_krylov(Amg &h, int64_t nvec0, int R) {
+    int64_t n = nvec0 * R;
+    h.kx.alloc(n); h.kr.alloc(n); h.kz.alloc(n); h.kp.alloc(n); h.kq.alloc(n); h.kb.alloc(n);
+    int64_t np = kDotGrid;
+    if (h.structured) np = std::max<int64_t>(np, h.op->n_tiles);
+    np = std::max<int64_t>(np, 148 * 16);
+    h.partials.alloc(np * 2 + 64);
+    h.scal.alloc(S_H + 256);
+}
+
+// ------------------------------------------------------------------------
+// level-0 operator application and the V-cycle
+// ------------------------------------------------------------------------
+
+namespace {
+
+// returns number of partial blocks written when DOT
+template <int R>
+int level0_apply(Amg &h, int mode, bool dot, const double *x, const double *r, double *y, cudaStream_t s) {
+    Level &L = h.lv[0];
+    double *part = h.partials.get();
+    if (h.structured) {
+        SpanView v = span_view(*h.op);
+        int g = (int)h.op->n_tiles;
+        if (g == 0) return 0;
+        const double *od = L.odinv.get();
+        if (mode == 0) {
+            if (dot) k_span<R, 0, true><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+            else k_span<R, 0, false><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+        } else if (mode == 1) {
+            if (dot) k_span<R, 1, true><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+            else k_span<R, 1, false><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+        } else if (mode == 2) {
+            k_span<R, 2, false><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+        } else {
+            if (dot) k_span<R, 3, true><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+            else k_span<R, 3, false><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+        }
+        SPFD_LAUNCH_CHECK();
+        return g;
+    }
+    const double *od = L.odinv.get();
+    switch (mode) {
+        case 0: return dot ? launch_csr<R, 0, true>(L.A, L.a_group, x, r, od, nullptr, y, part, s)
+                           : launch_csr<R, 0, false>(L.A, L.a_group, x, r, od, nullptr, y, part, s);
+        case 1: return dot ? launch_csr<R, 1, true>(L.A, L.a_group, x, r, od, nullptr, y, part, s)
+                           : launch_csr<R, 1, false>(L.A, L.a_group, x, r, od, nullptr, y, part, s);
+        case 2: return launch_csr<R, 2, false>(L.A, L.a_group, x, r, od, nullptr, y, part, s);
+        default: return dot ? launch_csr<R, 3, true>(L.A, L.a_group, x, r, od, nullptr, y, part, s)
+                            : launch_csr<R, 3, false>(L.A, L.a_group, x, r, od, nullptr, y, part, s);
+    }
+}
+
+// smoother/residual on level l (l > 0 or CSR level 0)
+template <int R>
+void level_apply(Amg &h, int l, int mode, const double *x, const double *r, double *y, cudaStream_t s) {
+    if (l == 0) { level0_apply<R>(h, mode, false, x, r, y, s); return; }
+    Level &L = h.lv[l];
+    const double *od = L.odinv.get();
+    switch (mode) {
+        case 1: launch_csr<R, 1, false>(L.A, L.a_group, x, r, od, nullptr, y, nullptr, s); break;
+        case 2: launch_csr<R, 2, false>(L.A, L.a_group, x, r, od, nullptr, y, nullptr, s); break;
+        default: launch_csr<R, 3, false>(L.A, L.a_group, x, r, od, nullptr, y, nullptr, s); break;
+    }
+}
+
+template <int R>
+void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
+    int nl = (int)h.lv.size();
+    Level &L = h.lv[l];
+    if (l == nl - 1) {
+        k_dense_mv<R><<<grid_for(h.nc * 32, 256, 148 * 8), 256, 0, s>>>(h.cinv.get(), h.nc, r, z);
+        SPFD_LAUNCH_CHECK();
+        return;
+    }
+    double *d = L.vd.get(), *t = L.vt.get();
+    const size_t bytes = (size_t)L.nvec * R * sizeof(double);
+    const double *xbase = nullptr;  // materialised pre-smoothed iterate (pre >= 2)
+    if (h.pre <= 1) {
+        // implicit first sweep x = omega D^-1 r, defect d = r - A x (linsolve.py:190-193)
+        level_apply<R>(h, l, 2, nullptr, r, d, s);
+    } else {
+        k_odinv_r<R><<<grid_for(L.nvec, 256, 148 * 16), 256, 0, s>>>(L.nvec, L.odinv.get(), r, t);
+        for (int it = 1; it < h.pre; ++it) {
+            level_apply<R>(h, l, 3, t, r, d, s);
+            SPFD_CUDA(cudaMemcpyAsync(t, d, bytes, cudaMemcpyDeviceToDevice, s));
+        }
+        level_apply<R>(h, l, 1, t, r, d, s);
+        xbase = t;
+    }
+    Level &C = h.lv[l + 1];
+    launch_csr<R, 0, false>(L.R, L.r_group, d, nullptr, nullptr, nullptr, C.vr.get(), nullptr, s);
+    vcycle_level<R>(h, l + 1, C.vr.get(), C.vx.get(), s);
+    // x1 = x + P e (linsolve.py:194) -> d
+    if (xbase) launch_csr<R, 5, false>(L.P, L.p_group, C.vx.get(), r, L.odinv.get(), xbase, d, nullptr, s);
+    else launch_csr<R, 4, false>(L.P, L.p_group, C.vx.get(), r, L.odinv.get(), nullptr, d, nullptr, s);
+    if (h.post == 0) {
+        SPFD_CUDA(cudaMemcpyAsync(z, d, bytes, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    // post sweeps x += omega D^-1 (r - A x) (linsolve.py:195-196), last one lands in z
+    const double *cur = d;
+    for (int it = 0; it < h.post; ++it) {
+        double *dst = (it == h.post - 1) ? z : (cur == d ? t : d);
+        level_apply<R>(h, l, 3, cur, r, dst, s);
+        cur = dst;
+    }
+}
+
+}  // namespace
+
+void amg_vcycle(Amg &h, const double *r, double *z, int nrhs, cudaStream_t s) {
+    if (nrhs == 1) vcycle_level<1>(h, 0, r, z, s);
+    else vcycle_level<2>(h, 0, r, z, s);
+}
+
+// ------------------------------------------------------------------------
+// PCG
+// ------------------------------------------------------------------------
+
+namespace {
+
+template <int R>
+void finalize(Amg &h, int nblocks, int slot, int what, cudaStream_t s) {
+    k_finalize<R><<<1, 256, 0, s>>>(h.partials.get(), nblocks, h.scal.get(), slot, what, 0.0);
+    SPFD_LAUNCH_CHECK();
+}
+
+template <int R>
+void dot(Amg &h, int64_t n, const double *a, const double *b, int slot, int what, cudaStream_t s) {
+    k_dot<R><<<kDotGrid, kDotThreads, 0, s>>>(n, a, b, h.partials.get());
+    SPFD_LAUNCH_CHECK();
+    finalize<R>(h, kDotGrid, slot, what, s);
+}
+
+template <int R>
+spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, double *h_trace, cudaStream_t s) {
+    spfd_report rep{};
+    int64_t n = h.lv[0].nvec;
+    double *r = h.kr.get(), *z = h.kz.get(), *p = h.kp.get(), *q = h.kq.get();
+    double *sc = h.scal.get();
+    SPFD_CUDA(cudaMemsetAsync(x, 0, n * R * sizeof(double), s));
+    SPFD_CUDA(cudaMemsetAsync(sc, 0, (S_H) * sizeof(double), s));
+    double ones[2] = {1.0, 1.0};
+    SPFD_CUDA(cudaMemcpyAsync(sc + S_ACTIVE, ones, R * sizeof(double), cudaMemcpyHostToDevice, s));
+    dot<R>(h, n, b, b, S_BB, F_STORE, s);
+    double hs[S_H];
+    SPFD_CUDA(cudaMemcpyAsync(hs, sc, S_H * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    double bnorm[2] = {std::sqrt(hs[S_BB]), R > 1 ? std::sqrt(hs[S_BB + 1]) : 0.0};
+    for (int c = 0; c < R; ++c)
+        if (!std::isfinite(bnorm[c])) { rep.status = SPFD_ENONFINITE; return rep; }
+    bool all_zero = true;
+    for (int c = 0; c < R; ++c) all_zero = all_zero && bnorm[c] == 0.0;
+    if (all_zero) { rep.converged = 1; return rep; }
+
+    int it = 0;
+    bool restart = true;
+    double tol = cfg.rel_tol;
+    while (true) {
+        if (restart) {
+            // r = b - A x ; z = M r ; rho = r.z ; p = z
+            level0_apply<R>(h, 1, false, x, b, r, s);
+            SPFD_CUDA(cudaMemcpyAsync(sc + S_ACTIVE, ones, R * sizeof(double), cudaMemcpyHostToDevice, s));
+            amg_vcycle(h, r, z, R, s);
+            dot<R>(h, n, r, z, S_RZ, F_BETA_INIT, s);
+            SPFD_CUDA(cudaMemcpyAsync(p, z, n * R * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            restart = false;
+        }
+        if (it >= cfg.max_iters) break;
+        int g = level0_apply<R>(h, 0, true, p, nullptr, q, s);  // q = A p, p.q
+        finalize<R>(h, g, S_PQ, F_ALPHA, s);
+        k_update_xr<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, x, r, p, q, h.partials.get());
+        SPFD_LAUNCH_CHECK();
+        finalize<R>(h, kDotGrid, S_RR, F_STORE, s);
+        k_set_active<<<1, 1, 0, s>>>(sc, R, tol);
+        SPFD_CUDA(cudaMemcpyAsync(hs, sc, S_H * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPFD_CUDA(cudaStreamSynchronize(s));
+        ++it;
+        bool done = true;
+        for (int c = 0; c < R; ++c) {
+            double est = bnorm[c] > 0 ? std::sqrt(hs[S_RR + c]) / bnorm[c] : 0.0;
+            if (!std::isfinite(est)) { rep.status = SPFD_ENONFINITE; rep.iterations = it; return rep; }
+            if (h_trace && it <= cfg.max_iters) h_trace[(int64_t)(it - 1) * R + c] = est;
+            if (est > tol) done = false;
+        }
+        if (done || it >= cfg.max_iters) {
+            // true residual check (linsolve.py:296-298 semantics)
+            int gt = level0_apply<R>(h, 1, true, x, b, q, s);
+            finalize<R>(h, gt, S_TMP, F_STORE, s);
+            SPFD_CUDA(cudaMemcpyAsync(hs, sc, S_H * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SPFD_CUDA(cudaStreamSynchronize(s));
+            bool ok = true;
+            for (int c = 0; c < R; ++c) {
+                double rel = bnorm[c] > 0 ? std::sqrt(hs[S_TMP + c]) / bnorm[c] : 0.0;
+                rep.rel_residual[c] = rel;
+                if (!(rel <= tol)) ok = false;
+            }
+            if (ok || it >= cfg.max_iters) {
+                rep.converged = ok ? 1 : 0;
+                break;
+            }
+            restart = true;  // recursive residual drifted: restart from the true residual
+            continue;
+        }
+        amg_vcycle(h, r, z, R, s);
+        dot<R>(h, n, r, z, S_RZ, F_BETA, s);
+        k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p);
+        SPFD_LAUNCH_CHECK();
+    }
+    rep.iterations = it;
+    return rep;
+}
+
+}  // namespace
+
+// level-0 interleaved helpers used by FGMRES (R = 1)
+namespace {
+
+__global__ void k_axpy_dev(int64_t n, const double *coef, double sign, const double *x, double *y) {
+    double a = sign * (*coef);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = fma(a, x[i], y[i]);
+}
+__global__ void k_scale_inv(int64_t n, const double *norm2, const double *x, double *y) {
+    double inv = 1.0 / sqrt(*norm2);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = x[i] * inv;
+}
+__global__ void k_gather_col(int64_t n, int R, int c, const double *inter, double *one) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        one[i] = inter[i * R + c];
+}
+__global__ void k_scatter_col(int64_t n, int R, int c, const double *one, double *inter) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        inter[i * R + c] = one[i];
+}
+__global__ void k_combine(int64_t n, int j, const double *y, const double *zb, double *x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int k = 0; k < j; ++k) acc += zb[(int64_t)k * n + i] * y[k];
+        x[i] += acc;
+    }
+}
+
+// FGMRES(m) for one rhs in R=1 layout (linsolve.py:200-298).
+spfd_report fgmres1(Amg &h, const double *b, double *x, const spfd_config &cfg, double *h_trace, cudaStream_t s) {
+    spfd_report rep{};
+    int64_t n = h.lv[0].nvec;
+    int m = cfg.restart;
+    SPFD_CHECK(m >= 1 && m <= 200, SPFD_EINVAL, "restart must be in [1, 200]");
+    if (h.fg_m < m) {
+        h.fg_basis.alloc((int64_t)(m + 1) * n);
+        h.fg_prec.alloc((int64_t)m * n);
+        h.fg_m = m;
+    }
+    double *V = h.fg_basis.get(), *Z = h.fg_prec.get();
+    double *w = h.kq.get(), *r = h.kr.get();
+    double *sc = h.scal.get();
+    const int G = grid_for(n, 256, 148 * 16);
+    SPFD_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+    SPFD_CUDA(cudaMemsetAsync(sc, 0, (S_H + 64) * sizeof(double), s));
+    double one = 1.0;
+    SPFD_CUDA(cudaMemcpyAsync(sc + S_ACTIVE, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+    dot<1>(h, n, b, b, S_BB, F_STORE, s);
+    double hb;
+    SPFD_CUDA(cudaMemcpyAsync(&hb, sc + S_BB, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    double bnorm = std::sqrt(hb);
+    if (!std::isfinite(bnorm)) { rep.status = SPFD_ENONFINITE; return rep; }
+    if (bnorm == 0.0) { rep.converged = 1; return rep; }
+    std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1);
+    int its = 0;
+    double rel = INFINITY;
+    DevBuf<double> ydev;
+    ydev.alloc(m + 1);
+    while (its < cfg.max_iters) {
+        level0_apply<1>(h, 1, false, x, b, r, s);  // r = b - A x
+        dot<1>(h, n, r, r, S_TMP, F_STORE, s);
+        double rr;
+        SPFD_CUDA(cudaMemcpyAsync(&rr, sc + S_TMP, sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPFD_CUDA(cudaStreamSynchronize(s));
+        double beta = std::sqrt(rr);
+        rel = beta / bnorm;
+        if (rel <= cfg.rel_tol) {
+            rep.iterations = its; rep.rel_residual[0] = rel; rep.converged = 1;
+            return rep;
+        }
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        k_scale_inv<<<G, 256, 0, s>>>(n, sc + S_TMP, r, V);
+        int j = 0;
+        while (j < m && its < cfg.max_iters) {
+            double *vj = V + (int64_t)j * n, *zj = Z + (int64_t)j * n;
+            amg_vcycle(h, vj, zj, 1, s);
+            level0_apply<1>(h, 0, false, zj, nullptr, w, s);
+            for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+                dot<1>(h, n, V + (int64_t)i * n, w, S_H + i, F_STORE, s);
+                k_axpy_dev<<<G, 256, 0, s>>>(n, sc + S_H + i, -1.0, V + (int64_t)i * n, w);
+            }
+            dot<1>(h, n, w, w, S_H + j + 1, F_STORE, s);
+            std::vector<double> col(j + 2);
+            SPFD_CUDA(cudaMemcpyAsync(col.data(), sc + S_H, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SPFD_CUDA(cudaStreamSynchronize(s));
+            double hn = std::sqrt(col[j + 1]);
+            if (!std::isfinite(hn)) { rep.status = SPFD_ENONFINITE; rep.iterations = its; return rep; }
+            for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = col[i];
+            for (int i = 0; i < j; ++i) {
+                double t1 = cs[i] * H[(size_t)i * m + j] + sn[i] * H[(size_t)(i + 1) * m + j];
+                double t2 = -sn[i] * H[(size_t)i * m + j] + cs[i] * H[(size_t)(i + 1) * m + j];
+                H[(size_t)i * m + j] = t1;
+                H[(size_t)(i + 1) * m + j] = t2;
+            }
+            double den = std::hypot(H[(size_t)j * m + j], hn);
+            if (den == 0.0) { cs[j] = 1.0; sn[j] = 0.0; }
+            else { cs[j] = H[(size_t)j * m + j] / den; sn[j] = hn / den; }
+            H[(size_t)j * m + j] = cs[j] * H[(size_t)j * m + j] + sn[j] * hn;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            ++its;
+            ++j;
+            double est = std::fabs(g[j]) / bnorm;
+            if (h_trace) h_trace[its - 1] = est;
+            if (hn == 0.0 || est <= cfg.rel_tol) break;
+            if (j < m) k_scale_inv<<<G, 256, 0, s>>>(n, sc + S_H + j, w, V + (int64_t)j * n);
+        }
+        if (j > 0) {
+            std::vector<double> y(j);
+            for (int i = j - 1; i >= 0; --i) {  // back substitution
+                double acc = g[i];
+                for (int k = i + 1; k < j; ++k) acc -= H[(size_t)i * m + k] * y[k];
+                y[i] = acc / H[(size_t)i * m + i];
+            }
+            for (double v : y)
+                if (!std::isfinite(v)) { rep.status = SPFD_ENONFINITE; rep.iterations = its; return rep; }
+            SPFD_CUDA(cudaMemcpyAsync(ydev.get(), y.data(), j * sizeof(double), cudaMemcpyHostToDevice, s));
+            k_combine<<<G, 256, 0, s>>>(n, j, ydev.get(), Z, x);
+            SPFD_LAUNCH_CHECK();
+        }
+    }
+    level0_apply<1>(h, 1, false, x, b, r, s);
+    dot<1>(h, n, r, r, S_TMP, F_STORE, s);
+    double rr;
+    SPFD_CUDA(cudaMemcpyAsync(&rr, sc + S_TMP, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    rel = std::sqrt(rr) / bnorm;
+    rep.iterations = its;
+    rep.rel_residual[0] = rel;
+    rep.converged = rel <= cfg.rel_tol;
+    return rep;
+}
+
+}  // namespace
+
+spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spfd_config &cfg, double *h_trace,
+                         cudaStream_t s) {
+    SPFD_CHECK(nrhs >= 1 && nrhs <= h.max_nrhs, SPFD_EINVAL, "nrhs exceeds the hierarchy workspace");
+    cudaEvent_t e0, e1;
+    SPFD_CUDA(cudaEventCreate(&e0));
+    SPFD_CUDA(cudaEventCreate(&e1));
+    SPFD_CUDA(cudaEventRecord(e0, s));
+    spfd_report rep{};
+    if (cfg.method == SPFD_METHOD_FGMRES) {
+        int64_t n = h.lv[0].nvec;
+        if (nrhs == 1) {
+            rep = fgmres1(h, b, x, cfg, h_trace, s);
+        } else {
+            DevBuf<double> b1, x1;
+            b1.alloc(n); x1.alloc(n);
+            std::vector<double> tr;
+            int G = grid_for(n, 256, 148 * 16);
+            rep.converged = 1;
+            for (int c = 0; c < nrhs; ++c) {
+                k_gather_col<<<G, 256, 0, s>>>(n, nrhs, c, b, b1.get());
+                if (h_trace) tr.assign((size_t)cfg.max_iters, 0.0);
+                spfd_report r1 = fgmres1(h, b1.get(), x1.get(), cfg, h_trace ? tr.data() : nullptr, s);
+                k_scatter_col<<<G, 256, 0, s>>>(n, nrhs, c, x1.get(), x);
+                if (h_trace)
+                    for (int k = 0; k < cfg.max_iters; ++k) h_trace[(int64_t)k * nrhs + c] = tr[k];
+                rep.iterations = std::max(rep.iterations, r1.iterations);
+                rep.rel_residual[c] = r1.rel_residual[0];
+                rep.converged = rep.converged && r1.converged;
+                if (r1.status) rep.status = r1.status;
+            }
+        }
+    } else {
+        rep = nrhs == 1 ? pcg<1>(h, b, x, cfg, h_trace, s) : pcg<2>(h, b, x, cfg, h_trace, s);
+    }
+    SPFD_CUDA(cudaEventRecord(e1, s));
+    SPFD_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    SPFD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    rep.solve_seconds = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return rep;
+}
+
+}  // namespace spfd

@@ -1,0 +1,105 @@
+"""Device-resident snapshot pipeline: assemble -> solve -> E-field.
+
+Mirrors the hot stages of `run_pipeline` (/root/reference/pkg/src/spfd/
+pipeline.py:158-175) and its setup-reuse seam (`_hierarchy`,
+pipeline.py:136,162; `run_benchmark` hoisting, :277-288).  A `Session`
+keeps the operator and AMG hierarchy resident on the GPU; each snapshot is
+one C-ABI call (`spfd_snapshot`): RHS assembly, the Krylov solve and the
+fused E-field / voxel average, with the real and imaginary parts batched.
+Non-convergence raises PipelineError("solve") like the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import PipelineError
+from .fit_operators import DeviceOperator
+from .linsolve import AmgHierarchy, SolveConfig, SolveReport, amg_setup
+
+
+class Session:
+    """Operator + hierarchy for one (phantom, frequency), reused across
+    snapshots (C5 of BASELINE.json)."""
+
+    def __init__(self, model, frequency_hz: float, cfg: SolveConfig | None = None):
+        self.cfg = cfg or SolveConfig(rel_tol=1e-8)
+        self.frequency_hz = float(frequency_hz)
+        self.omega = 2.0 * math.pi * self.frequency_hz
+        t0 = time.perf_counter()
+        self.op = DeviceOperator(model, frequency_hz, pin=True)
+        self.assemble_seconds = time.perf_counter() - t0
+        from .fit_operators import StencilMatrix  # noqa: F401
+        self.hierarchy: AmgHierarchy = amg_setup(_OpRef(self.op), self.cfg)
+        self._c = _lib.make_config(self.cfg)
+        self._vox = None
+        self._psi = None
+
+    @property
+    def n_dofs(self) -> int:
+        return self.op.n_dofs
+
+    @property
+    def n_cond_voxels(self) -> int:
+        return self.op.n_cond_voxels
+
+    def voxel_indices(self):
+        return self.op.export(_lib.EXPORT_VOXEL_INDICES)
+
+    def snapshot(self, a, keep_psi: bool = False, stream=None):
+        """One snapshot from device-resident edge potentials `a`
+        ((nrhs, n_edges) CUDA float64).  Returns (voxel |E| (nrhs, n_vox)
+        CUDA tensor, SolveReport, psi or None)."""
+        if not (isinstance(a, torch.Tensor) and a.is_cuda and a.dtype == torch.float64):
+            raise ValueError("snapshot() takes a CUDA float64 tensor; use snapshot_host() for numpy input")
+        if a.dim() == 1:
+            a = a.reshape(1, -1)
+        nrhs = a.shape[0]
+        if a.shape[1] != self.op.n_edges or nrhs not in (1, 2):
+            raise ValueError(f"expected (nrhs<=2, {self.op.n_edges}) edge potentials, got {tuple(a.shape)}")
+        a = a.contiguous()
+        if self._vox is None or self._vox.shape[0] != nrhs:
+            self._vox = torch.empty((nrhs, max(self.op.n_cond_voxels, 1)), dtype=torch.float64, device="cuda")
+            self._psi = torch.empty((nrhs, max(self.op.n_dofs, 1)), dtype=torch.float64, device="cuda")
+        rep = _lib.Report()
+        _lib.check(_lib.load().spfd_snapshot(self.op.handle, self.hierarchy.handle, _lib.ptr(a), self.omega,
+                                             _lib.ptr(self._psi) if keep_psi else ctypes.c_void_p(0),
+                                             _lib.ptr(self._vox), nrhs, ctypes.byref(self._c), ctypes.byref(rep),
+                                             _lib.stream_ptr(stream)))
+        rels = tuple(float(rep.rel_residual[k]) for k in range(nrhs))
+        report = SolveReport(iterations=int(rep.iterations), rel_residual=max(rels), converged=bool(rep.converged),
+                             setup_seconds=self.hierarchy.setup_seconds, solve_seconds=float(rep.solve_seconds),
+                             level_sizes=list(self.hierarchy.level_sizes),
+                             peak_matrix_memory_bytes=self.hierarchy.matrix_memory_bytes(), rel_residuals=rels,
+                             method=self.cfg.method)
+        if not report.converged:
+            raise PipelineError("solve", f"solver did not converge: residual {report.rel_residual:.3e} "
+                                         f"after {report.iterations} iterations")
+        vox = self._vox[:, :self.op.n_cond_voxels]
+        psi = self._psi[:, :self.op.n_dofs] if keep_psi else None
+        return vox, report, psi
+
+    def snapshot_host(self, a_host: np.ndarray, pinned: bool = True):
+        """End-to-end from host memory: H2D of the potentials, snapshot,
+        D2H of the voxel field.  Returns (numpy (nrhs, n_vox), report)."""
+        a_t = torch.from_numpy(np.ascontiguousarray(a_host, dtype=np.float64))
+        if pinned:
+            a_t = a_t.pin_memory()
+        a_d = a_t.to("cuda", non_blocking=True)
+        vox, rep, _ = self.snapshot(a_d)
+        return vox.cpu().numpy(), rep
+
+
+class _OpRef:
+    """Minimal matrix-like object carrying the operator (selects the
+    structured amg_setup path without materialising the host CSR)."""
+
+    def __init__(self, op: DeviceOperator):
+        self._spfd_op = op
+        self.shape = (op.n_dofs, op.n_dofs)

@@ -1,0 +1,221 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Writes tests/golden/<case>.npz.  The GPU box never reads /root/reference;
+it only reads these committed fixtures.  Every array comes straight from the
+reference package (`spfd`): conductances, the assembled CSR matrix and RHS,
+DOF maps, the AMG hierarchy (aggregates, P, R, coarse operators), the
+FGMRES solution at rel_tol 1e-12, and the E-field chain.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import scipy.sparse as sp  # noqa: E402
+from spfd import dosimetry as rd  # noqa: E402
+from spfd import field_source as rf  # noqa: E402
+from spfd import fit_operators as ro  # noqa: E402
+from spfd import gauging as rg  # noqa: E402
+from spfd import linsolve as rl  # noqa: E402
+from spfd import voxel_model as rv  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+FREQ = 85e3
+
+
+def block(dims, kappa=0.2, spacing=0.002):
+    ids = np.ones(dims, dtype=np.uint16)
+    table = {0: rv.Tissue("free_space", rv.ConductivitySamples.constant(0.0)),
+             1: rv.Tissue("tissue", rv.ConductivitySamples.constant(kappa))}
+    return rv.VoxelModel(dims, (spacing,) * 3, (0.0, 0.0, 0.0), ids, table)
+
+
+def two_blobs():
+    """Two separate conductive bodies, an internal cavity and a row with two
+    spans: exercises multi-component pinning and holes."""
+    dims = (14, 9, 8)
+    ids = np.zeros(dims, dtype=np.uint16)
+    ids[1:6, 1:8, 1:7] = 1
+    ids[8:13, 2:7, 2:6] = 2
+    ids[3, 4, 3] = 0          # cavity inside body 1
+    table = {0: rv.Tissue("free_space", rv.ConductivitySamples.constant(0.0)),
+             1: rv.Tissue("a", rv.ConductivitySamples.from_pairs([(1e3, 0.1), (1e6, 0.4)])),
+             2: rv.Tissue("b", rv.ConductivitySamples.constant(0.05))}
+    return rv.VoxelModel(dims, (0.002, 0.0025, 0.003), (0.0, 0.0, 0.0), ids, table)
+
+
+def reference_potential(model, b):
+    """Uniform field through the reference's own chain: lattice sampling,
+    face interpolation, comb-tree gauging (pipeline.py:105-156)."""
+    grid = ro.StaggeredGrid.from_model(model)
+    lattice = rf.Lattice.covering(grid, (2, 2, 2))
+    samples = rf.sample_on_lattice(rf.UniformField(b), lattice, FREQ)
+    flux = rf.interpolate_to_faces(samples, grid)
+    flux = rf.divergence_clean(flux, grid, 1e-10)
+    tree = rg.build_tree(grid, "comb")
+    return rg.gauge_vector_potential(flux, grid, tree, 1e-10)
+
+
+def dipole_potential(model, moment, center):
+    grid = ro.StaggeredGrid.from_model(model)
+    out = []
+    for axis in range(3):
+        ed = grid.edge_dims(axis)
+        c = []
+        for a in range(3):
+            v = np.arange(ed[a]) * model.spacing[a]
+            if a == axis:
+                v = v + 0.5 * model.spacing[a]
+            c.append(v - center[a])
+        X, Y, Z = c[0][:, None, None], c[1][None, :, None], c[2][None, None, :]
+        r3 = (X * X + Y * Y + Z * Z) ** 1.5
+        m = moment
+        comp = [m[1] * Z - m[2] * Y, m[2] * X - m[0] * Z, m[0] * Y - m[1] * X][axis]
+        out.append((1e-7 * comp / r3 * model.spacing[axis]).ravel(order="F"))
+    return np.concatenate(out)
+
+
+def csr_parts(prefix, m, d):
+    m = sp.csr_matrix(m)
+    d[prefix + "_indptr"] = m.indptr.astype(np.int64)
+    d[prefix + "_indices"] = m.indices.astype(np.int32)
+    d[prefix + "_data"] = m.data.astype(np.float64)
+    d[prefix + "_shape"] = np.array(m.shape, dtype=np.int64)
+
+
+def hierarchy_parts(h, d, max_levels_store=10):
+    d["amg_sizes"] = np.array(h.level_sizes, dtype=np.int64)
+    for l, lv in enumerate(h.levels[:max_levels_store]):
+        csr_parts(f"A{l}", lv.matrix, d)
+        if lv.prolongation is not None:
+            csr_parts(f"P{l}", lv.prolongation, d)
+            csr_parts(f"R{l}", lv.restriction, d)
+
+
+def aggregates(h, cfg):
+    """Re-run the reference's strength graph + plain_aggregation per level."""
+    from spfd._kernels import plain_aggregation
+    out = []
+    for l, lv in enumerate(h.levels[:-1]):
+        ip, ix, sv = rl._strength_graph(lv.matrix, cfg.strength_threshold * 0.5 ** l)
+        agg, _ = plain_aggregation(ip, ix, sv, lv.matrix.shape[0])
+        out.append(agg.astype(np.int32))
+    return out
+
+
+def model_case(name, model, a, solve=True, store_amg=True):
+    grid = ro.StaggeredGrid.from_model(model)
+    d = {}
+    d["dims"] = np.array(model.dims, dtype=np.int64)
+    d["spacing"] = np.array(model.spacing, dtype=np.float64)
+    d["ids"] = np.asarray(model.tissue_ids, dtype=np.uint16).ravel(order="F")
+    lut = np.zeros(int(model.tissue_ids.max()) + 1)
+    for tid, t in model.tissue_table.items():
+        if tid < lut.size:
+            lut[tid] = t.conductivity.at(FREQ)
+    d["lut"] = lut
+    d["freq"] = np.array(FREQ)
+    d["a"] = np.asarray(a, dtype=np.float64)
+    system = ro.assemble_poisson(model, grid, a, FREQ)
+    d["w"] = system.edge_conductance
+    csr_parts("matrix", system.matrix, d)
+    d["rhs"] = system.rhs
+    d["dof_to_node"] = system.dof_to_node.astype(np.int64)
+    d["pinned"] = system.pinned_nodes.astype(np.int64)
+    d["n_components"] = np.array(system.n_components)
+    d["n_conductive"] = np.array(system.n_conductive_nodes)
+    labels = rv.conductive_component_labels(model, FREQ)
+    d["labels"] = labels.astype(np.int32)
+    cfg = rl.SolveConfig(rel_tol=1e-12)
+    h = rl.amg_setup(system.matrix, cfg)
+    if store_amg:
+        hierarchy_parts(h, d)
+        for l, agg in enumerate(aggregates(h, cfg)):
+            d[f"agg{l}"] = agg
+    if solve and system.rhs.any():
+        psi, rep = rl.fgmres_solve(system.matrix, system.rhs, h, cfg)
+        d["psi"] = psi
+        d["fgmres_iters"] = np.array(rep.iterations)
+        omega = 2 * math.pi * FREQ
+        v = rd.edge_voltages(a, psi, system, omega)
+        nf = rd.node_field_strength(v, grid, model, FREQ)
+        vals, idx = rd.voxel_average(nf, grid, model, FREQ)
+        d["omega"] = np.array(omega)
+        d["volts"] = v
+        d["node_field"] = nf.ravel(order="F")
+        d["vox"] = vals
+        d["vox_idx"] = idx.astype(np.int64)
+    # a random residual through the reference V-cycle
+    rng = np.random.default_rng(20240817)
+    r = rng.standard_normal(system.n_dofs)
+    d["vcycle_in"] = r
+    d["vcycle_out"] = rl.v_cycle(h, r)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(name, "dofs", system.n_dofs, "levels", h.level_sizes, "bytes",
+          os.path.getsize(os.path.join(OUT, f"{name}.npz")))
+
+
+def matrix_case(name, a):
+    d = {}
+    cfg = rl.SolveConfig(rel_tol=1e-12)
+    h = rl.amg_setup(a, cfg)
+    hierarchy_parts(h, d)
+    for l, agg in enumerate(aggregates(h, cfg)):
+        d[f"agg{l}"] = agg
+    rng = np.random.default_rng(20240817)
+    b = rng.standard_normal(a.shape[0])
+    x, rep = rl.fgmres_solve(a, b, h, cfg)
+    d["b"] = b
+    d["x"] = x
+    d["fgmres_iters"] = np.array(rep.iterations)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(name, "n", a.shape[0], "levels", h.level_sizes)
+
+
+def laplacian_3d(n):
+    d = sp.diags([-np.ones(n - 1), 2 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1])
+    eye = sp.identity(n)
+    return (sp.kron(sp.kron(d, eye), eye) + sp.kron(sp.kron(eye, d), eye)
+            + sp.kron(sp.kron(eye, eye), d)).tocsr()
+
+
+def main():
+    rng = np.random.default_rng(20240817)
+    m = block((6, 6, 6))
+    g = ro.StaggeredGrid.from_model(m)
+    model_case("box6_random", m, rng.standard_normal(g.n_edges))
+
+    m = rv.make_phantom("sphere", (8, 8, 8), 0.002, radius_m=0.006)
+    model_case("sphere8_uniform", m, reference_potential(m, (0.0, 0.0, 1e-6)))
+
+    m = rv.make_phantom("layered-block", (14, 12, 16), 0.002, layers=4,
+                        kappa_spm=[0.17, 0.04, 0.35, 0.02], size_m=(0.02, 0.016, 0.024))
+    model_case("layered_dipole", m, dipole_potential(m, (0.0, 0.0, 7.0), (0.014, 0.012, -0.05)))
+
+    m = two_blobs()
+    g = ro.StaggeredGrid.from_model(m)
+    model_case("two_blobs", m, rng.standard_normal(g.n_edges))
+
+    m = block((16, 16, 16))
+    model_case("box16_uniform", m, reference_potential(m, (0.3e-6, -0.2e-6, 1e-6)))
+
+    m = rv.make_phantom("cylinder", (20, 20, 12), 0.002, radius_m=0.016, kappa_spm=0.3)
+    model_case("cylinder_uniform", m, reference_potential(m, (0.0, 0.0, 1e-6)))
+
+    matrix_case("laplacian12", laplacian_3d(12))
+
+
+if __name__ == "__main__":
+    main()
