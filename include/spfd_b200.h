@@ -129,7 +129,7 @@ int spfd_node_field(spfd_op_t op, const double *v, double *node, int nrhs,
 int spfd_voxel_average(spfd_op_t op, const double *node, double *vox, int nrhs,
                        void *stream);
 /* Fused chain a, psi -> voxel |E| without materialising edge voltages or the
- * node box: bit-identical to the three calls above.  node_out may be NULL. */
+ * node box: bit-identical to the three calls above. */
 int spfd_efield_voxavg(spfd_op_t op, const double *a, const double *psi,
                        double omega, double *vox, int nrhs, void *stream);
 
@@ -213,6 +213,18 @@ int spfd_solve(spfd_amg_t amg, const double *b, double *x, int nrhs,
 int spfd_snapshot(spfd_op_t op, spfd_amg_t amg, const double *a, double omega,
                   double *psi, double *vox, int nrhs, const spfd_config *h_cfg,
                   spfd_report *h_rep, void *stream);
+
+/* ---- measurement ---------------------------------------------------------- */
+
+/* Time `reps` back-to-back launches of one level-0 kernel between CUDA
+ * events on `stream` (after 3 warm-up launches):
+ *   which = 0 fine SpMV q = A p (+ p.q partials), 1 fused pre-smooth +
+ *   defect, 2 post-smooth sweep, 3 one full V-cycle.
+ * h_ms: ms per launch; h_bytes: algorithmic bytes per launch (0 for 3). */
+int spfd_bench_kernel(spfd_amg_t amg, int which, int reps, int nrhs, double *h_ms, double *h_bytes,
+                      void *stream);
+/* Number of kernels this library has launched so far (process-wide). */
+int64_t spfd_launch_count(void);
 
 #ifdef __cplusplus
 }

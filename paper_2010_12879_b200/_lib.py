@@ -120,6 +120,8 @@ _SIGS = {
     "spfd_vcycle": (_INT, [_VP, _VP, _VP, _INT, _VP]),
     "spfd_solve": (_INT, [_VP, _VP, _VP, _INT, _VP, _VP, _VP, _VP]),
     "spfd_snapshot": (_INT, [_VP, _VP, _VP, _D, _VP, _VP, _INT, _VP, _VP, _VP]),
+    "spfd_bench_kernel": (_INT, [_VP, _INT, _INT, _INT, _VP, _VP, _VP]),
+    "spfd_launch_count": (ctypes.c_int64, []),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

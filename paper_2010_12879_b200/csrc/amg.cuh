@@ -70,6 +70,7 @@ void amg_level_agg(Amg &h, int level, int32_t *agg, cudaStream_t s);
 void amg_to_level0(Amg &h, const double *planar, double *inter, int nrhs, cudaStream_t s);
 void amg_from_level0(Amg &h, const double *inter, double *planar, int nrhs, cudaStream_t s);
 
+double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cudaStream_t s);
 spfd_report krylov_solve(Amg &h, const double *b_inter, double *x_inter, int nrhs, const spfd_config &cfg,
                          double *h_trace, cudaStream_t s);
 

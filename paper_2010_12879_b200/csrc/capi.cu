@@ -1,4 +1,5 @@
 // extern "C" boundary of libspfd_b200.so (include/spfd_b200.h).
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -15,6 +16,9 @@ struct spfd_amg_s {
 namespace spfd {
 
 static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+int64_t launch_count() { return g_launches.load(); }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void set_last_error(const std::string &msg) { g_last_error = msg; }
 
 template <class F>
@@ -260,5 +264,14 @@ int spfd_snapshot(spfd_op_t hop, spfd_amg_t h, const double *a, double omega, do
         SPFD_CUDA(cudaStreamSynchronize(S(stream)));
     });
 }
+
+int spfd_bench_kernel(spfd_amg_t h, int which, int reps, int nrhs, double *h_ms, double *h_bytes, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && h_ms && h_bytes && which >= 0 && which <= 3, SPFD_EINVAL, "bad argument");
+        *h_ms = amg_bench_kernel(*h->amg, which, reps, nrhs, h_bytes, S(stream));
+    });
+}
+
+int64_t spfd_launch_count(void) { return spfd::launch_count(); }
 
 }  // extern "C"

@@ -32,7 +32,15 @@ void set_last_error(const std::string &msg);
         if (!(cond)) throw ::spfd::Error((code), (msg));                       \
     } while (0)
 
-#define SPFD_LAUNCH_CHECK() SPFD_CUDA(cudaGetLastError())
+// Every kernel launch on the library's paths is followed by this check; it
+// also counts launches (bench.py reports them as `gpu_launches`).
+int64_t launch_count();
+void count_launch();
+#define SPFD_LAUNCH_CHECK()                                                    \
+    do {                                                                       \
+        ::spfd::count_launch();                                                \
+        SPFD_CUDA(cudaGetLastError());                                         \
+    } while (0)
 
 // ------------------------------------------------------- device buffers --
 // RAII device allocation (stream-ordered).  Handles own their buffers; the

@@ -249,6 +249,21 @@ __global__ void k_dense_mv(const double *cinv, int64_t n, const double *r, doubl
     }
 }
 
+template <int R>
+__global__ void k_span_gather(const int32_t *dof_to_pos, int64_t n, const double *span, double *out) {
+    for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int c = 0; c < R; ++c) out[d * R + c] = span[(int64_t)dof_to_pos[d] * R + c];
+}
+template <int R>
+__global__ void k_span_scatter(const int32_t *pos_to_dof, int64_t L, const double *in, double *span) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L; p += (int64_t)gridDim.x * blockDim.x) {
+        int d = pos_to_dof[p];
+#pragma unroll
+        for (int c = 0; c < R; ++c) span[p * R + c] = d >= 0 ? in[(int64_t)d * R + c] : 0.0;
+    }
+}
+
 // ---- elementwise / BLAS-1 ----------------------------------------------
 template <int R>
 __global__ void k_odinv_r(int64_t n, const double *od, const double *r, double *x) {
@@ -453,7 +468,17 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
     int nl = (int)h.lv.size();
     Level &L = h.lv[l];
     if (l == nl - 1) {
-        k_dense_mv<R><<<grid_for(h.nc * 32, 256, 148 * 8), 256, 0, s>>>(h.cinv.get(), h.nc, r, z);
+        if (l == 0 && h.structured) {
+            // single-level structured hierarchy: the dense inverse acts on DOF order
+            const Operator &op = *h.op;
+            k_span_gather<R><<<grid_for(op.n_dofs, 256, 148 * 16), 256, 0, s>>>(op.dof_to_pos.get(), op.n_dofs, r,
+                                                                                L.vd.get());
+            k_dense_mv<R><<<grid_for(h.nc * 32, 256, 148 * 8), 256, 0, s>>>(h.cinv.get(), h.nc, L.vd.get(),
+                                                                           L.vt.get());
+            k_span_scatter<R><<<grid_for(op.L, 256, 148 * 16), 256, 0, s>>>(op.pos_to_dof.get(), op.L, L.vt.get(), z);
+        } else {
+            k_dense_mv<R><<<grid_for(h.nc * 32, 256, 148 * 8), 256, 0, s>>>(h.cinv.get(), h.nc, r, z);
+        }
         SPFD_LAUNCH_CHECK();
         return;
     }
@@ -736,6 +761,56 @@ spfd_report fgmres1(Amg &h, const double *b, double *x, const spfd_config &cfg, 
 }
 
 }  // namespace
+
+// Back-to-back launches of one level-0 kernel between two events on `s`
+// (bench.py roofline).  Returns ms per launch; *bytes = algorithmic bytes
+// per launch (each distinct array read or written once).
+double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cudaStream_t s) {
+    SPFD_CHECK(nrhs >= 1 && nrhs <= h.max_nrhs && reps >= 1, SPFD_EINVAL, "bad bench arguments");
+    Level &L = h.lv[0];
+    int64_t n = L.nvec;
+    SPFD_CUDA(cudaMemsetAsync(h.kp.get(), 0x3f, n * nrhs * sizeof(double), s));
+    SPFD_CUDA(cudaMemsetAsync(h.kr.get(), 0x3e, n * nrhs * sizeof(double), s));
+    double R = nrhs;
+    double b = 0.0;
+    if (h.structured) {
+        double pos = (double)h.op->L;
+        double mask = pos / 8.0;
+        if (which == 0) b = pos * (24.0 + 16.0 * R) + mask;              // w, x -> y
+        else if (which == 1) b = pos * (32.0 + 16.0 * R) + mask;         // w, odinv, r -> d
+        else if (which == 2) b = pos * (32.0 + 24.0 * R) + mask;         // w, odinv, x, r -> x'
+        else b = 0.0;
+    } else {
+        double nnz = (double)L.A.nnz, rows = (double)L.A.rows;
+        double mat = nnz * 12.0 + (rows + 1) * 8.0;
+        if (which == 0) b = mat + rows * 16.0 * R;
+        else if (which == 1) b = mat + rows * (8.0 + 16.0 * R);
+        else if (which == 2) b = mat + rows * (8.0 + 24.0 * R);
+    }
+    auto launch = [&]() {
+        if (which == 3) {
+            amg_vcycle(h, h.kr.get(), h.kz.get(), nrhs, s);
+            return;
+        }
+        int mode = which == 0 ? 0 : (which == 1 ? 2 : 3);
+        if (nrhs == 1) level0_apply<1>(h, mode, which == 0, h.kp.get(), h.kr.get(), h.kq.get(), s);
+        else level0_apply<2>(h, mode, which == 0, h.kp.get(), h.kr.get(), h.kq.get(), s);
+    };
+    for (int i = 0; i < 3; ++i) launch();
+    cudaEvent_t e0, e1;
+    SPFD_CUDA(cudaEventCreate(&e0));
+    SPFD_CUDA(cudaEventCreate(&e1));
+    SPFD_CUDA(cudaEventRecord(e0, s));
+    for (int i = 0; i < reps; ++i) launch();
+    SPFD_CUDA(cudaEventRecord(e1, s));
+    SPFD_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    SPFD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *bytes = b;
+    return ms / reps;
+}
 
 spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spfd_config &cfg, double *h_trace,
                          cudaStream_t s) {

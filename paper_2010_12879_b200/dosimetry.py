@@ -18,18 +18,23 @@ import torch
 
 from .fit_operators import DeviceOperator, PoissonSystem, StaggeredGrid
 
-_OP_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_OP_CACHE: dict = {}
 
 
 def _operator_for(model, frequency_hz, system=None) -> DeviceOperator:
     if system is not None:
         return system.operator
-    per_model = _OP_CACHE.setdefault(model, {})
-    key = float(frequency_hz)
-    op = per_model.get(key)
-    if op is None:
-        op = DeviceOperator(model, frequency_hz, pin=True)
-        per_model[key] = op
+    # models are frozen dataclasses holding arrays (unhashable): key by id
+    # and keep a weak reference to detect reuse of the id after collection
+    key = (id(model), float(frequency_hz))
+    hit = _OP_CACHE.get(key)
+    if hit is not None and hit[0]() is model:
+        return hit[1]
+    op = DeviceOperator(model, frequency_hz, pin=True)
+    try:
+        _OP_CACHE[key] = (weakref.ref(model), op)
+    except TypeError:
+        pass
     return op
 
 
