@@ -34,6 +34,9 @@ struct Level {
     Csr P, R;                 // solve-layout prolongation / restriction
     Csr P_dof, R_dof;         // DOF-numbered copies (structured level 0 only; exports)
     DevBuf<int32_t> agg;      // aggregate per row (DOF numbering)
+    DevBuf<int32_t> agg_pos;  // structured level 0: aggregate per span position (-1 = none)
+    DevBuf<int64_t> mem_ptr;  // structured level 0: aggregate -> member positions (CSR of T^T)
+    DevBuf<int32_t> mem_pos;
     DevBuf<double> dinv;      // [nvec]
     DevBuf<double> odinv;     // [nvec] omega * dinv
     DevBuf<double> vr, vx, vd, vt;  // workspaces [nvec * max_nrhs]

@@ -566,6 +566,48 @@ __global__ void k_dofs_to_span_1(const int32_t *pos_to_dof, int64_t L, const dou
     }
 }
 
+__global__ void k_agg_pos(const int32_t *pos_to_dof, int64_t L, const int32_t *agg, int32_t *out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int d = pos_to_dof[p];
+        out[p] = d >= 0 ? agg[d] : -1;
+    }
+}
+
+__global__ void k_member_init(const int32_t *dof_to_pos, int64_t n, int32_t *pos) {
+    for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x)
+        pos[d] = dof_to_pos[d];
+}
+
+__global__ void k_count_agg(const int32_t *agg, int64_t n, int64_t *cnt) {
+    for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd((unsigned long long *)&cnt[agg[d]], 1ull);
+}
+
+// members of every aggregate in ascending position order: stable radix sort
+// of (aggregate id, position) pairs in DOF order (positions ascend with DOFs)
+void build_members(const int32_t *agg, int64_t n, int64_t n_agg, const int32_t *dof_to_pos, DevBuf<int64_t> &mptr,
+                   DevBuf<int32_t> &mpos, cudaStream_t s) {
+    const int T = 256;
+    DevBuf<int32_t> k1, v0;
+    k1.alloc(n); v0.alloc(n);
+    mpos.alloc(n);
+    k_member_init<<<grid_for(n, T), T, 0, s>>>(dof_to_pos, n, v0.get());
+    size_t bytes = 0;
+    int end_bit = bits_for((uint64_t)n_agg);
+    SPFD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, agg, k1.get(), v0.get(), mpos.get(), n, 0, end_bit, s));
+    DevBuf<uint8_t> tmp;
+    tmp.alloc(bytes);
+    SPFD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, agg, k1.get(), v0.get(), mpos.get(), n, 0, end_bit, s));
+    DevBuf<int64_t> cnt;
+    cnt.alloc(n_agg + 1);
+    SPFD_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+    k_count_agg<<<grid_for(n, T), T, 0, s>>>(agg, n, cnt.get());
+    SPFD_LAUNCH_CHECK();
+    mptr.alloc(n_agg + 1);
+    scan_excl(cnt.get(), mptr.get(), n_agg + 1, s);
+}
+
 int pick_group(int64_t nnz, int64_t rows) {
     double avg = rows > 0 ? (double)nnz / (double)rows : 1.0;
     if (avg <= 6.0) return 4;
@@ -722,7 +764,7 @@ int64_t Amg::device_bytes() const {
                 partials.bytes() + scal.bytes() + fg_basis.bytes() + fg_prec.bytes();
     for (auto &l : lv)
         b += l.A.bytes() + l.P.bytes() + l.R.bytes() + l.P_dof.bytes() + l.R_dof.bytes() + l.agg.bytes() +
-             l.dinv.bytes() + l.odinv.bytes() + l.vr.bytes() + l.vx.bytes() + l.vd.bytes() + l.vt.bytes();
+             l.dinv.bytes() + l.odinv.bytes() + l.agg_pos.bytes() + l.mem_ptr.bytes() + l.mem_pos.bytes() + l.vr.bytes() + l.vx.bytes() + l.vd.bytes() + l.vt.bytes();
     return b;
 }
 
@@ -798,40 +840,22 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
                                                                L.odinv.get());
             SPFD_LAUNCH_CHECK();
             if (l < nl - 1) {
-                // P/R in span numbering; keep DOF copies for export
-                Csr &Pd = L.P;
-                Csr &Rd = L.R;
-                Csr Ps, Rs;
-                DevBuf<int64_t> cnt;
-                cnt.alloc(L.nvec + 1);
-                SPFD_CUDA(cudaMemsetAsync(cnt.get() + L.nvec, 0, sizeof(int64_t), s));
-                k_span_rowcnt<<<grid_for(L.nvec, T), T, 0, s>>>(h->op->pos_to_dof.get(), L.nvec, Pd.ptr.get(),
-                                                                cnt.get());
-                Ps.alloc(L.nvec, Pd.cols, Pd.nnz);
-                scan_excl(cnt.get(), Ps.ptr.get(), L.nvec + 1, s);
-                SPFD_CUDA(cudaMemcpyAsync(Ps.col.get(), Pd.col.get(), Pd.nnz * sizeof(int32_t),
-                                          cudaMemcpyDeviceToDevice, s));
-                SPFD_CUDA(cudaMemcpyAsync(Ps.val.get(), Pd.val.get(), Pd.nnz * sizeof(double),
-                                          cudaMemcpyDeviceToDevice, s));
-                Rs.alloc(Rd.rows, L.nvec, Rd.nnz);
-                SPFD_CUDA(cudaMemcpyAsync(Rs.ptr.get(), Rd.ptr.get(), (Rd.rows + 1) * sizeof(int64_t),
-                                          cudaMemcpyDeviceToDevice, s));
-                SPFD_CUDA(cudaMemcpyAsync(Rs.val.get(), Rd.val.get(), Rd.nnz * sizeof(double),
-                                          cudaMemcpyDeviceToDevice, s));
-                if (Rd.nnz)
-                    k_map_cols<<<grid_for(Rd.nnz, T), T, 0, s>>>(Rd.col.get(), Rd.nnz, h->op->dof_to_pos.get(),
-                                                                 Rs.col.get());
+                // matrix-free transfers: aggregate per span position and the
+                // member lists of T^T (ascending positions); P/R kept in DOF
+                // numbering only for export
+                L.agg_pos.alloc(L.nvec);
+                k_agg_pos<<<grid_for(L.nvec, T), T, 0, s>>>(h->op->pos_to_dof.get(), L.nvec, L.agg.get(),
+                                                            L.agg_pos.get());
                 SPFD_LAUNCH_CHECK();
+                build_members(L.agg.get(), L.n, h->lv[l + 1].n, h->op->dof_to_pos.get(), L.mem_ptr, L.mem_pos, s);
                 L.P_dof = std::move(L.P);
                 L.R_dof = std::move(L.R);
-                L.P = std::move(Ps);
-                L.R = std::move(Rs);
             }
         } else {
             finish_level(L, mats[l], h->omega, s);
             L.A = std::move(mats[l]);
         }
-        if (l < nl - 1) {
+        if (l < nl - 1 && !(l == 0 && h->structured)) {
             L.p_group = pick_group(L.P.nnz, L.P.rows);
             L.r_group = pick_group(L.R.nnz, L.R.rows);
         }

@@ -183,12 +183,13 @@ __global__ void k_row_span(const uint8_t *flags, Geo g, int64_t n_rows, int *lo_
     }
 }
 
+// row table entry {offset, lo, hi, j}
 __global__ void k_rows_pack(const int *lo, const int *hi, const int *off, int64_t n_rows,
-                            int64_t L, int4 *rows) {
+                            int64_t L, int NY, int4 *rows) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n_rows;
          r += (int64_t)gridDim.x * blockDim.x) {
         if (r == n_rows) rows[r] = make_int4((int)L, 0, 0, 0);
-        else rows[r] = make_int4(off[r], lo[r], hi[r], 0);
+        else rows[r] = make_int4(off[r], lo[r], hi[r], (int)(r % NY));
     }
 }
 
@@ -474,7 +475,7 @@ Operator *op_create(const int64_t *dims, const double *spacing, const uint16_t *
         }
         op->rows.alloc(op->n_rows + 1);
         k_rows_pack<<<grid_for(op->n_rows + 1, T), T, 0, s>>>(lo.get(), hi.get(), off.get(), op->n_rows,
-                                                             op->L, op->rows.get());
+                                                             op->L, (int)op->NY, op->rows.get());
         op->n_tiles = (op->L + kTile - 1) / kTile;
         op->tile_row.alloc(op->n_tiles + 1);
         k_tile_rows<<<grid_for(op->n_tiles + 1, T), T, 0, s>>>(op->rows.get(), op->n_rows, op->n_tiles,

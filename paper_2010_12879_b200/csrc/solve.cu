@@ -38,88 +38,143 @@ __device__ __forceinline__ int frow(const int4 *rows, int r0, int r1, int p) {
     return lo;
 }
 
-// Stencil product at position p with the input given by a functor X(pos, c)
-// (so x = odinv*r or z + beta*p can be formed on the fly at the neighbours).
-// Sum order is the reference's sorted-column order.
-template <int R, class X>
-__device__ __forceinline__ void stencil_at(const SpanView &v, int p, int r, int i, int4 q, X xat, double (&s)[R]) {
-    int j = r % v.NY;
-    double wxp = v.wx[p], wyp = v.wy[p], wzp = v.wz[p];
-    double wxm = 0.0, wym = 0.0, wzm = 0.0;
-    int pxm = -1, pym = -1, pzm = -1, pxp = -1, pyp = -1, pzp = -1;
-    if (i > q.y) { pxm = p - 1; wxm = v.wx[pxm]; }
-    if (i + 1 < q.z) pxp = p + 1;
-    if (j > 0) { pym = spos(v.rows, r - 1, i); if (pym >= 0) wym = v.wy[pym]; }
-    if (j + 1 < v.NY) pyp = spos(v.rows, r + 1, i);
-    if (r >= v.NY) { pzm = spos(v.rows, r - v.NY, i); if (pzm >= 0) wzm = v.wz[pzm]; }
-    if (r + v.NY < v.n_rows) pzp = spos(v.rows, r + v.NY, i);
-    double d = add_rn(add_rn(add_rn(add_rn(add_rn(wxp, wyp), wzp), wxm), wym), wzm);
-#pragma unroll
-    for (int c = 0; c < R; ++c) {
-        double a = 0.0;
-        if (pzm >= 0) a = add_rn(a, mul_rn(-wzm, xat(pzm, c)));
-        if (pym >= 0) a = add_rn(a, mul_rn(-wym, xat(pym, c)));
-        if (pxm >= 0) a = add_rn(a, mul_rn(-wxm, xat(pxm, c)));
-        a = add_rn(a, mul_rn(d, xat(p, c)));
-        if (pxp >= 0) a = add_rn(a, mul_rn(-wxp, xat(pxp, c)));
-        if (pyp >= 0) a = add_rn(a, mul_rn(-wyp, xat(pyp, c)));
-        if (pzp >= 0) a = add_rn(a, mul_rn(-wzp, xat(pzp, c)));
-        s[c] = a;
+// R-wide vector element (R = 1: double, R = 2: double2 real/imag pair)
+template <int R> struct V;
+template <> struct V<1> {
+    using T = double;
+    static __device__ __forceinline__ T ld(const double *p, int64_t i) { return p[i]; }
+    static __device__ __forceinline__ void st(double *p, int64_t i, T v) { p[i] = v; }
+    static __device__ __forceinline__ T zero() { return 0.0; }
+    static __device__ __forceinline__ T axpy(double a, T x, T y) { return add_rn(y, mul_rn(a, x)); }  // exact y + a*x
+    static __device__ __forceinline__ T fma_(double a, T x, T y) { return fma(a, x, y); }
+    static __device__ __forceinline__ T sub(T a, T b) { return a - b; }
+    static __device__ __forceinline__ T add(T a, T b) { return a + b; }
+    static __device__ __forceinline__ T scale(double a, T x) { return a * x; }
+    static __device__ __forceinline__ double dot(T a, T b, int) { return a * b; }
+    static __device__ __forceinline__ double comp(T a, int) { return a; }
+};
+template <> struct V<2> {
+    using T = double2;
+    static __device__ __forceinline__ T ld(const double *p, int64_t i) { return reinterpret_cast<const double2 *>(p)[i]; }
+    static __device__ __forceinline__ void st(double *p, int64_t i, T v) { reinterpret_cast<double2 *>(p)[i] = v; }
+    static __device__ __forceinline__ T zero() { return make_double2(0.0, 0.0); }
+    static __device__ __forceinline__ T axpy(double a, T x, T y) {
+        return make_double2(add_rn(y.x, mul_rn(a, x.x)), add_rn(y.y, mul_rn(a, x.y)));
     }
+    static __device__ __forceinline__ T fma_(double a, T x, T y) { return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y)); }
+    static __device__ __forceinline__ T sub(T a, T b) { return make_double2(a.x - b.x, a.y - b.y); }
+    static __device__ __forceinline__ T add(T a, T b) { return make_double2(a.x + b.x, a.y + b.y); }
+    static __device__ __forceinline__ T scale(double a, T x) { return make_double2(a * x.x, a * x.y); }
+    static __device__ __forceinline__ double dot(T a, T b, int c) { return c == 0 ? a.x * b.x : a.y * b.y; }
+    static __device__ __forceinline__ double comp(T a, int c) { return c == 0 ? a.x : a.y; }
+};
+
+// Neighbourhood of one span position: the 6 edge weights and the positions
+// of the 6 neighbours (-1 outside the conductive spans).
+struct Nbr {
+    double wxp, wyp, wzp, wxm, wym, wzm, diag;
+    int pxm, pym, pzm, pxp, pyp, pzp;
+};
+
+__device__ __forceinline__ Nbr neighbours(const SpanView &v, int p, int r, int4 q) {
+    Nbr n;
+    const int i = q.y + (p - q.x), j = q.w;
+    n.wxp = v.wx[p]; n.wyp = v.wy[p]; n.wzp = v.wz[p];
+    n.wxm = 0.0; n.wym = 0.0; n.wzm = 0.0;
+    n.pxm = (i > q.y) ? p - 1 : -1;
+    n.pxp = (i + 1 < q.z) ? p + 1 : -1;
+    n.pym = (j > 0) ? spos(v.rows, r - 1, i) : -1;
+    n.pyp = (j + 1 < v.NY) ? spos(v.rows, r + 1, i) : -1;
+    n.pzm = (r >= v.NY) ? spos(v.rows, r - v.NY, i) : -1;
+    n.pzp = (r + v.NY < v.n_rows) ? spos(v.rows, r + v.NY, i) : -1;
+    if (n.pxm >= 0) n.wxm = v.wx[n.pxm];
+    if (n.pym >= 0) n.wym = v.wy[n.pym];
+    if (n.pzm >= 0) n.wzm = v.wz[n.pzm];
+    // reference diagonal order: tail edges x, y, z then head edges x, y, z
+    n.diag = add_rn(add_rn(add_rn(add_rn(add_rn(n.wxp, n.wyp), n.wzp), n.wxm), n.wym), n.wzm);
+    return n;
 }
 
-struct ArrX {
-    const double *x;
-    int R;
-    __device__ double operator()(int p, int c) const { return x[(int64_t)p * R + c]; }
-};
-struct ScaledX {  // odinv * r
-    const double *od, *r;
-    int R;
-    __device__ double operator()(int p, int c) const { return od[p] * r[(int64_t)p * R + c]; }
+// (A x)_p in the reference's sorted-column order; X(pos) -> V<R>::T.
+template <int R, class X>
+__device__ __forceinline__ typename V<R>::T apply_row(const Nbr &n, int p, X xat) {
+    using W = V<R>;
+    typename W::T s = W::zero();
+    if (n.pzm >= 0) s = W::axpy(-n.wzm, xat(n.pzm), s);
+    if (n.pym >= 0) s = W::axpy(-n.wym, xat(n.pym), s);
+    if (n.pxm >= 0) s = W::axpy(-n.wxm, xat(n.pxm), s);
+    s = W::axpy(n.diag, xat(p), s);
+    if (n.pxp >= 0) s = W::axpy(-n.wxp, xat(n.pxp), s);
+    if (n.pyp >= 0) s = W::axpy(-n.wyp, xat(n.pyp), s);
+    if (n.pzp >= 0) s = W::axpy(-n.wzp, xat(n.pzp), s);
+    return s;
+}
+
+struct SpanArgs {
+    const double *x;      // input vector (modes 0, 1, 3)
+    const double *r;      // right-hand side / residual
+    const double *od;     // omega * D^-1 (span)
+    const double *base;   // mode 4: materialised smoother iterate (or null -> od*r)
+    const double *ec;     // mode 4: coarse correction (level-1 vector)
+    const int32_t *aggp;  // mode 4: aggregate of each position (-1 = none)
+    double *y;            // output
+    double *partials;     // per-CTA dot partials
 };
 
-// ---- span (structured level 0) kernels --------------------------------
-// MODE 0: y = A x (+ partial x.y if DOT)
-// MODE 1: y = r - A x
-// MODE 2: y = r - A (odinv r)
-// MODE 3: y = x + odinv (r - A x) (+ partial r.y if DOT)
+// MODE 0: y = A x (+ partial x.y)
+// MODE 1: y = r - A x (+ partial y.y)
+// MODE 2: y = r - A (od r)            (implicit first Jacobi sweep + defect)
+// MODE 3: y = x + od (r - A x) (+ partial r.y)   (Jacobi sweep)
+// MODE 4: y = base + e - od (A e), e = T ec      (matrix-free prolongation
+//         with P = (I - omega D^-1 A) T; base = od r when null)
 template <int R, int MODE, bool DOT>
-__global__ void __launch_bounds__(kSpanThreads) k_span(SpanView v, const double *__restrict__ x,
-                                                       const double *__restrict__ r,
-                                                       const double *__restrict__ od, double *__restrict__ y,
-                                                       double *__restrict__ partials) {
+__global__ void __launch_bounds__(kSpanThreads) k_span(SpanView v, SpanArgs a) {
+    using W = V<R>;
+    using T = typename W::T;
     __shared__ double red[32 * R];
-    int t = blockIdx.x;
-    int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
+    const int t = blockIdx.x;
+    const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
     double dot[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) dot[c] = 0.0;
-#pragma unroll
+    int row = r0;
     for (int u = 0; u < kTile / kSpanThreads; ++u) {
-        int p = t * kTile + u * kSpanThreads + threadIdx.x;
-        if (p < v.L) {
-            int row = frow(v.rows, r0, r1, p);
-            int4 q = v.rows[row];
-            int i = q.y + (p - q.x);
-            double s[R];
-            if (MODE == 2) stencil_at<R>(v, p, row, i, q, ScaledX{od, r, R}, s);
-            else stencil_at<R>(v, p, row, i, q, ArrX{x, R}, s);
-            bool dof = mbit(v.mask, p);
+        const int p = t * kTile + u * kSpanThreads + threadIdx.x;
+        if (p >= v.L) break;
+        row = frow(v.rows, row, r1, p);
+        const int4 q = v.rows[row];
+        const Nbr n = neighbours(v, p, row, q);
+        const bool dof = mbit(v.mask, p);
+        T out;
+        if (MODE == 2) {
+            const double *od = a.od, *rr = a.r;
+            T s = apply_row<R>(n, p, [&](int pp) { return W::scale(od[pp], W::ld(rr, pp)); });
+            out = W::sub(W::ld(rr, p), s);
+        } else if (MODE == 4) {
+            const double *ec = a.ec;
+            const int32_t *ag = a.aggp;
+            auto eat = [&](int pp) {
+                int g = ag[pp];
+                return g >= 0 ? W::ld(ec, g) : W::zero();
+            };
+            T s = apply_row<R>(n, p, eat);
+            T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
+            out = W::sub(W::add(b, eat(p)), W::scale(a.od[p], s));
+        } else {
+            const double *xx = a.x;
+            T s = apply_row<R>(n, p, [&](int pp) { return W::ld(xx, pp); });
+            if (MODE == 0) out = s;
+            else if (MODE == 1) out = W::sub(W::ld(a.r, p), s);
+            else out = W::add(W::ld(xx, p), W::scale(a.od[p], W::sub(W::ld(a.r, p), s)));
+        }
+        if (!dof) out = W::zero();
+        W::st(a.y, p, out);
+        if (DOT) {
 #pragma unroll
             for (int c = 0; c < R; ++c) {
-                double out;
-                int64_t e = (int64_t)p * R + c;
-                if (MODE == 0) out = s[c];
-                else if (MODE == 1 || MODE == 2) out = r[e] - s[c];
-                else out = x[e] + od[p] * (r[e] - s[c]);
-                out = dof ? out : 0.0;
-                y[e] = out;
-                if (DOT) {
-                    if (MODE == 0) dot[c] += x[e] * out;
-                    else if (MODE == 3) dot[c] += r[e] * out;
-                    else dot[c] += out * out;
-                }
+                if (MODE == 0) dot[c] += W::dot(W::ld(a.x, p), out, c);
+                else if (MODE == 3) dot[c] += W::dot(W::ld(a.r, p), out, c);
+                else dot[c] += W::dot(out, out, c);
             }
         }
     }
@@ -127,7 +182,19 @@ __global__ void __launch_bounds__(kSpanThreads) k_span(SpanView v, const double 
         block_sum<R>(dot, red);
         if (threadIdx.x == 0)
 #pragma unroll
-            for (int c = 0; c < R; ++c) partials[blockIdx.x * R + c] = dot[c];
+            for (int c = 0; c < R; ++c) a.partials[blockIdx.x * R + c] = dot[c];
+    }
+}
+
+// Restriction r_c = T^T u: sequential sum over each aggregate's member
+// positions (ascending) -- deterministic, no atomics.
+template <int R>
+__global__ void k_agg_sum(const int64_t *mptr, const int32_t *mpos, int64_t n_agg, const double *u, double *rc) {
+    using W = V<R>;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_agg; g += (int64_t)gridDim.x * blockDim.x) {
+        typename W::T s = W::zero();
+        for (int64_t q = mptr[g]; q < mptr[g + 1]; ++q) s = W::add(s, W::ld(u, mpos[q]));
+        W::st(rc, g, s);
     }
 }
 
@@ -422,18 +489,18 @@ int level0_apply(Amg &h, int mode, bool dot, const double *x, const double *r, d
         SpanView v = span_view(*h.op);
         int g = (int)h.op->n_tiles;
         if (g == 0) return 0;
-        const double *od = L.odinv.get();
+        SpanArgs sa{x, r, L.odinv.get(), nullptr, nullptr, nullptr, y, part};
         if (mode == 0) {
-            if (dot) k_span<R, 0, true><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
-            else k_span<R, 0, false><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+            if (dot) k_span<R, 0, true><<<g, kSpanThreads, 0, s>>>(v, sa);
+            else k_span<R, 0, false><<<g, kSpanThreads, 0, s>>>(v, sa);
         } else if (mode == 1) {
-            if (dot) k_span<R, 1, true><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
-            else k_span<R, 1, false><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+            if (dot) k_span<R, 1, true><<<g, kSpanThreads, 0, s>>>(v, sa);
+            else k_span<R, 1, false><<<g, kSpanThreads, 0, s>>>(v, sa);
         } else if (mode == 2) {
-            k_span<R, 2, false><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+            k_span<R, 2, false><<<g, kSpanThreads, 0, s>>>(v, sa);
         } else {
-            if (dot) k_span<R, 3, true><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
-            else k_span<R, 3, false><<<g, kSpanThreads, 0, s>>>(v, x, r, od, y, part);
+            if (dot) k_span<R, 3, true><<<g, kSpanThreads, 0, s>>>(v, sa);
+            else k_span<R, 3, false><<<g, kSpanThreads, 0, s>>>(v, sa);
         }
         SPFD_LAUNCH_CHECK();
         return g;
@@ -464,6 +531,57 @@ void level_apply(Amg &h, int l, int mode, const double *x, const double *r, doub
 }
 
 template <int R>
+void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s);
+
+// Fine level of a structured hierarchy, transfers matrix-free through the
+// aggregates (P = (I - omega D^-1 A) T, R = P^T):
+//   d  = r - A(od r)                      pre-smooth + defect
+//   u  = d - A(od d),  r_c = T^T u        restriction P^T d
+//   x1 = od r + e - od A e,  e = T e_c    prolongation + correction
+//   z  = x1 + od (r - A x1)               post-smooth
+template <int R>
+void vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
+    Level &L = h.lv[0];
+    Level &C = h.lv[1];
+    SpanView v = span_view(*h.op);
+    const int g = (int)h.op->n_tiles;
+    double *d = L.vd.get(), *t = L.vt.get(), *u = L.vr.get();
+    const size_t bytes = (size_t)L.nvec * R * sizeof(double);
+    const double *od = L.odinv.get();
+    const double *xbase = nullptr;
+    if (h.pre <= 1) {
+        k_span<R, 2, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{nullptr, r, od, nullptr, nullptr, nullptr, d, nullptr});
+    } else {
+        k_odinv_r<R><<<grid_for(L.nvec, 256, 148 * 16), 256, 0, s>>>(L.nvec, od, r, t);
+        for (int it = 1; it < h.pre; ++it) {
+            k_span<R, 3, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{t, r, od, nullptr, nullptr, nullptr, d, nullptr});
+            SPFD_CUDA(cudaMemcpyAsync(t, d, bytes, cudaMemcpyDeviceToDevice, s));
+        }
+        k_span<R, 1, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{t, r, od, nullptr, nullptr, nullptr, d, nullptr});
+        xbase = t;
+    }
+    SPFD_LAUNCH_CHECK();
+    k_span<R, 2, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr});
+    SPFD_LAUNCH_CHECK();
+    k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n, u, C.vr.get());
+    SPFD_LAUNCH_CHECK();
+    vcycle_level<R>(h, 1, C.vr.get(), C.vx.get(), s);
+    k_span<R, 4, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr});
+    SPFD_LAUNCH_CHECK();
+    if (h.post == 0) {
+        SPFD_CUDA(cudaMemcpyAsync(z, d, bytes, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    const double *cur = d;
+    for (int it = 0; it < h.post; ++it) {
+        double *dst = (it == h.post - 1) ? z : (cur == d ? t : d);
+        k_span<R, 3, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{cur, r, od, nullptr, nullptr, nullptr, dst, nullptr});
+        SPFD_LAUNCH_CHECK();
+        cur = dst;
+    }
+}
+
+template <int R>
 void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
     int nl = (int)h.lv.size();
     Level &L = h.lv[l];
@@ -480,6 +598,10 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
             k_dense_mv<R><<<grid_for(h.nc * 32, 256, 148 * 8), 256, 0, s>>>(h.cinv.get(), h.nc, r, z);
         }
         SPFD_LAUNCH_CHECK();
+        return;
+    }
+    if (l == 0 && h.structured) {
+        vcycle_fine_mf<R>(h, r, z, s);
         return;
     }
     double *d = L.vd.get(), *t = L.vt.get();
