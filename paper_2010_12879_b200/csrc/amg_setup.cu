@@ -570,7 +570,7 @@ __global__ void k_agg_pos(const int32_t *pos_to_dof, int64_t L, const int32_t *a
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L;
          p += (int64_t)gridDim.x * blockDim.x) {
         int d = pos_to_dof[p];
-        out[p] = d >= 0 ? agg[d] : -1;
+        out[p] = d >= 0 ? agg[d] + 1 : 0;  // aggregate id + 1, 0 = none
     }
 }
 

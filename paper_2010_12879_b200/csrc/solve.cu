@@ -6,6 +6,8 @@
 // solves are bitwise identical (test_linsolve.py:157-166).
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "amg.cuh"
 
@@ -120,6 +122,20 @@ struct SpanArgs {
     double *y;            // output
     double *partials;     // per-CTA dot partials
 };
+
+// Input of a fine-level stencil at a position, per mode (see k_span).
+template <int R, int MODE>
+__device__ __forceinline__ typename V<R>::T xin(const SpanArgs &a, int pp) {
+    using W = V<R>;
+    if (MODE == 2) return W::scale(a.od[pp], W::ld(a.r, pp));
+    if (MODE == 4) {
+        int g1 = a.aggp[pp];  // aggregate id + 1, 0 = none
+        return g1 > 0 ? W::ld(a.ec, g1 - 1) : W::zero();
+    }
+    return W::ld(a.x, pp);
+}
+
+#include "plane.cuh"
 
 // MODE 0: y = A x (+ partial x.y)
 // MODE 1: y = r - A x (+ partial y.y)
@@ -480,29 +496,71 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
 
 namespace {
 
+bool use_plane_kernel() {
+    static int v = -1;
+    if (v < 0) {
+        // the 2.5-D plane kernel is experimental (latency-bound at 1-2
+        // CTAs/SM); the flat span kernel is the default
+        const char *e = getenv("SPFD_SPAN_KERNEL");
+        v = (e && std::string(e) == "plane") ? 1 : 0;
+    }
+    return v == 1;
+}
+
+template <int R, int MODE>
+PlaneGeo plane_geometry(const Operator &op) {
+    size_t per = (size_t)kPlaneSlots * (kPlaneJB + 2) * op.NX * PlaneStage<R, MODE>::bytes + 64;
+    int cps = (int)((227 * 1024) / (per + 1024));
+    if (cps > 8) cps = 8;
+    if (cps < 1) cps = 1;
+    return plane_geo(op, cps);
+}
+
+// Launch one fine-level stencil pass (flat span kernel; the 2.5-D plane
+// kernel with SPFD_SPAN_KERNEL=plane).  Returns the number of CTAs (dot
+// partials written when DOT).
+template <int R, int MODE, bool DOT>
+int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
+    SpanView v = span_view(op);
+    if (!use_plane_kernel()) {
+        int g = (int)op.n_tiles;
+        if (g > 0) k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
+        SPFD_LAUNCH_CHECK();
+        return g;
+    }
+    static int max_dyn = -1;
+    if (max_dyn < 0) {
+        int dev = 0, optin = 0;
+        SPFD_CUDA(cudaGetDevice(&dev));
+        SPFD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        cudaFuncAttributes fa;
+        SPFD_CUDA(cudaFuncGetAttributes(&fa, k_plane<R, MODE, DOT>));
+        max_dyn = optin - (int)fa.sharedSizeBytes;
+        SPFD_CUDA(cudaFuncSetAttribute(k_plane<R, MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
+    }
+    PlaneGeo g = plane_geometry<R, MODE>(op);
+    size_t smem = plane_smem<R, MODE>(g);
+    SPFD_CHECK(smem <= (size_t)max_dyn, SPFD_EINVAL, "x-extent too large for the plane kernel");
+    int grid = g.jblocks * g.kblocks;
+    k_plane<R, MODE, DOT><<<grid, kPlaneThreads, smem, s>>>(v, g, a);
+    SPFD_LAUNCH_CHECK();
+    return grid;
+}
+
 // returns number of partial blocks written when DOT
 template <int R>
 int level0_apply(Amg &h, int mode, bool dot, const double *x, const double *r, double *y, cudaStream_t s) {
     Level &L = h.lv[0];
     double *part = h.partials.get();
     if (h.structured) {
-        SpanView v = span_view(*h.op);
         int g = (int)h.op->n_tiles;
         if (g == 0) return 0;
         SpanArgs sa{x, r, L.odinv.get(), nullptr, nullptr, nullptr, y, part};
-        if (mode == 0) {
-            if (dot) k_span<R, 0, true><<<g, kSpanThreads, 0, s>>>(v, sa);
-            else k_span<R, 0, false><<<g, kSpanThreads, 0, s>>>(v, sa);
-        } else if (mode == 1) {
-            if (dot) k_span<R, 1, true><<<g, kSpanThreads, 0, s>>>(v, sa);
-            else k_span<R, 1, false><<<g, kSpanThreads, 0, s>>>(v, sa);
-        } else if (mode == 2) {
-            k_span<R, 2, false><<<g, kSpanThreads, 0, s>>>(v, sa);
-        } else {
-            if (dot) k_span<R, 3, true><<<g, kSpanThreads, 0, s>>>(v, sa);
-            else k_span<R, 3, false><<<g, kSpanThreads, 0, s>>>(v, sa);
-        }
-        SPFD_LAUNCH_CHECK();
+        const Operator &op = *h.op;
+        if (mode == 0) g = dot ? launch_fine<R, 0, true>(op, sa, s) : launch_fine<R, 0, false>(op, sa, s);
+        else if (mode == 1) g = dot ? launch_fine<R, 1, true>(op, sa, s) : launch_fine<R, 1, false>(op, sa, s);
+        else if (mode == 2) g = launch_fine<R, 2, false>(op, sa, s);
+        else g = dot ? launch_fine<R, 3, true>(op, sa, s) : launch_fine<R, 3, false>(op, sa, s);
         return g;
     }
     const double *od = L.odinv.get();
@@ -550,23 +608,23 @@ void vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
     const double *od = L.odinv.get();
     const double *xbase = nullptr;
     if (h.pre <= 1) {
-        k_span<R, 2, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{nullptr, r, od, nullptr, nullptr, nullptr, d, nullptr});
+        launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, r, od, nullptr, nullptr, nullptr, d, nullptr}, s);
     } else {
         k_odinv_r<R><<<grid_for(L.nvec, 256, 148 * 16), 256, 0, s>>>(L.nvec, od, r, t);
         for (int it = 1; it < h.pre; ++it) {
-            k_span<R, 3, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{t, r, od, nullptr, nullptr, nullptr, d, nullptr});
+            launch_fine<R, 3, false>(*h.op, SpanArgs{t, r, od, nullptr, nullptr, nullptr, d, nullptr}, s);
             SPFD_CUDA(cudaMemcpyAsync(t, d, bytes, cudaMemcpyDeviceToDevice, s));
         }
-        k_span<R, 1, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{t, r, od, nullptr, nullptr, nullptr, d, nullptr});
+        launch_fine<R, 1, false>(*h.op, SpanArgs{t, r, od, nullptr, nullptr, nullptr, d, nullptr}, s);
         xbase = t;
     }
     SPFD_LAUNCH_CHECK();
-    k_span<R, 2, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr});
+    launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr}, s);
     SPFD_LAUNCH_CHECK();
     k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n, u, C.vr.get());
     SPFD_LAUNCH_CHECK();
     vcycle_level<R>(h, 1, C.vr.get(), C.vx.get(), s);
-    k_span<R, 4, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr});
+    launch_fine<R, 4, false>(*h.op, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr}, s);
     SPFD_LAUNCH_CHECK();
     if (h.post == 0) {
         SPFD_CUDA(cudaMemcpyAsync(z, d, bytes, cudaMemcpyDeviceToDevice, s));
@@ -575,7 +633,7 @@ void vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
     const double *cur = d;
     for (int it = 0; it < h.post; ++it) {
         double *dst = (it == h.post - 1) ? z : (cur == d ? t : d);
-        k_span<R, 3, false><<<g, kSpanThreads, 0, s>>>(v, SpanArgs{cur, r, od, nullptr, nullptr, nullptr, dst, nullptr});
+        launch_fine<R, 3, false>(*h.op, SpanArgs{cur, r, od, nullptr, nullptr, nullptr, dst, nullptr}, s);
         SPFD_LAUNCH_CHECK();
         cur = dst;
     }
