@@ -34,7 +34,7 @@ struct Level {
     Csr P, R;                 // solve-layout prolongation / restriction
     Csr P_dof, R_dof;         // DOF-numbered copies (structured level 0 only; exports)
     DevBuf<int32_t> agg;      // aggregate per row (DOF numbering)
-    DevBuf<int32_t> agg_pos;  // structured level 0: aggregate per span position (-1 = none)
+    DevBuf<int32_t> agg_pos;  // structured level 0: aggregate id + 1 per span position (0 = none)
     DevBuf<int64_t> mem_ptr;  // structured level 0: aggregate -> member positions (CSR of T^T)
     DevBuf<int32_t> mem_pos;
     DevBuf<double> dinv;      // [nvec]
@@ -59,6 +59,7 @@ struct Amg {
     DevBuf<double> scal;      // device scalars
     DevBuf<double> fg_basis, fg_prec;  // FGMRES basis (allocated on demand)
     int64_t fg_m = 0;
+    int vc_partials = 0;      // r.z partials written by the last V-cycle (0 = none)
     int64_t device_bytes() const;
 };
 

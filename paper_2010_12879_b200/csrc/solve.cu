@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(kSpanThreads) k_span(SpanView v, SpanArgs a) {
             const double *ec = a.ec;
             const int32_t *ag = a.aggp;
             auto eat = [&](int pp) {
-                int g = ag[pp];
-                return g >= 0 ? W::ld(ec, g) : W::zero();
+                int g1 = ag[pp];  // aggregate id + 1, 0 = none
+                return g1 > 0 ? W::ld(ec, g1 - 1) : W::zero();
             };
             T s = apply_row<R>(n, p, eat);
             T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
@@ -203,25 +203,30 @@ __global__ void __launch_bounds__(kSpanThreads) k_span(SpanView v, SpanArgs a) {
 }
 
 // Restriction r_c = T^T u: sequential sum over each aggregate's member
-// positions (ascending) -- deterministic, no atomics.
+// positions (ascending) -- deterministic, no atomics.  Optionally also
+// writes x0_c = od_c * r_c, the next level's implicit first Jacobi sweep.
 template <int R>
-__global__ void k_agg_sum(const int64_t *mptr, const int32_t *mpos, int64_t n_agg, const double *u, double *rc) {
+__global__ void k_agg_sum(const int64_t *mptr, const int32_t *mpos, int64_t n_agg, const double *u, double *rc,
+                          const double *od_c, double *x0_c) {
     using W = V<R>;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_agg; g += (int64_t)gridDim.x * blockDim.x) {
         typename W::T s = W::zero();
         for (int64_t q = mptr[g]; q < mptr[g + 1]; ++q) s = W::add(s, W::ld(u, mpos[q]));
         W::st(rc, g, s);
+        if (x0_c) W::st(x0_c, g, W::scale(od_c[g], s));
     }
 }
 
 // ---- CSR kernels (G lanes per row) ------------------------------------
-// MODE 0: y = M x;  1: y = r - M x;  2: y = r - M(odinv r);
+// MODE 0: y = M x (aux: also od_aux * y);  1: y = r - M x;  2: y = r - M(odinv r);
 // MODE 3: y = x + odinv (r - M x);  4: y = odinv r + M e (prolongation, x=e)
 // MODE 5: y = base + M e (prolongation on a materialised smoother iterate)
 template <int G, int R, int MODE, bool DOT>
 __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__restrict__ r,
                       const double *__restrict__ od, const double *__restrict__ base, double *__restrict__ y,
-                      double *__restrict__ partials) {
+                      double *__restrict__ partials, const double *__restrict__ od_aux, double *__restrict__ aux) {
+    using W = V<R>;
+    using T = typename W::T;
     __shared__ double red[32 * R];
     const int lane = threadIdx.x % G;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -234,39 +239,41 @@ __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__r
     for (int64_t rbase = warp * GPW; rbase < m.rows; rbase += nwarp * GPW) {
         const int64_t row = rbase + (threadIdx.x & 31) / G;
         const bool valid = row < m.rows;
-        double acc[R];
-#pragma unroll
-        for (int c = 0; c < R; ++c) acc[c] = 0.0;
+        T acc = W::zero();
         if (valid) {
-            for (int64_t q = m.ptr[row] + lane; q < m.ptr[row + 1]; q += G) {
-                int col = m.col[q];
-                double a = m.val[q];
-#pragma unroll
-                for (int c = 0; c < R; ++c) {
-                    double xv = MODE == 2 ? od[col] * r[(int64_t)col * R + c] : x[(int64_t)col * R + c];
-                    acc[c] = fma(a, xv, acc[c]);
-                }
+            const int64_t q1 = m.ptr[row + 1];
+            for (int64_t q = m.ptr[row] + lane; q < q1; q += G) {
+                const int col = m.col[q];
+                const double a = m.val[q];
+                const T xv = MODE == 2 ? W::scale(od[col], W::ld(r, col)) : W::ld(x, col);
+                acc = W::fma_(a, xv, acc);
             }
         }
+        double ac[R];
 #pragma unroll
-        for (int c = 0; c < R; ++c)
+        for (int c = 0; c < R; ++c) {
+            ac[c] = W::comp(acc, c);
 #pragma unroll
-            for (int o = G / 2; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o, G);
+            for (int o = G / 2; o > 0; o >>= 1) ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], o, G);
+        }
         if (valid && lane == 0) {
+            T sum;
+            if constexpr (R == 1) sum = ac[0];
+            else sum = make_double2(ac[0], ac[1]);
+            T out;
+            if (MODE == 0) out = sum;
+            else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(r, row), sum);
+            else if (MODE == 3) out = W::add(W::ld(x, row), W::scale(od[row], W::sub(W::ld(r, row), sum)));
+            else if (MODE == 4) out = W::add(W::scale(od[row], W::ld(r, row)), sum);
+            else out = W::add(W::ld(base, row), sum);
+            W::st(y, row, out);
+            if (MODE == 0 && aux) W::st(aux, row, W::scale(od_aux[row], out));
+            if (DOT) {
 #pragma unroll
-            for (int c = 0; c < R; ++c) {
-                int64_t e = row * R + c;
-                double out;
-                if (MODE == 0) out = acc[c];
-                else if (MODE == 1 || MODE == 2) out = r[e] - acc[c];
-                else if (MODE == 3) out = x[e] + od[row] * (r[e] - acc[c]);
-                else if (MODE == 4) out = od[row] * r[e] + acc[c];
-                else out = base[e] + acc[c];
-                y[e] = out;
-                if (DOT) {
-                    if (MODE == 0) dot[c] += x[e] * out;
-                    else if (MODE == 3) dot[c] += r[e] * out;
-                    else dot[c] += out * out;
+                for (int c = 0; c < R; ++c) {
+                    if (MODE == 0) dot[c] += W::dot(W::ld(x, row), out, c);
+                    else if (MODE == 3) dot[c] += W::dot(W::ld(r, row), out, c);
+                    else dot[c] += W::dot(out, out, c);
                 }
             }
         }
@@ -290,19 +297,19 @@ inline int csr_grid(int64_t rows, int G) {
 
 template <int G, int R, int MODE, bool DOT>
 void launch_csr_g(const Csr &m, const double *x, const double *r, const double *od, const double *base, double *y,
-                  double *partials, cudaStream_t s, int grid) {
-    k_csr<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials);
+                  double *partials, cudaStream_t s, int grid, const double *od_aux, double *aux) {
+    k_csr<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials, od_aux, aux);
 }
 
 template <int R, int MODE, bool DOT>
 int launch_csr(const Csr &m, int G, const double *x, const double *r, const double *od, const double *base,
-               double *y, double *partials, cudaStream_t s) {
+               double *y, double *partials, cudaStream_t s, const double *od_aux = nullptr, double *aux = nullptr) {
     int grid = csr_grid(m.rows, G);
     switch (G) {
-        case 4: launch_csr_g<4, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid); break;
-        case 8: launch_csr_g<8, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid); break;
-        case 16: launch_csr_g<16, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid); break;
-        default: launch_csr_g<32, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid); break;
+        case 4: launch_csr_g<4, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux); break;
+        case 8: launch_csr_g<8, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux); break;
+        case 16: launch_csr_g<16, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux); break;
+        default: launch_csr_g<32, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux); break;
     }
     SPFD_LAUNCH_CHECK();
     return grid;
@@ -358,36 +365,44 @@ __global__ void k_odinv_r(int64_t n, const double *od, const double *r, double *
 // partial a.b per rhs (fixed grid)
 template <int R>
 __global__ void k_dot(int64_t n, const double *a, const double *b, double *partials) {
+    using W = V<R>;
     __shared__ double red[32 * R];
     double d[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) d[c] = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const typename W::T av = W::ld(a, i), bv = W::ld(b, i);
 #pragma unroll
-        for (int c = 0; c < R; ++c) d[c] = fma(a[i * R + c], b[i * R + c], d[c]);
+        for (int c = 0; c < R; ++c) d[c] = fma(W::comp(av, c), W::comp(bv, c), d[c]);
+    }
     block_sum<R>(d, red);
     if (threadIdx.x == 0)
 #pragma unroll
         for (int c = 0; c < R; ++c) partials[blockIdx.x * R + c] = d[c];
 }
 
+template <int R>
+__device__ __forceinline__ typename V<R>::T vfma(const double (&a)[R], typename V<R>::T x, typename V<R>::T y) {
+    if constexpr (R == 1) return fma(a[0], x, y);
+    else return make_double2(fma(a[0], x.x, y.x), fma(a[1], x.y, y.y));
+}
+
 // x += alpha p ; r -= alpha q ; partial r.r
 template <int R>
 __global__ void k_update_xr(int64_t n, const double *scal, double *x, double *r, const double *p, const double *q,
                             double *partials) {
+    using W = V<R>;
     __shared__ double red[32 * R];
-    double a[R], d[R];
+    double a[R], na[R], d[R];
 #pragma unroll
-    for (int c = 0; c < R; ++c) { a[c] = scal[S_ALPHA + c]; d[c] = 0.0; }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int c = 0; c < R; ++c) { a[c] = scal[S_ALPHA + c]; na[c] = -a[c]; d[c] = 0.0; }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        W::st(x, i, vfma<R>(a, W::ld(p, i), W::ld(x, i)));
+        const typename W::T rv = vfma<R>(na, W::ld(q, i), W::ld(r, i));
+        W::st(r, i, rv);
 #pragma unroll
-        for (int c = 0; c < R; ++c) {
-            int64_t e = i * R + c;
-            x[e] = fma(a[c], p[e], x[e]);
-            double rv = fma(-a[c], q[e], r[e]);
-            r[e] = rv;
-            d[c] = fma(rv, rv, d[c]);
-        }
+        for (int c = 0; c < R; ++c) d[c] = fma(W::comp(rv, c), W::comp(rv, c), d[c]);
+    }
     block_sum<R>(d, red);
     if (threadIdx.x == 0)
 #pragma unroll
@@ -397,12 +412,12 @@ __global__ void k_update_xr(int64_t n, const double *scal, double *x, double *r,
 // p = z + beta p
 template <int R>
 __global__ void k_xpby(int64_t n, const double *scal, const double *z, double *p) {
+    using W = V<R>;
     double b[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) b[c] = scal[S_BETA + c];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-#pragma unroll
-        for (int c = 0; c < R; ++c) p[i * R + c] = fma(b[c], p[i * R + c], z[i * R + c]);
+        W::st(p, i, vfma<R>(b, W::ld(p, i), W::ld(z, i)));
 }
 
 // Sum per-CTA partials in index order; then apply `what`.
@@ -597,8 +612,10 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s);
 //   u  = d - A(od d),  r_c = T^T u        restriction P^T d
 //   x1 = od r + e - od A e,  e = T e_c    prolongation + correction
 //   z  = x1 + od (r - A x1)               post-smooth
+// Returns the number of CTA partials of r.z written by the last sweep
+// (0 if none), so PCG needs no separate dot pass.
 template <int R>
-void vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
+int vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
     Level &L = h.lv[0];
     Level &C = h.lv[1];
     SpanView v = span_view(*h.op);
@@ -621,22 +638,29 @@ void vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
     SPFD_LAUNCH_CHECK();
     launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr}, s);
     SPFD_LAUNCH_CHECK();
-    k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n, u, C.vr.get());
+    // level 1 gets r_1 and (when it smooths) its first Jacobi iterate od_1 r_1
+    const bool x0 = h.pre <= 1 && (int)h.lv.size() > 2;
+    k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n, u, C.vr.get(),
+                                                             C.odinv.get(), x0 ? C.vt.get() : nullptr);
     SPFD_LAUNCH_CHECK();
     vcycle_level<R>(h, 1, C.vr.get(), C.vx.get(), s);
     launch_fine<R, 4, false>(*h.op, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr}, s);
     SPFD_LAUNCH_CHECK();
     if (h.post == 0) {
         SPFD_CUDA(cudaMemcpyAsync(z, d, bytes, cudaMemcpyDeviceToDevice, s));
-        return;
+        return 0;
     }
     const double *cur = d;
+    int parts = 0;
     for (int it = 0; it < h.post; ++it) {
-        double *dst = (it == h.post - 1) ? z : (cur == d ? t : d);
-        launch_fine<R, 3, false>(*h.op, SpanArgs{cur, r, od, nullptr, nullptr, nullptr, dst, nullptr}, s);
-        SPFD_LAUNCH_CHECK();
+        const bool last = it == h.post - 1;
+        double *dst = last ? z : (cur == d ? t : d);
+        SpanArgs sa{cur, r, od, nullptr, nullptr, nullptr, dst, h.partials.get()};
+        if (last) parts = launch_fine<R, 3, true>(*h.op, sa, s);
+        else launch_fine<R, 3, false>(*h.op, sa, s);
         cur = dst;
     }
+    return parts;
 }
 
 template <int R>
@@ -659,15 +683,17 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
         return;
     }
     if (l == 0 && h.structured) {
-        vcycle_fine_mf<R>(h, r, z, s);
+        h.vc_partials = vcycle_fine_mf<R>(h, r, z, s);
         return;
     }
     double *d = L.vd.get(), *t = L.vt.get();
     const size_t bytes = (size_t)L.nvec * R * sizeof(double);
     const double *xbase = nullptr;  // materialised pre-smoothed iterate (pre >= 2)
     if (h.pre <= 1) {
-        // implicit first sweep x = omega D^-1 r, defect d = r - A x (linsolve.py:190-193)
-        level_apply<R>(h, l, 2, nullptr, r, d, s);
+        // implicit first sweep x = omega D^-1 r, defect d = r - A x (linsolve.py:190-193);
+        // on coarse levels the restriction already wrote x = od r into vt
+        if (l > 0) level_apply<R>(h, l, 1, t, r, d, s);
+        else level_apply<R>(h, l, 2, nullptr, r, d, s);
     } else {
         k_odinv_r<R><<<grid_for(L.nvec, 256, 148 * 16), 256, 0, s>>>(L.nvec, L.odinv.get(), r, t);
         for (int it = 1; it < h.pre; ++it) {
@@ -678,7 +704,9 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
         xbase = t;
     }
     Level &C = h.lv[l + 1];
-    launch_csr<R, 0, false>(L.R, L.r_group, d, nullptr, nullptr, nullptr, C.vr.get(), nullptr, s);
+    const bool x0 = h.pre <= 1 && l + 1 < nl - 1;
+    launch_csr<R, 0, false>(L.R, L.r_group, d, nullptr, nullptr, nullptr, C.vr.get(), nullptr, s, C.odinv.get(),
+                            x0 ? C.vt.get() : nullptr);
     vcycle_level<R>(h, l + 1, C.vr.get(), C.vx.get(), s);
     // x1 = x + P e (linsolve.py:194) -> d
     if (xbase) launch_csr<R, 5, false>(L.P, L.p_group, C.vx.get(), r, L.odinv.get(), xbase, d, nullptr, s);
@@ -699,6 +727,7 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
 }  // namespace
 
 void amg_vcycle(Amg &h, const double *r, double *z, int nrhs, cudaStream_t s) {
+    h.vc_partials = 0;
     if (nrhs == 1) vcycle_level<1>(h, 0, r, z, s);
     else vcycle_level<2>(h, 0, r, z, s);
 }
@@ -752,7 +781,8 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
             level0_apply<R>(h, 1, false, x, b, r, s);
             SPFD_CUDA(cudaMemcpyAsync(sc + S_ACTIVE, ones, R * sizeof(double), cudaMemcpyHostToDevice, s));
             amg_vcycle(h, r, z, R, s);
-            dot<R>(h, n, r, z, S_RZ, F_BETA_INIT, s);
+            if (h.vc_partials > 0) finalize<R>(h, h.vc_partials, S_RZ, F_BETA_INIT, s);
+            else dot<R>(h, n, r, z, S_RZ, F_BETA_INIT, s);
             SPFD_CUDA(cudaMemcpyAsync(p, z, n * R * sizeof(double), cudaMemcpyDeviceToDevice, s));
             restart = false;
         }
@@ -793,7 +823,8 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
             continue;
         }
         amg_vcycle(h, r, z, R, s);
-        dot<R>(h, n, r, z, S_RZ, F_BETA, s);
+        if (h.vc_partials > 0) finalize<R>(h, h.vc_partials, S_RZ, F_BETA, s);  // r.z fused into the post-smooth
+        else dot<R>(h, n, r, z, S_RZ, F_BETA, s);
         k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p);
         SPFD_LAUNCH_CHECK();
     }
