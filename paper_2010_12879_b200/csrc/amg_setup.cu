@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <chrono>
+#include <cstdlib>
 
 #include "amg.cuh"
 
@@ -608,12 +609,19 @@ void build_members(const int32_t *agg, int64_t n, int64_t n_agg, const int32_t *
     scan_excl(cnt.get(), mptr.get(), n_agg + 1, s);
 }
 
+// lanes per row of the CSR kernels: small groups keep the per-row
+// reduction/epilogue overhead low (the coarse rows hold ~10-40 entries)
 int pick_group(int64_t nnz, int64_t rows) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char *e = getenv("SPFD_CSR_GROUP");
+        forced = e ? atoi(e) : 0;
+    }
+    if (forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
     double avg = rows > 0 ? (double)nnz / (double)rows : 1.0;
-    if (avg <= 6.0) return 4;
-    if (avg <= 14.0) return 8;
-    if (avg <= 28.0) return 16;
-    return 32;
+    if (avg <= 12.0) return 4;
+    if (avg <= 48.0) return 8;
+    return 16;
 }
 
 // One coarsening step on level l (CSR A in level numbering).  Returns false
