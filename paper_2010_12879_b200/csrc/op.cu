@@ -206,6 +206,24 @@ __global__ void k_tile_rows(const int4 *rows, int64_t n_rows, int64_t n_tiles, i
     }
 }
 
+// Warp work items: every row is cut into chunks of 32 consecutive positions.
+__global__ void k_item_count(const int4 *rows, int64_t n_rows, int *cnt) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int len = rows[r].z - rows[r].y;
+        cnt[r] = (len + 31) / 32;
+    }
+}
+
+__global__ void k_item_fill(const int4 *rows, int64_t n_rows, const int *off, int2 *items) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int len = rows[r].z - rows[r].y;
+        int o = off[r];
+        for (int s = 0; s < len; s += 32) items[o++] = make_int2((int)r, s);
+    }
+}
+
 // Sum of the <= 4 voxel conductivities around an edge in the reference's
 // (da, db) order, then *0.25, then *geom (fit_operators.py:289-324).
 __device__ __forceinline__ double kap(const uint16_t *ids, const double *lut, Geo g, int i, int j,
@@ -476,6 +494,19 @@ Operator *op_create(const int64_t *dims, const double *spacing, const uint16_t *
         op->rows.alloc(op->n_rows + 1);
         k_rows_pack<<<grid_for(op->n_rows + 1, T), T, 0, s>>>(lo.get(), hi.get(), off.get(), op->n_rows,
                                                              op->L, (int)op->NY, op->rows.get());
+        {
+            DevBuf<int> icnt, ioff;
+            icnt.alloc(op->n_rows + 1);
+            ioff.alloc(op->n_rows + 1);
+            SPFD_CUDA(cudaMemsetAsync(icnt.get() + op->n_rows, 0, sizeof(int), s));
+            k_item_count<<<grid_for(op->n_rows, T), T, 0, s>>>(op->rows.get(), op->n_rows, icnt.get());
+            SPFD_LAUNCH_CHECK();
+            exclusive_scan(icnt.get(), ioff.get(), op->n_rows + 1, s);
+            op->n_items = read_scalar(ioff.get() + op->n_rows, s);
+            op->items.alloc(op->n_items + 1);
+            k_item_fill<<<grid_for(op->n_rows, T), T, 0, s>>>(op->rows.get(), op->n_rows, ioff.get(), op->items.get());
+            SPFD_LAUNCH_CHECK();
+        }
         op->n_tiles = (op->L + kTile - 1) / kTile;
         op->tile_row.alloc(op->n_tiles + 1);
         k_tile_rows<<<grid_for(op->n_tiles + 1, T), T, 0, s>>>(op->rows.get(), op->n_rows, op->n_tiles,

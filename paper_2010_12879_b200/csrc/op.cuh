@@ -28,6 +28,8 @@ struct Operator {
 
     DevBuf<int4> rows;               // [n_rows+1] {off, lo, hi, j|k<<?>}  (sentinel at end)
     DevBuf<int32_t> tile_row;        // [n_tiles+1] first row of each tile
+    DevBuf<int2> items;              // [n_items] (row, first column offset) warp work items
+    int64_t n_items = 0;
     DevBuf<double> wx, wy, wz;       // [L] edge conductance of the +axis edge at each position
     DevBuf<double> diag;             // [L] reference-order diagonal (0 for non-DOF)
     DevBuf<double> dinv;             // [L] 1/diag (0 for non-DOF)
@@ -41,7 +43,7 @@ struct Operator {
     DevBuf<double> ws_a, ws_b;       // span workspaces [L*2]
 
     int64_t device_bytes() const {
-        return rows.bytes() + tile_row.bytes() + wx.bytes() + wy.bytes() + wz.bytes() +
+        return rows.bytes() + tile_row.bytes() + items.bytes() + wx.bytes() + wy.bytes() + wz.bytes() +
                diag.bytes() + dinv.bytes() + dofmask.bytes() + pos_to_dof.bytes() +
                dof_to_pos.bytes() + pinned.bytes() + vox_cond.bytes() + vrow_off.bytes() +
                nnz_row.bytes() + ws_a.bytes() + ws_b.bytes();
@@ -52,6 +54,8 @@ struct Operator {
 struct SpanView {
     const int4 *rows;
     const int32_t *tile_row;
+    const int2 *items;       // warp items: 32 consecutive positions of one row
+    int64_t n_items;
     const double *wx, *wy, *wz;
     const uint32_t *mask;
     int64_t L;
@@ -60,7 +64,7 @@ struct SpanView {
 };
 
 inline SpanView span_view(const Operator &op) {
-    return SpanView{op.rows.get(), op.tile_row.get(), op.wx.get(), op.wy.get(), op.wz.get(),
+    return SpanView{op.rows.get(), op.tile_row.get(), op.items.get(), op.n_items, op.wx.get(), op.wy.get(), op.wz.get(),
                     op.dofmask.get(), op.L, (int)op.NY, (int)op.n_rows};
 }
 

@@ -144,7 +144,7 @@ __device__ __forceinline__ typename V<R>::T xin(const SpanArgs &a, int pp) {
 // MODE 4: y = base + e - od (A e), e = T ec      (matrix-free prolongation
 //         with P = (I - omega D^-1 A) T; base = od r when null)
 template <int R, int MODE, bool DOT>
-__global__ void __launch_bounds__(kSpanThreads) k_span(SpanView v, SpanArgs a) {
+__global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a) {
     using W = V<R>;
     using T = typename W::T;
     __shared__ double red[32 * R];
@@ -191,6 +191,113 @@ __global__ void __launch_bounds__(kSpanThreads) k_span(SpanView v, SpanArgs a) {
                 if (MODE == 0) dot[c] += W::dot(W::ld(a.x, p), out, c);
                 else if (MODE == 3) dot[c] += W::dot(W::ld(a.r, p), out, c);
                 else dot[c] += W::dot(out, out, c);
+            }
+        }
+    }
+    if (DOT) {
+        block_sum<R>(dot, red);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int c = 0; c < R; ++c) a.partials[blockIdx.x * R + c] = dot[c];
+    }
+}
+
+template <class T>
+__device__ __forceinline__ T shfl_up1(T v);
+template <>
+__device__ __forceinline__ double shfl_up1<double>(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+template <>
+__device__ __forceinline__ double2 shfl_up1<double2>(double2 v) {
+    return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+template <class T>
+__device__ __forceinline__ T shfl_dn1(T v);
+template <>
+__device__ __forceinline__ double shfl_dn1<double>(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+template <>
+__device__ __forceinline__ double2 shfl_dn1<double2>(double2 v) {
+    return make_double2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+
+// Row-chunk kernel: each warp takes work items of 32 consecutive positions
+// of ONE row, so the row record and the four neighbour-row records are
+// warp-uniform (broadcast) loads, every neighbour access is a contiguous
+// (coalesced) run, and the +-x neighbours come from lane shuffles.  Same
+// MODEs and the same reference-order arithmetic as k_span.
+template <int R, int MODE, bool DOT>
+__global__ void __launch_bounds__(256) k_items(SpanView v, SpanArgs a) {
+    using W = V<R>;
+    using T = typename W::T;
+    constexpr unsigned FULL = 0xffffffffu;
+    __shared__ double red[32 * R];
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double dot[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) dot[c] = 0.0;
+    for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < v.n_items; it += nwarp) {
+        const int2 item = v.items[it];
+        const int r = item.x;
+        const int4 q = v.rows[r];
+        const int j = q.w;
+        const int4 qym = j > 0 ? v.rows[r - 1] : make_int4(0, 0, 0, 0);
+        const int4 qyp = j + 1 < v.NY ? v.rows[r + 1] : make_int4(0, 0, 0, 0);
+        const int4 qzm = r >= v.NY ? v.rows[r - v.NY] : make_int4(0, 0, 0, 0);
+        const int4 qzp = r + v.NY < v.n_rows ? v.rows[r + v.NY] : make_int4(0, 0, 0, 0);
+        const int i0 = q.y + item.y;
+        const int i = i0 + lane;
+        const bool on = i < q.z;
+        const int ic = on ? i : i0;            // inactive lanes mirror lane 0
+        const int p = q.x + (ic - q.y);
+        const bool hxm = ic > q.y, hxp = ic + 1 < q.z;
+        const double wxp = v.wx[p], wyp = v.wy[p], wzp = v.wz[p];
+        double wxm = __shfl_up_sync(FULL, wxp, 1);
+        if (lane == 0) wxm = hxm ? v.wx[p - 1] : 0.0;
+        if (!hxm) wxm = 0.0;
+        const int pym = (ic >= qym.y && ic < qym.z) ? qym.x + (ic - qym.y) : -1;
+        const int pyp = (ic >= qyp.y && ic < qyp.z) ? qyp.x + (ic - qyp.y) : -1;
+        const int pzm = (ic >= qzm.y && ic < qzm.z) ? qzm.x + (ic - qzm.y) : -1;
+        const int pzp = (ic >= qzp.y && ic < qzp.z) ? qzp.x + (ic - qzp.y) : -1;
+        const double wym = pym >= 0 ? v.wy[pym] : 0.0;
+        const double wzm = pzm >= 0 ? v.wz[pzm] : 0.0;
+        const T xc = xin<R, MODE>(a, p);
+        T xxm = shfl_up1(xc), xxp = shfl_dn1(xc);
+        if (lane == 0) xxm = hxm ? xin<R, MODE>(a, p - 1) : W::zero();
+        if (lane == 31 || !on) xxp = hxp ? xin<R, MODE>(a, p + 1) : W::zero();
+        if (!hxm) xxm = W::zero();
+        if (!hxp) xxp = W::zero();
+        const T xym = pym >= 0 ? xin<R, MODE>(a, pym) : W::zero();
+        const T xyp = pyp >= 0 ? xin<R, MODE>(a, pyp) : W::zero();
+        const T xzm = pzm >= 0 ? xin<R, MODE>(a, pzm) : W::zero();
+        const T xzp = pzp >= 0 ? xin<R, MODE>(a, pzp) : W::zero();
+        // reference diagonal order: tail edges x, y, z then head edges x, y, z
+        const double diag = add_rn(add_rn(add_rn(add_rn(add_rn(wxp, wyp), wzp), wxm), wym), wzm);
+        T s = W::zero();
+        s = W::axpy(-wzm, xzm, s);
+        s = W::axpy(-wym, xym, s);
+        s = W::axpy(-wxm, xxm, s);
+        s = W::axpy(diag, xc, s);
+        s = W::axpy(-wxp, xxp, s);
+        s = W::axpy(-wyp, xyp, s);
+        s = W::axpy(-wzp, xzp, s);
+        T out;
+        if (MODE == 0) out = s;
+        else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(a.r, p), s);
+        else if (MODE == 3) out = W::add(xc, W::scale(a.od[p], W::sub(W::ld(a.r, p), s)));
+        else {
+            const T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
+            out = W::sub(W::add(b, xc), W::scale(a.od[p], s));
+        }
+        if (!mbit(v.mask, p)) out = W::zero();
+        if (on) {
+            W::st(a.y, p, out);
+            if (DOT) {
+#pragma unroll
+                for (int c = 0; c < R; ++c) {
+                    if (MODE == 0) dot[c] += W::dot(xc, out, c);
+                    else if (MODE == 3) dot[c] += W::dot(W::ld(a.r, p), out, c);
+                    else dot[c] += W::dot(out, out, c);
+                }
             }
         }
     }
@@ -511,15 +618,17 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
 
 namespace {
 
-bool use_plane_kernel() {
+// 0 = row-chunk items, 1 = 2.5-D plane, 2 = flat per-position (default: the
+// highest occupancy and the best measured HBM throughput)
+int fine_kernel_kind() {
     static int v = -1;
     if (v < 0) {
         // the 2.5-D plane kernel is experimental (latency-bound at 1-2
         // CTAs/SM); the flat span kernel is the default
         const char *e = getenv("SPFD_SPAN_KERNEL");
-        v = (e && std::string(e) == "plane") ? 1 : 0;
+        v = (e && std::string(e) == "plane") ? 1 : ((e && std::string(e) == "items") ? 0 : 2);
     }
-    return v == 1;
+    return v;
 }
 
 template <int R, int MODE>
@@ -537,7 +646,14 @@ PlaneGeo plane_geometry(const Operator &op) {
 template <int R, int MODE, bool DOT>
 int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
     SpanView v = span_view(op);
-    if (!use_plane_kernel()) {
+    const int kind = fine_kernel_kind();
+    if (kind == 0) {
+        int g = grid_for(op.n_items * 32, 256, 148 * 16);
+        k_items<R, MODE, DOT><<<g, 256, 0, s>>>(v, a);
+        SPFD_LAUNCH_CHECK();
+        return g;
+    }
+    if (kind == 2) {
         int g = (int)op.n_tiles;
         if (g > 0) k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
         SPFD_LAUNCH_CHECK();
