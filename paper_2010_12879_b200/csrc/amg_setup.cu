@@ -619,9 +619,11 @@ int pick_group(int64_t nnz, int64_t rows) {
     }
     if (forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
     double avg = rows > 0 ? (double)nnz / (double)rows : 1.0;
-    if (avg <= 12.0) return 4;
-    if (avg <= 48.0) return 8;
-    return 16;
+    int g = avg <= 12.0 ? 4 : (avg <= 48.0 ? 8 : 16);
+    // small coarse matrices: widen the groups until the launch fills the
+    // machine (latency, not bandwidth, bounds those levels)
+    while (g < 32 && rows * (int64_t)g < (int64_t)148 * 32 * 64) g *= 2;
+    return g;
 }
 
 // One coarsening step on level l (CSR A in level numbering).  Returns false

@@ -40,6 +40,7 @@ class Session:
         self._c = _lib.make_config(self.cfg)
         self._vox = None
         self._psi = None
+        self._a_dev = None
 
     @property
     def n_dofs(self) -> int:
@@ -85,15 +86,22 @@ class Session:
         psi = self._psi[:, :self.op.n_dofs] if keep_psi else None
         return vox, report, psi
 
-    def snapshot_host(self, a_host: np.ndarray, pinned: bool = True):
+    def snapshot_host(self, a_host, out=None):
         """End-to-end from host memory: H2D of the potentials, snapshot,
-        D2H of the voxel field.  Returns (numpy (nrhs, n_vox), report)."""
-        a_t = torch.from_numpy(np.ascontiguousarray(a_host, dtype=np.float64))
-        if pinned:
-            a_t = a_t.pin_memory()
-        a_d = a_t.to("cuda", non_blocking=True)
-        vox, rep, _ = self.snapshot(a_d)
-        return vox.cpu().numpy(), rep
+        D2H of the voxel field.  `a_host` is a numpy array or a (preferably
+        pinned) CPU tensor; `out` an optional pinned CPU tensor
+        (nrhs, n_vox) that receives the result.  Returns (numpy, report)."""
+        a_t = a_host if isinstance(a_host, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(a_host, dtype=np.float64))
+        if self._a_dev is None or self._a_dev.shape != a_t.shape:
+            self._a_dev = torch.empty(a_t.shape, dtype=torch.float64, device="cuda")
+        self._a_dev.copy_(a_t, non_blocking=a_t.is_pinned())
+        vox, rep, _ = self.snapshot(self._a_dev)
+        if out is None:
+            out = torch.empty(vox.shape, dtype=torch.float64, pin_memory=True)
+        out.copy_(vox, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out.numpy(), rep
 
 
 class _OpRef:
