@@ -190,6 +190,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="host = gloo host-callback transport (testing several ranks on one GPU)")
+    ap.add_argument("--replicate-below", type=int, default=100_000,
+                    help="coarse levels with fewer rows are solved redundantly on every rank")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -222,9 +226,14 @@ def main():
 
     from paper_2010_12879_b200 import Session, SolveConfig, _lib
 
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    dev = local % ndev if args.transport == "host" else local
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.transport == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     w = build_workload(args.config)
     log(f"[bench] rank {rank}: {w.name}, building operator + AMG")
     cfg = SolveConfig(rel_tol=REL_TOL, max_nrhs=2)
@@ -235,6 +244,11 @@ def main():
     h = sess.hierarchy
     log(f"[bench] dofs {sess.n_dofs} levels {h.level_sizes} setup {h.setup_seconds:.3f}s (device) "
         f"{setup_wall:.3f}s wall incl. assembly")
+    if world > 1:
+        from paper_2010_12879_b200.distributed import Communicator
+        comm = Communicator.nccl() if args.transport == "nccl" else Communicator.host()
+        sess.distribute(comm, replicate_below=args.replicate_below)
+        log(f"[bench] rank {rank}: planes {sess.plane_range} dofs {sess.dof_range} voxels {sess.vox_range}")
     a_host = torch.from_numpy(np.ascontiguousarray(w.a)).pin_memory()
     a_dev = a_host.to("cuda")
     lib = _lib.load()
@@ -266,7 +280,8 @@ def main():
     launches = (lib.spfd_launch_count() - n0) // args.steps
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms], dtype=torch.float64)
+        t = t.cuda() if args.transport == "nccl" else t
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
@@ -279,7 +294,8 @@ def main():
     torch.cuda.synchronize()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
-    out_host = torch.empty((w.a.shape[0], sess.n_cond_voxels), dtype=torch.float64, pin_memory=True)
+    v0, v1 = sess.vox_range
+    out_host = torch.empty((w.a.shape[0], v1 - v0), dtype=torch.float64, pin_memory=True)
     e2.record(stream)
     for _ in range(args.steps):
         vox_host, rep = sess.snapshot_host(a_host, out=out_host)
@@ -287,11 +303,16 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3) / args.steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_ms], dtype=torch.float64)
+        t = t.cuda() if args.transport == "nccl" else t
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    h2d = int(w.a.nbytes)
-    d2h = int(vox_host.nbytes)
+    h2d, d2h = sess.host_bytes(w.a.shape[0])
+    if world > 1:
+        t = torch.tensor([h2d, d2h], dtype=torch.float64)
+        t = t.cuda() if args.transport == "nccl" else t
+        dist.all_reduce(t)
+        h2d, d2h = int(t[0].item()), int(t[1].item())
 
     # roofline of the dominant kernel (fine-level matrix-free SpMV, both rhs)
     import ctypes
@@ -325,14 +346,15 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": False,
-        "scaling": "weak",
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (Duke-like layered elliptic cylinder, uniform B re/im, comb-gauge edge potentials)",
         "config": {
             "workload": f"{args.config} {w.name}: {n_dofs} DOFs, complex (re/im) rhs batched",
             "rel_tol": REL_TOL, "method": "AMG-PCG (SA-AMG V(1,1), reference aggregation)",
-            "parallelism": "replicas" if world > 1 else "single GPU",
+            "parallelism": (f"z-slab decomposition over {world} GPUs (NCCL send/recv halos, allgathered dots; "
+                            f"coarse levels < {args.replicate_below} rows replicated)") if world > 1 else "single GPU",
             "l2": "inputs larger than L2 (fine-level working set >> 126 MB)",
             "step": "rhs assembly + solve to 1e-8 (both rhs) + fused E-field/voxel average",
         },

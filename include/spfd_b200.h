@@ -214,6 +214,45 @@ int spfd_snapshot(spfd_op_t op, spfd_amg_t amg, const double *a, double omega,
                   double *psi, double *vox, int nrhs, const spfd_config *h_cfg,
                   spfd_report *h_rep, void *stream);
 
+/* ---- multi-GPU z-slabs --------------------------------------- */
+
+typedef struct spfd_comm_s *spfd_comm_t;
+
+/* Host transport (testing several processes on one GPU, or any custom
+ * transport): the library synchronises its stream, then calls
+ *   exchange(user, n, peer[], kind[], buf[], bytes[])  kind 0 = send, 1 = recv
+ *   allgather(user, send, recv, bytes)                 rank-ordered
+ * with DEVICE buffers; both must complete before returning 0. */
+typedef struct {
+    void *user;
+    int (*exchange)(void *user, int n, const int *peer, const int *kind, void *const *buf, const int64_t *bytes);
+    int (*allgather)(void *user, const void *send, void *recv, int64_t bytes);
+} spfd_comm_callbacks;
+
+/* NCCL transport over NVLink / NVSwitch (NCCL loaded with dlopen).
+ * h_unique_id: 128-byte ncclUniqueId produced by spfd_nccl_unique_id on
+ * one rank and broadcast (e.g. with torch.distributed). */
+int spfd_nccl_unique_id(void *h_unique_id);
+int spfd_comm_init_nccl(const void *h_unique_id, int rank, int nranks, spfd_comm_t *out);
+int spfd_comm_init_callbacks(const spfd_comm_callbacks *h_cb, int rank, int nranks, spfd_comm_t *out);
+int spfd_comm_destroy(spfd_comm_t comm);
+
+/* Attach a z-slab decomposition to an operator hierarchy (collective; every
+ * rank holds the identical operator and hierarchy, so aggregates and
+ * iteration counts do not depend on the number of GPUs).  Rank r owns the
+ * node planes [k_r, k_{r+1}) balanced by span positions; coarse rows belong
+ * to the rank owning their aggregate's lowest member; levels below
+ * `replicate_below` rows are solved redundantly on every rank.  Afterwards
+ * spfd_solve / spfd_snapshot run distributed: halo planes and coarse halos
+ * travel over the transport, dot products are allgathered and summed in rank
+ * order (bitwise reproducible for a fixed rank count).  Vectors stay
+ * full-length; only the owned range is computed.
+ *   h_range[0..5] (out): first/last+1 DOF, first/last+1 conductive voxel
+ *   owned by this rank (psi / vox outputs are valid there), and the owned
+ *   node planes [k_r, k_{r+1}). */
+int spfd_amg_distribute(spfd_amg_t amg, spfd_comm_t comm, int64_t replicate_below, int64_t *h_range,
+                        void *stream);
+
 /* ---- measurement ---------------------------------------------------------- */
 
 /* Time `reps` back-to-back launches of one level-0 kernel between CUDA
@@ -225,6 +264,8 @@ int spfd_bench_kernel(spfd_amg_t amg, int which, int reps, int nrhs, double *h_m
                       void *stream);
 /* Number of kernels this library has launched so far (process-wide). */
 int64_t spfd_launch_count(void);
+/* Synchronous copy between any host/device pointers (host transports). */
+int spfd_copy(void *dst, const void *src, int64_t bytes);
 
 #ifdef __cplusplus
 }

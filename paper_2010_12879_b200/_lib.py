@@ -122,7 +122,22 @@ _SIGS = {
     "spfd_snapshot": (_INT, [_VP, _VP, _VP, _D, _VP, _VP, _INT, _VP, _VP, _VP]),
     "spfd_bench_kernel": (_INT, [_VP, _INT, _INT, _INT, _VP, _VP, _VP]),
     "spfd_launch_count": (ctypes.c_int64, []),
+    "spfd_copy": (_INT, [_VP, _VP, _I64]),
+    "spfd_nccl_unique_id": (_INT, [_VP]),
+    "spfd_comm_init_nccl": (_INT, [_VP, _INT, _INT, _VP]),
+    "spfd_comm_init_callbacks": (_INT, [_VP, _INT, _INT, _VP]),
+    "spfd_comm_destroy": (_INT, [_VP]),
+    "spfd_amg_distribute": (_INT, [_VP, _VP, _I64, _VP, _VP]),
 }
+
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                               ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_void_p),
+                               ctypes.POINTER(ctypes.c_int64))
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+
+
+class CommCallbacks(ctypes.Structure):
+    _fields_ = [("user", ctypes.c_void_p), ("exchange", EXCHANGE_FN), ("allgather", ALLGATHER_FN)]
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
 

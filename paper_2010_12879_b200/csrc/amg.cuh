@@ -43,6 +43,9 @@ struct Level {
     int p_group = 4, r_group = 32, a_group = 32;  // lanes per row in CSR kernels
 };
 
+struct Dist;   // z-slab decomposition (dist.cuh)
+struct Comm;   // transport (comm.cuh)
+
 struct Amg {
     std::vector<Level> lv;
     Operator *op = nullptr;   // structured level 0 (not owned)
@@ -60,6 +63,11 @@ struct Amg {
     DevBuf<double> fg_basis, fg_prec;  // FGMRES basis (allocated on demand)
     int64_t fg_m = 0;
     int vc_partials = 0;      // r.z partials written by the last V-cycle (0 = none)
+    Dist *dist = nullptr;     // set by amg_distribute (owned)
+    Amg() = default;
+    Amg(const Amg &) = delete;
+    Amg &operator=(const Amg &) = delete;
+    ~Amg();
     int64_t device_bytes() const;
 };
 
@@ -74,6 +82,10 @@ void amg_level_agg(Amg &h, int level, int32_t *agg, cudaStream_t s);
 void amg_to_level0(Amg &h, const double *planar, double *inter, int nrhs, cudaStream_t s);
 void amg_from_level0(Amg &h, const double *inter, double *planar, int nrhs, cudaStream_t s);
 
+int csr_group(int64_t nnz, int64_t rows);  // lanes per row of the CSR kernels
+void amg_distribute(Amg &h, Comm *comm, int64_t replicate_below, int64_t *range, cudaStream_t s);
+void dist_range_exchange(Amg &h, double *v, int nrhs, cudaStream_t s);
+void dist_info(const Amg &h, int64_t *out);  // pb, pe, voxel-row begin, end
 double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cudaStream_t s);
 spfd_report krylov_solve(Amg &h, const double *b_inter, double *x_inter, int nrhs, const spfd_config &cfg,
                          double *h_trace, cudaStream_t s);

@@ -769,6 +769,8 @@ bool coarsen(Level &L, const Csr &A, double theta, double omega, Csr &Ac, Csr &P
 
 }  // namespace
 
+int csr_group(int64_t nnz, int64_t rows) { return pick_group(nnz, rows); }
+
 int64_t Amg::device_bytes() const {
     int64_t b = cinv.bytes() + kx.bytes() + kr.bytes() + kz.bytes() + kp.bytes() + kq.bytes() + kb.bytes() +
                 partials.bytes() + scal.bytes() + fg_basis.bytes() + fg_prec.bytes();

@@ -4,6 +4,7 @@
 #include <string>
 
 #include "amg.cuh"
+#include "comm.cuh"
 
 struct spfd_op_s {
     spfd::Operator *op;
@@ -11,6 +12,9 @@ struct spfd_op_s {
 struct spfd_amg_s {
     spfd::Amg *amg;
     spfd::Operator *op;  // not owned
+};
+struct spfd_comm_s {
+    spfd::Comm *comm;
 };
 
 namespace spfd {
@@ -256,12 +260,60 @@ int spfd_snapshot(spfd_op_t hop, spfd_amg_t h, const double *a, double omega, do
         Amg &m = *h->amg;
         Operator &op = *hop->op;
         // rhs straight into the span layout, solve, fused E-field from the span iterate
-        op_rhs_span(op, a, m.kb.get(), nrhs, S(stream));
-        *rep = krylov_solve(m, m.kb.get(), m.kx.get(), nrhs, *cfg, nullptr, S(stream));
-        if (rep->status == SPFD_ENONFINITE) throw Error(SPFD_ENONFINITE, "non-finite value in the Krylov iteration");
-        op_efield_voxavg_span(op, a, m.kx.get(), omega, vox, op.ws_b.get(), nrhs, S(stream));
+        if (m.dist) {
+            int64_t rg[4];
+            dist_info(m, rg);
+            op_rhs_span(op, a, m.kb.get(), nrhs, S(stream), rg[0], rg[1]);
+            *rep = krylov_solve(m, m.kb.get(), m.kx.get(), nrhs, *cfg, nullptr, S(stream));
+            if (rep->status == SPFD_ENONFINITE) throw Error(SPFD_ENONFINITE, "non-finite value in the Krylov iteration");
+            op_node_field_span(op, a, m.kx.get(), omega, op.ws_b.get(), nrhs, S(stream), rg[0], rg[1]);
+            dist_range_exchange(m, op.ws_b.get(), nrhs, S(stream));   // node plane k_{r+1} from the next rank
+            op_voxavg_span(op, op.ws_b.get(), vox, nrhs, S(stream), rg[2], rg[3]);
+        } else {
+            op_rhs_span(op, a, m.kb.get(), nrhs, S(stream));
+            *rep = krylov_solve(m, m.kb.get(), m.kx.get(), nrhs, *cfg, nullptr, S(stream));
+            if (rep->status == SPFD_ENONFINITE) throw Error(SPFD_ENONFINITE, "non-finite value in the Krylov iteration");
+            op_efield_voxavg_span(op, a, m.kx.get(), omega, vox, op.ws_b.get(), nrhs, S(stream));
+        }
         if (psi) op_span_to_dofs(op, m.kx.get(), psi, nrhs, S(stream));
         SPFD_CUDA(cudaStreamSynchronize(S(stream)));
+    });
+}
+
+int spfd_nccl_unique_id(void *h_id) {
+    return guarded([&] {
+        SPFD_CHECK(h_id, SPFD_EINVAL, "null argument");
+        nccl_unique_id(h_id);
+    });
+}
+
+int spfd_comm_init_nccl(const void *h_id, int rank, int nranks, spfd_comm_t *out) {
+    return guarded([&] {
+        SPFD_CHECK(h_id && out && nranks >= 1 && rank >= 0 && rank < nranks, SPFD_EINVAL, "bad argument");
+        *out = new spfd_comm_s{comm_nccl(h_id, rank, nranks)};
+    });
+}
+
+int spfd_comm_init_callbacks(const spfd_comm_callbacks *cb, int rank, int nranks, spfd_comm_t *out) {
+    return guarded([&] {
+        SPFD_CHECK(cb && out && nranks >= 1 && rank >= 0 && rank < nranks, SPFD_EINVAL, "bad argument");
+        *out = new spfd_comm_s{comm_host(*cb, rank, nranks)};
+    });
+}
+
+int spfd_comm_destroy(spfd_comm_t c) {
+    return guarded([&] {
+        if (!c) return;
+        delete c->comm;
+        delete c;
+    });
+}
+
+int spfd_amg_distribute(spfd_amg_t h, spfd_comm_t c, int64_t replicate_below, int64_t *h_range, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(h && c && h_range, SPFD_EINVAL, "null argument");
+        SPFD_CHECK(h->amg->dist == nullptr, SPFD_EINVAL, "hierarchy already distributed");
+        amg_distribute(*h->amg, c->comm, replicate_below, h_range, S(stream));
     });
 }
 
@@ -273,5 +325,11 @@ int spfd_bench_kernel(spfd_amg_t h, int which, int reps, int nrhs, double *h_ms,
 }
 
 int64_t spfd_launch_count(void) { return spfd::launch_count(); }
+
+int spfd_copy(void *dst, const void *src, int64_t bytes) {
+    return guarded([&] {
+        if (bytes > 0) SPFD_CUDA(cudaMemcpy(dst, src, (size_t)bytes, cudaMemcpyDefault));
+    });
+}
 
 }  // extern "C"

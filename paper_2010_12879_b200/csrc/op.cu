@@ -737,13 +737,14 @@ inline EdgeIdx edge_idx(const Operator &op) {
 
 template <int R>
 __global__ void __launch_bounds__(kSpanThreads) k_rhs(SpanView v, EdgeIdx e, const double *__restrict__ a,
-                                                      int64_t E, typename Vec<R>::T *__restrict__ rhs) {
+                                                      int64_t E, typename Vec<R>::T *__restrict__ rhs, PosRange pr) {
     using T = typename Vec<R>::T;
-    int t = blockIdx.x;
+    int t = pr.tile0 + blockIdx.x;
     int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
     for (int u = 0; u < kTile / kSpanThreads; ++u) {
         int p = t * kTile + u * kSpanThreads + threadIdx.x;
-        if (p >= v.L) break;
+        if (p >= pr.pe) break;
+        if (p < pr.pb) continue;
         int r = find_row(v.rows, r0, r1, p);
         int4 q = v.rows[r];
         int i = q.y + (p - q.x);
@@ -768,14 +769,24 @@ __global__ void __launch_bounds__(kSpanThreads) k_rhs(SpanView v, EdgeIdx e, con
     }
 }
 
-void op_rhs_span(const Operator &op, const double *a, double *rhs_span, int nrhs, cudaStream_t s) {
-    if (op.n_tiles == 0) return;
+PosRange pos_range(const Operator &op, int64_t pb, int64_t pe) {
+    if (pe > op.L || pe < 0) pe = op.L;
+    if (pb < 0) pb = 0;
+    PosRange r{pb, pe, (int)(pb / kTile), 0};
+    r.tiles = (int)((pe + kTile - 1) / kTile) - r.tile0;
+    return r;
+}
+
+void op_rhs_span(const Operator &op, const double *a, double *rhs_span, int nrhs, cudaStream_t s, int64_t pb,
+                 int64_t pe) {
+    PosRange pr = pos_range(op, pb, pe);
+    if (pr.tiles <= 0) return;
     SpanView v = span_view(op);
     EdgeIdx e = edge_idx(op);
     if (nrhs == 1)
-        k_rhs<1><<<(int)op.n_tiles, kSpanThreads, 0, s>>>(v, e, a, op.n_edges, rhs_span);
+        k_rhs<1><<<pr.tiles, kSpanThreads, 0, s>>>(v, e, a, op.n_edges, rhs_span, pr);
     else
-        k_rhs<2><<<(int)op.n_tiles, kSpanThreads, 0, s>>>(v, e, a, op.n_edges, (double2 *)rhs_span);
+        k_rhs<2><<<pr.tiles, kSpanThreads, 0, s>>>(v, e, a, op.n_edges, (double2 *)rhs_span, pr);
     SPFD_LAUNCH_CHECK();
 }
 
@@ -941,12 +952,13 @@ template <int R>
 __global__ void __launch_bounds__(kSpanThreads) k_node_field_span(SpanView v, EdgeIdx e, const double *__restrict__ a,
                                                                   int64_t E, const double *__restrict__ psi,
                                                                   double omega, double sx, double sy, double sz,
-                                                                  double *__restrict__ node) {
-    int t = blockIdx.x;
+                                                                  double *__restrict__ node, PosRange pr) {
+    int t = pr.tile0 + blockIdx.x;
     int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
     for (int u = 0; u < kTile / kSpanThreads; ++u) {
         int p = t * kTile + u * kSpanThreads + threadIdx.x;
-        if (p >= v.L) break;
+        if (p >= pr.pe) break;
+        if (p < pr.pb) continue;
         int r = find_row(v.rows, r0, r1, p);
         int4 q = v.rows[r];
         int i = q.y + (p - q.x);
@@ -987,33 +999,48 @@ struct SpanNodeAt {
 };
 
 template <int R>
-__global__ void k_voxavg_span(const uint8_t *vc, Geo g, const int32_t *vrow_off, int64_t n_vrows,
+__global__ void k_voxavg_span(const uint8_t *vc, Geo g, const int32_t *vrow_off, int64_t vr_b, int64_t n_vrows,
                               int64_t n_cv, SpanNodeAt<R> at, double *vox) {
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    for (int64_t vr = warp; vr < n_vrows; vr += ((int64_t)gridDim.x * blockDim.x) >> 5)
+    for (int64_t vr = vr_b + warp; vr < n_vrows; vr += ((int64_t)gridDim.x * blockDim.x) >> 5)
         voxel_row_avg(vc, g, vrow_off, vr, n_cv, at, R, vox);
+}
+
+void op_node_field_span(const Operator &op, const double *a, const double *psi_span, double omega,
+                        double *node_span, int nrhs, cudaStream_t s, int64_t pb, int64_t pe) {
+    PosRange pr = pos_range(op, pb, pe);
+    if (pr.tiles <= 0) return;
+    SpanView v = span_view(op);
+    EdgeIdx e = edge_idx(op);
+    if (nrhs == 1)
+        k_node_field_span<1><<<pr.tiles, kSpanThreads, 0, s>>>(v, e, a, op.n_edges, psi_span, omega, op.sx, op.sy,
+                                                               op.sz, node_span, pr);
+    else
+        k_node_field_span<2><<<pr.tiles, kSpanThreads, 0, s>>>(v, e, a, op.n_edges, psi_span, omega, op.sx, op.sy,
+                                                               op.sz, node_span, pr);
+    SPFD_LAUNCH_CHECK();
+}
+
+void op_voxavg_span(const Operator &op, const double *node_span, double *vox, int nrhs, cudaStream_t s,
+                    int64_t vr_b, int64_t vr_e) {
+    Geo g{(int)op.nx, (int)op.ny, (int)op.nz, (int)op.NX, (int)op.NY, (int)op.NZ};
+    int64_t nvr = op.ny * op.nz;
+    if (vr_e < 0 || vr_e > nvr) vr_e = nvr;
+    if (vr_e <= vr_b) return;
+    int gv = grid_for((vr_e - vr_b) * 32, 256, 148 * 32);
+    if (nrhs == 1)
+        k_voxavg_span<1><<<gv, 256, 0, s>>>(op.vox_cond.get(), g, op.vrow_off.get(), vr_b, vr_e, op.n_cond_vox,
+                                            SpanNodeAt<1>{op.rows.get(), node_span, (int)op.NY}, vox);
+    else
+        k_voxavg_span<2><<<gv, 256, 0, s>>>(op.vox_cond.get(), g, op.vrow_off.get(), vr_b, vr_e, op.n_cond_vox,
+                                            SpanNodeAt<2>{op.rows.get(), node_span, (int)op.NY}, vox);
+    SPFD_LAUNCH_CHECK();
 }
 
 void op_efield_voxavg_span(const Operator &op, const double *a, const double *psi_span, double omega,
                            double *vox, double *node_span_ws, int nrhs, cudaStream_t s) {
-    if (op.n_tiles == 0) return;
-    SpanView v = span_view(op);
-    EdgeIdx e = edge_idx(op);
-    Geo g{(int)op.nx, (int)op.ny, (int)op.nz, (int)op.NX, (int)op.NY, (int)op.NZ};
-    int64_t nvr = op.ny * op.nz;
-    int gv = grid_for(nvr * 32, 256, 148 * 32);
-    if (nrhs == 1) {
-        k_node_field_span<1><<<(int)op.n_tiles, kSpanThreads, 0, s>>>(v, e, a, op.n_edges, psi_span, omega,
-                                                                       op.sx, op.sy, op.sz, node_span_ws);
-        k_voxavg_span<1><<<gv, 256, 0, s>>>(op.vox_cond.get(), g, op.vrow_off.get(), nvr, op.n_cond_vox,
-                                            SpanNodeAt<1>{op.rows.get(), node_span_ws, (int)op.NY}, vox);
-    } else {
-        k_node_field_span<2><<<(int)op.n_tiles, kSpanThreads, 0, s>>>(v, e, a, op.n_edges, psi_span, omega,
-                                                                       op.sx, op.sy, op.sz, node_span_ws);
-        k_voxavg_span<2><<<gv, 256, 0, s>>>(op.vox_cond.get(), g, op.vrow_off.get(), nvr, op.n_cond_vox,
-                                            SpanNodeAt<2>{op.rows.get(), node_span_ws, (int)op.NY}, vox);
-    }
-    SPFD_LAUNCH_CHECK();
+    op_node_field_span(op, a, psi_span, omega, node_span_ws, nrhs, s, 0, -1);
+    op_voxavg_span(op, node_span_ws, vox, nrhs, s, 0, -1);
 }
 
 // ------------------------------------------------------------------------

@@ -68,6 +68,13 @@ inline SpanView span_view(const Operator &op) {
                     op.dofmask.get(), op.L, (int)op.NY, (int)op.n_rows};
 }
 
+// Owned position range [pb, pe) of a span kernel launch (z-slab).
+struct PosRange {
+    int64_t pb, pe;
+    int tile0, tiles;
+};
+PosRange pos_range(const Operator &op, int64_t pb, int64_t pe);  // pe < 0: up to L
+
 // Host entry points implemented in op.cu
 Operator *op_create(const int64_t *dims, const double *spacing, const uint16_t *ids,
                     const double *lut, int64_t lut_len, int pin, cudaStream_t s);
@@ -79,7 +86,11 @@ void op_span_to_dofs(const Operator &op, const double *span, double *planar, int
                      cudaStream_t s);
 void op_stencil_span(const Operator &op, const double *x, double *y, int nrhs, cudaStream_t s);
 void op_rhs_span(const Operator &op, const double *a, double *rhs_span, int nrhs,
-                 cudaStream_t s);
+                 cudaStream_t s, int64_t pb = 0, int64_t pe = -1);
+void op_node_field_span(const Operator &op, const double *a, const double *psi_span, double omega,
+                        double *node_span, int nrhs, cudaStream_t s, int64_t pb, int64_t pe);
+void op_voxavg_span(const Operator &op, const double *node_span, double *vox, int nrhs, cudaStream_t s,
+                    int64_t vr_b, int64_t vr_e);
 void op_edge_voltages(const Operator &op, const double *a, const double *psi_span,
                       double omega, double *v, int nrhs, cudaStream_t s);
 void op_node_field(const Operator &op, const double *v, double *node, int nrhs, cudaStream_t s);

@@ -9,7 +9,10 @@
 #include <cstdlib>
 #include <string>
 
+#include <cub/cub.cuh>
+
 #include "amg.cuh"
+#include "comm.cuh"
 
 namespace spfd {
 
@@ -21,7 +24,7 @@ constexpr int kDotThreads = 256;
 // device scalar slots (per rhs k)
 enum {
     S_RHO = 0, S_PQ = 2, S_RR = 4, S_ALPHA = 6, S_BETA = 8, S_BB = 10, S_RZ = 12, S_ACTIVE = 14,
-    S_TMP = 16, S_H = 32  // FGMRES Hessenberg column / scratch from S_H
+    S_TMP = 16, S_LOC = 20, S_H = 32  // S_LOC: per-rank partial scalars; FGMRES Hessenberg column from S_H
 };
 
 __device__ __forceinline__ bool mbit(const uint32_t *m, int64_t p) { return (m[p >> 5] >> (p & 31)) & 1u; }
@@ -121,6 +124,9 @@ struct SpanArgs {
     const int32_t *aggp;  // mode 4: aggregate of each position (-1 = none)
     double *y;            // output
     double *partials;     // per-CTA dot partials
+    int64_t pb = 0;       // owned position range [pb, pe) (z-slab); defaults = all
+    int64_t pe = INT64_MAX;
+    int tile0 = 0;        // first tile of the launch (set by launch_fine)
 };
 
 // Input of a fine-level stencil at a position, per mode (see k_span).
@@ -148,7 +154,8 @@ __global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a
     using W = V<R>;
     using T = typename W::T;
     __shared__ double red[32 * R];
-    const int t = blockIdx.x;
+    const int t = a.tile0 + blockIdx.x;
+    const int64_t pend = a.pe < v.L ? a.pe : v.L;
     const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
     double dot[R];
 #pragma unroll
@@ -156,7 +163,8 @@ __global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a
     int row = r0;
     for (int u = 0; u < kTile / kSpanThreads; ++u) {
         const int p = t * kTile + u * kSpanThreads + threadIdx.x;
-        if (p >= v.L) break;
+        if (p >= pend) break;
+        if (p < a.pb) continue;
         row = frow(v.rows, row, r1, p);
         const int4 q = v.rows[row];
         const Nbr n = neighbours(v, p, row, q);
@@ -331,7 +339,8 @@ __global__ void k_agg_sum(const int64_t *mptr, const int32_t *mpos, int64_t n_ag
 template <int G, int R, int MODE, bool DOT>
 __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__restrict__ r,
                       const double *__restrict__ od, const double *__restrict__ base, double *__restrict__ y,
-                      double *__restrict__ partials, const double *__restrict__ od_aux, double *__restrict__ aux) {
+                      double *__restrict__ partials, const double *__restrict__ od_aux, double *__restrict__ aux,
+                      const int32_t *__restrict__ rowmap) {
     using W = V<R>;
     using T = typename W::T;
     __shared__ double red[32 * R];
@@ -364,22 +373,23 @@ __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__r
             for (int o = G / 2; o > 0; o >>= 1) ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], o, G);
         }
         if (valid && lane == 0) {
+            const int64_t gr = rowmap ? (int64_t)rowmap[row] : row;  // global row (owned-row CSR)
             T sum;
             if constexpr (R == 1) sum = ac[0];
             else sum = make_double2(ac[0], ac[1]);
             T out;
             if (MODE == 0) out = sum;
-            else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(r, row), sum);
-            else if (MODE == 3) out = W::add(W::ld(x, row), W::scale(od[row], W::sub(W::ld(r, row), sum)));
-            else if (MODE == 4) out = W::add(W::scale(od[row], W::ld(r, row)), sum);
-            else out = W::add(W::ld(base, row), sum);
-            W::st(y, row, out);
-            if (MODE == 0 && aux) W::st(aux, row, W::scale(od_aux[row], out));
+            else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(r, gr), sum);
+            else if (MODE == 3) out = W::add(W::ld(x, gr), W::scale(od[gr], W::sub(W::ld(r, gr), sum)));
+            else if (MODE == 4) out = W::add(W::scale(od[gr], W::ld(r, gr)), sum);
+            else out = W::add(W::ld(base, gr), sum);
+            W::st(y, gr, out);
+            if (MODE == 0 && aux) W::st(aux, gr, W::scale(od_aux[gr], out));
             if (DOT) {
 #pragma unroll
                 for (int c = 0; c < R; ++c) {
-                    if (MODE == 0) dot[c] += W::dot(W::ld(x, row), out, c);
-                    else if (MODE == 3) dot[c] += W::dot(W::ld(r, row), out, c);
+                    if (MODE == 0) dot[c] += W::dot(W::ld(x, gr), out, c);
+                    else if (MODE == 3) dot[c] += W::dot(W::ld(r, gr), out, c);
                     else dot[c] += W::dot(out, out, c);
                 }
             }
@@ -404,19 +414,21 @@ inline int csr_grid(int64_t rows, int G) {
 
 template <int G, int R, int MODE, bool DOT>
 void launch_csr_g(const Csr &m, const double *x, const double *r, const double *od, const double *base, double *y,
-                  double *partials, cudaStream_t s, int grid, const double *od_aux, double *aux) {
-    k_csr<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials, od_aux, aux);
+                  double *partials, cudaStream_t s, int grid, const double *od_aux, double *aux,
+                  const int32_t *rowmap) {
+    k_csr<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials, od_aux, aux, rowmap);
 }
 
 template <int R, int MODE, bool DOT>
 int launch_csr(const Csr &m, int G, const double *x, const double *r, const double *od, const double *base,
-               double *y, double *partials, cudaStream_t s, const double *od_aux = nullptr, double *aux = nullptr) {
+               double *y, double *partials, cudaStream_t s, const double *od_aux = nullptr, double *aux = nullptr,
+               const int32_t *rowmap = nullptr) {
     int grid = csr_grid(m.rows, G);
     switch (G) {
-        case 4: launch_csr_g<4, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux); break;
-        case 8: launch_csr_g<8, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux); break;
-        case 16: launch_csr_g<16, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux); break;
-        default: launch_csr_g<32, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux); break;
+        case 4: launch_csr_g<4, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
+        case 8: launch_csr_g<8, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
+        case 16: launch_csr_g<16, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
+        default: launch_csr_g<32, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
     }
     SPFD_LAUNCH_CHECK();
     return grid;
@@ -653,9 +665,13 @@ int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
         SPFD_LAUNCH_CHECK();
         return g;
     }
-    if (kind == 2) {
-        int g = (int)op.n_tiles;
-        if (g > 0) k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
+    if (kind == 2 || a.pb > 0 || a.pe < op.L) {
+        const int64_t pe = a.pe < op.L ? a.pe : op.L;
+        const int t0 = (int)(a.pb / kTile), t1 = (int)((pe + kTile - 1) / kTile);
+        SpanArgs b = a;
+        b.tile0 = t0;
+        int g = t1 - t0;
+        if (g > 0) k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, b);
         SPFD_LAUNCH_CHECK();
         return g;
     }
@@ -950,6 +966,23 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
 
 }  // namespace
 
+#include "dist.cuh"
+
+void amg_distribute(Amg &h, Comm *comm, int64_t replicate_below, int64_t *range, cudaStream_t s) {
+    amg_distribute_impl(h, comm, replicate_below, range, s);
+}
+
+void dist_range_exchange(Amg &h, double *v, int nrhs, cudaStream_t s) {
+    if (h.dist) range_exchange(*h.dist, v, nrhs, s);
+}
+
+void dist_info(const Amg &h, int64_t *out) {
+    const Dist &D = *h.dist;
+    out[0] = D.pb; out[1] = D.pe; out[2] = D.vrow_b; out[3] = D.vrow_e;
+}
+
+Amg::~Amg() { delete dist; }
+
 // level-0 interleaved helpers used by FGMRES (R = 1)
 namespace {
 
@@ -1147,6 +1180,8 @@ spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spf
     SPFD_CUDA(cudaEventCreate(&e1));
     SPFD_CUDA(cudaEventRecord(e0, s));
     spfd_report rep{};
+    SPFD_CHECK(!(h.dist && cfg.method == SPFD_METHOD_FGMRES), SPFD_EINVAL,
+               "the distributed solve supports PCG only");
     if (cfg.method == SPFD_METHOD_FGMRES) {
         int64_t n = h.lv[0].nvec;
         if (nrhs == 1) {
@@ -1170,6 +1205,8 @@ spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spf
                 if (r1.status) rep.status = r1.status;
             }
         }
+    } else if (h.dist) {
+        rep = nrhs == 1 ? pcg_dist<1>(h, b, x, cfg, h_trace, s) : pcg_dist<2>(h, b, x, cfg, h_trace, s);
     } else {
         rep = nrhs == 1 ? pcg<1>(h, b, x, cfg, h_trace, s) : pcg<2>(h, b, x, cfg, h_trace, s);
     }

@@ -41,6 +41,35 @@ class Session:
         self._vox = None
         self._psi = None
         self._a_dev = None
+        self.comm = None
+        self.dof_range = (0, self.op.n_dofs)
+        self.vox_range = (0, self.op.n_cond_voxels)
+
+    def distribute(self, comm, replicate_below: int = 100_000):
+        """Split the solve into z-slabs over `comm` (a distributed.Communicator):
+        this rank then computes only its planes; `dof_range` / `vox_range`
+        give the slices of psi / voxel |E| it produces."""
+        rng = (ctypes.c_int64 * 6)()
+        _lib.check(_lib.load().spfd_amg_distribute(self.hierarchy.handle, comm.handle, int(replicate_below), rng,
+                                                   _lib.stream_ptr()))
+        self.comm = comm
+        self.dof_range = (int(rng[0]), int(rng[1]))
+        self.vox_range = (int(rng[2]), int(rng[3]))
+        self.plane_range = (int(rng[4]), int(rng[5]))
+        return self
+
+    def edge_slices(self):
+        """Edge-index ranges this rank reads (all edges on one GPU): x- and
+        y-edges of its node planes, z-edges of its planes and the one below."""
+        nx, ny, nz = self.op.dims
+        NX, NY = nx + 1, ny + 1
+        if self.comm is None:
+            return [(0, self.op.n_edges)]
+        kb, ke = self.plane_range
+        ex, ey = nx * NY * (nz + 1), NX * ny * (nz + 1)
+        return [(nx * NY * kb, nx * NY * ke),
+                (ex + NX * ny * kb, ex + NX * ny * ke),
+                (ex + ey + NX * NY * max(kb - 1, 0), ex + ey + NX * NY * min(ke, nz))]
 
     @property
     def n_dofs(self) -> int:
@@ -93,15 +122,25 @@ class Session:
         (nrhs, n_vox) that receives the result.  Returns (numpy, report)."""
         a_t = a_host if isinstance(a_host, torch.Tensor) else torch.from_numpy(
             np.ascontiguousarray(a_host, dtype=np.float64))
+        if a_t.dim() == 1:
+            a_t = a_t.reshape(1, -1)
         if self._a_dev is None or self._a_dev.shape != a_t.shape:
             self._a_dev = torch.empty(a_t.shape, dtype=torch.float64, device="cuda")
-        self._a_dev.copy_(a_t, non_blocking=a_t.is_pinned())
+        nb = a_t.is_pinned()
+        for e0, e1 in self.edge_slices():   # only the edges this rank's slab reads
+            self._a_dev[:, e0:e1].copy_(a_t[:, e0:e1], non_blocking=nb)
         vox, rep, _ = self.snapshot(self._a_dev)
+        v0, v1 = self.vox_range
         if out is None:
-            out = torch.empty(vox.shape, dtype=torch.float64, pin_memory=True)
-        out.copy_(vox, non_blocking=True)
+            out = torch.empty((vox.shape[0], v1 - v0), dtype=torch.float64, pin_memory=True)
+        out.copy_(vox[:, v0:v1], non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return out.numpy(), rep
+
+    def host_bytes(self, nrhs: int):
+        """(H2D, D2H) bytes per snapshot_host call on this rank."""
+        h2d = sum(e1 - e0 for e0, e1 in self.edge_slices()) * 8 * nrhs
+        return h2d, (self.vox_range[1] - self.vox_range[0]) * 8 * nrhs
 
 
 class _OpRef:

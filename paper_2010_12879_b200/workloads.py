@@ -58,8 +58,9 @@ def box_model(dims, kappa=0.2, spacing=0.002) -> VoxelModel:
 
 
 def layered_block_model(n=128, spacing=0.002) -> VoxelModel:
+    # 0.2048 m block in a 0.256 m box at 128^3, scaled with n
     return make_phantom("layered-block", (n, n, n), spacing, layers=4, kappa_spm=[0.17, 0.04, 0.35, 0.02],
-                        size_m=(0.2048,) * 3)
+                        size_m=(0.0016 * n,) * 3)
 
 
 def duke_like_model(spacing=0.002) -> VoxelModel:
@@ -170,3 +171,8 @@ def small_box(n=12, kappa=0.2) -> Workload:
     a = np.stack([uniform_potential(model.dims, 0.002, (0, 0, 1e-6)),
                   uniform_potential(model.dims, 0.002, (0.5e-6, 0.2e-6, 0))])
     return Workload(f"box {n}^3", model, FREQ_HZ, a)
+
+
+def c2_small() -> Workload:
+    """C2 geometry at 48^3 (multi-process tests)."""
+    return c2(48)
