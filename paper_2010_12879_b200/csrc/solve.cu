@@ -142,6 +142,7 @@ __device__ __forceinline__ typename V<R>::T xin(const SpanArgs &a, int pp) {
 }
 
 #include "plane.cuh"
+#include "tile.cuh"
 
 // MODE 0: y = A x (+ partial x.y)
 // MODE 1: y = r - A x (+ partial y.y)
@@ -638,7 +639,10 @@ int fine_kernel_kind() {
         // the 2.5-D plane kernel is experimental (latency-bound at 1-2
         // CTAs/SM); the flat span kernel is the default
         const char *e = getenv("SPFD_SPAN_KERNEL");
-        v = (e && std::string(e) == "plane") ? 1 : ((e && std::string(e) == "items") ? 0 : 2);
+        v = 2;
+        if (e && std::string(e) == "plane") v = 1;
+        if (e && std::string(e) == "items") v = 0;
+        if (e && std::string(e) == "tile") v = 3;
     }
     return v;
 }
@@ -659,6 +663,28 @@ template <int R, int MODE, bool DOT>
 int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
     SpanView v = span_view(op);
     const int kind = fine_kernel_kind();
+    if (kind == 3 && a.pb == 0 && a.pe >= op.L) {
+        static int max_dyn = -1;
+        using SM = TileSmem<R, MODE>;
+        if (max_dyn < 0) {
+            int dev = 0, optin = 0;
+            SPFD_CUDA(cudaGetDevice(&dev));
+            SPFD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+            cudaFuncAttributes fa;
+            SPFD_CUDA(cudaFuncGetAttributes(&fa, k_tile<R, MODE, DOT>));
+            max_dyn = optin - (int)fa.sharedSizeBytes;
+            SPFD_CUDA(cudaFuncSetAttribute(k_tile<R, MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
+        }
+        SPFD_CHECK(SM::bytes <= (size_t)max_dyn, SPFD_EINVAL, "tile kernel shared memory exceeds the opt-in limit");
+        int cps = (int)((228 * 1024) / (SM::bytes + 2048));
+        TileGeo g = tile_geo(op, cps < 1 ? 1 : cps);
+        SpanArgs b = a;
+        b.pe = op.L;
+        int grid = g.itiles * g.jtiles * g.ktiles;
+        k_tile<R, MODE, DOT><<<grid, kTileThreads, SM::bytes, s>>>(v, g, b);
+        SPFD_LAUNCH_CHECK();
+        return grid;
+    }
     if (kind == 0) {
         int g = grid_for(op.n_items * 32, 256, 148 * 16);
         k_items<R, MODE, DOT><<<g, 256, 0, s>>>(v, a);
