@@ -143,6 +143,7 @@ __device__ __forceinline__ typename V<R>::T xin(const SpanArgs &a, int pp) {
 
 #include "plane.cuh"
 #include "tile.cuh"
+#include "tail.cuh"
 
 // MODE 0: y = A x (+ partial x.y)
 // MODE 1: y = r - A x (+ partial y.y)
@@ -150,13 +151,13 @@ __device__ __forceinline__ typename V<R>::T xin(const SpanArgs &a, int pp) {
 // MODE 3: y = x + od (r - A x) (+ partial r.y)   (Jacobi sweep)
 // MODE 4: y = base + e - od (A e), e = T ec      (matrix-free prolongation
 //         with P = (I - omega D^-1 A) T; base = od r when null)
-template <int R, int MODE, bool DOT>
+template <int R, int MODE, bool DOT, bool RANGED = false>
 __global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a) {
     using W = V<R>;
     using T = typename W::T;
     __shared__ double red[32 * R];
-    const int t = a.tile0 + blockIdx.x;
-    const int64_t pend = a.pe < v.L ? a.pe : v.L;
+    const int t = RANGED ? a.tile0 + blockIdx.x : blockIdx.x;
+    const int64_t pend = RANGED ? (a.pe < v.L ? a.pe : v.L) : v.L;
     const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
     double dot[R];
 #pragma unroll
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a
     for (int u = 0; u < kTile / kSpanThreads; ++u) {
         const int p = t * kTile + u * kSpanThreads + threadIdx.x;
         if (p >= pend) break;
-        if (p < a.pb) continue;
+        if (RANGED && p < a.pb) continue;
         row = frow(v.rows, row, r1, p);
         const int4 q = v.rows[row];
         const Nbr n = neighbours(v, p, row, q);
@@ -691,13 +692,19 @@ int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
         SPFD_LAUNCH_CHECK();
         return g;
     }
-    if (kind == 2 || a.pb > 0 || a.pe < op.L) {
+    if (a.pb > 0 || a.pe < op.L) {  // owned z-slab range
         const int64_t pe = a.pe < op.L ? a.pe : op.L;
         const int t0 = (int)(a.pb / kTile), t1 = (int)((pe + kTile - 1) / kTile);
         SpanArgs b = a;
         b.tile0 = t0;
         int g = t1 - t0;
-        if (g > 0) k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, b);
+        if (g > 0) k_span<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, b);
+        SPFD_LAUNCH_CHECK();
+        return g;
+    }
+    if (kind == 2) {
+        int g = (int)op.n_tiles;
+        if (g > 0) k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
         SPFD_LAUNCH_CHECK();
         return g;
     }
@@ -763,6 +770,56 @@ void level_apply(Amg &h, int l, int mode, const double *x, const double *r, doub
 
 template <int R>
 void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s);
+
+// first level handled by the cooperative tail kernel (0 = none)
+int tail_level(const Amg &h) {
+    static int enabled = -1;
+    if (enabled < 0) {
+        const char *e = getenv("SPFD_TAIL");
+        // measured slower than the per-level kernels on C3 (grid barriers
+        // cost more than the launches they replace): opt-in
+        enabled = (e && std::string(e) == "1") ? 1 : 0;
+    }
+    const int nl = (int)h.lv.size();
+    if (!enabled || h.pre > 1 || h.post != 1 || nl < 3) return 0;
+    for (int l = 1; l < nl - 1; ++l)
+        if (h.lv[l].n <= 150000 && nl - 1 - l <= kTailMax) return l;
+    return 0;
+}
+
+template <int R>
+void run_tail(Amg &h, int l0, const double *r, double *z, cudaStream_t s) {
+    const int nl = (int)h.lv.size();
+    TailArgs t{};
+    t.nlev = nl - 1 - l0;
+    for (int i = 0; i < t.nlev; ++i) {
+        Level &L = h.lv[l0 + i];
+        TailLevel &T = t.lv[i];
+        T.A = view(L.A); T.P = view(L.P); T.R = view(L.R);
+        T.od = L.odinv.get();
+        T.r = i == 0 ? const_cast<double *>(r) : L.vr.get();
+        T.x = i == 0 ? z : L.vx.get();
+        T.d = L.vd.get();
+        T.gA = L.a_group; T.gP = L.p_group; T.gR = L.r_group;
+    }
+    Level &C = h.lv[nl - 1];
+    t.cinv = h.cinv.get();
+    t.nc = h.nc;
+    t.rc = C.vr.get();
+    t.zc = C.vx.get();
+    static int blocks = 0;
+    if (blocks == 0) {
+        int dev = 0, sms = 0, per = 0;
+        SPFD_CUDA(cudaGetDevice(&dev));
+        SPFD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        SPFD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tail<R>, 256, 0));
+        blocks = sms * (per < 4 ? per : 4);
+        if (blocks < 1) blocks = 1;
+    }
+    void *args[] = {&t};
+    SPFD_CUDA(cudaLaunchCooperativeKernel((const void *)k_tail<R>, blocks, 256, args, 0, s));
+    SPFD_LAUNCH_CHECK();
+}
 
 // Fine level of a structured hierarchy, transfers matrix-free through the
 // aggregates (P = (I - omega D^-1 A) T, R = P^T):
@@ -842,6 +899,10 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
     }
     if (l == 0 && h.structured) {
         h.vc_partials = vcycle_fine_mf<R>(h, r, z, s);
+        return;
+    }
+    if (l > 0 && l == tail_level(h)) {
+        run_tail<R>(h, l, r, z, s);
         return;
     }
     double *d = L.vd.get(), *t = L.vt.get();
