@@ -64,6 +64,8 @@ struct Amg {
     int64_t fg_m = 0;
     int vc_partials = 0;      // r.z partials written by the last V-cycle (0 = none)
     Dist *dist = nullptr;     // set by amg_distribute (owned)
+    cudaStream_t side = nullptr;            // PCG x-update overlap stream
+    cudaEvent_t ev_alpha = nullptr, ev_x = nullptr;
     Amg() = default;
     Amg(const Amg &) = delete;
     Amg &operator=(const Amg &) = delete;

@@ -530,6 +530,36 @@ __global__ void k_update_xr(int64_t n, const double *scal, double *x, double *r,
         for (int c = 0; c < R; ++c) partials[blockIdx.x * R + c] = d[c];
 }
 
+// split update for overlap: r -= alpha q (+ r.r) on the solve stream while
+// x += alpha p runs on a side stream during the next V-cycle
+template <int R>
+__global__ void k_update_r(int64_t n, const double *scal, double *r, const double *q, double *partials) {
+    using W = V<R>;
+    __shared__ double red[32 * R];
+    double na[R], d[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) { na[c] = -scal[S_ALPHA + c]; d[c] = 0.0; }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const typename W::T rv = vfma<R>(na, W::ld(q, i), W::ld(r, i));
+        W::st(r, i, rv);
+#pragma unroll
+        for (int c = 0; c < R; ++c) d[c] = fma(W::comp(rv, c), W::comp(rv, c), d[c]);
+    }
+    block_sum<R>(d, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int c = 0; c < R; ++c) partials[blockIdx.x * R + c] = d[c];
+}
+template <int R>
+__global__ void k_update_x(int64_t n, const double *scal, double *x, const double *p) {
+    using W = V<R>;
+    double a[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) a[c] = scal[S_ALPHA + c];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        W::st(x, i, vfma<R>(a, W::ld(p, i), W::ld(x, i)));
+}
+
 // p = z + beta p
 template <int R>
 __global__ void k_xpby(int64_t n, const double *scal, const double *z, double *p) {
@@ -624,6 +654,9 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
     np = std::max<int64_t>(np, 148 * 16);
     h.partials.alloc(np * 2 + 64);
     h.scal.alloc(S_H + 256);
+    SPFD_CUDA(cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking));
+    SPFD_CUDA(cudaEventCreateWithFlags(&h.ev_alpha, cudaEventDisableTiming));
+    SPFD_CUDA(cudaEventCreateWithFlags(&h.ev_x, cudaEventDisableTiming));
 }
 
 // ------------------------------------------------------------------------
@@ -1008,7 +1041,14 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
         if (it >= cfg.max_iters) break;
         int g = level0_apply<R>(h, 0, true, p, nullptr, q, s);  // q = A p, p.q
         finalize<R>(h, g, S_PQ, F_ALPHA, s);
-        k_update_xr<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, x, r, p, q, h.partials.get());
+        // x += alpha p on the side stream, overlapping the V-cycle (which is
+        // L1/latency-bound and leaves HBM bandwidth idle); joined before p changes
+        SPFD_CUDA(cudaEventRecord(h.ev_alpha, s));
+        SPFD_CUDA(cudaStreamWaitEvent(h.side, h.ev_alpha, 0));
+        k_update_x<R><<<grid_for(n, 256, 148 * 8), 256, 0, h.side>>>(n, sc, x, p);
+        SPFD_LAUNCH_CHECK();
+        SPFD_CUDA(cudaEventRecord(h.ev_x, h.side));
+        k_update_r<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, r, q, h.partials.get());
         SPFD_LAUNCH_CHECK();
         finalize<R>(h, kDotGrid, S_RR, F_STORE, s);
         k_set_active<<<1, 1, 0, s>>>(sc, R, tol);
@@ -1024,6 +1064,7 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
         }
         if (done || it >= cfg.max_iters) {
             // true residual check (linsolve.py:296-298 semantics)
+            SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
             int gt = level0_apply<R>(h, 1, true, x, b, q, s);
             finalize<R>(h, gt, S_TMP, F_STORE, s);
             SPFD_CUDA(cudaMemcpyAsync(hs, sc, S_H * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1044,9 +1085,11 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
         amg_vcycle(h, r, z, R, s);
         if (h.vc_partials > 0) finalize<R>(h, h.vc_partials, S_RZ, F_BETA, s);  // r.z fused into the post-smooth
         else dot<R>(h, n, r, z, S_RZ, F_BETA, s);
+        SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));  // x += alpha p done before p changes
         k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p);
         SPFD_LAUNCH_CHECK();
     }
+    SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
     rep.iterations = it;
     return rep;
 }
@@ -1068,7 +1111,12 @@ void dist_info(const Amg &h, int64_t *out) {
     out[0] = D.pb; out[1] = D.pe; out[2] = D.vrow_b; out[3] = D.vrow_e;
 }
 
-Amg::~Amg() { delete dist; }
+Amg::~Amg() {
+    delete dist;
+    if (side) cudaStreamDestroy(side);
+    if (ev_alpha) cudaEventDestroy(ev_alpha);
+    if (ev_x) cudaEventDestroy(ev_x);
+}
 
 // level-0 interleaved helpers used by FGMRES (R = 1)
 namespace {
