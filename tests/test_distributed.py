@@ -115,3 +115,34 @@ def test_distributed_snapshot_matches_single_gpu(replicate_below):
     # both solves at rel.res 1e-10 (psi ~1e-11, E ~1e-8)
     assert np.linalg.norm(pd - psi) <= 1e-8 * np.linalg.norm(psi)
     assert np.abs(vd - vox).max() <= 1e-7 * np.abs(vox).max()
+
+
+def _nccl_single_worker(rank, size, port, out):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2010_12879_b200 import Session, SolveConfig, workloads
+    from paper_2010_12879_b200.distributed import Communicator
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=size,
+                            device_id=torch.device("cuda", 0))
+    w = workloads.c2_small()
+    sess = Session(w.model, w.frequency_hz, SolveConfig(rel_tol=1e-10))
+    a = torch.from_numpy(w.a).cuda()
+    ref, rep0, _ = sess.snapshot(a)
+    ref = ref.cpu()
+    sess2 = Session(w.model, w.frequency_hz, SolveConfig(rel_tol=1e-10))
+    sess2.distribute(Communicator.nccl(), replicate_below=1000)   # NCCL transport, one rank
+    vox, rep, _ = sess2.snapshot(a)
+    torch.save({"ref": ref, "vox": vox.cpu(), "it": (rep0.iterations, rep.iterations)}, os.path.join(out, "n.pt"))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_transport_single_rank():
+    """The NCCL transport (dlopen, comm init, grouped send/recv, allgather)
+    on one rank: the distributed code path must reproduce the plain solve."""
+    with tempfile.TemporaryDirectory() as out:
+        mp.spawn(_nccl_single_worker, args=(1, _port(), out), nprocs=1, join=True)
+        d = torch.load(os.path.join(out, "n.pt"))
+    assert d["it"][0] == d["it"][1]
+    assert torch.allclose(d["vox"], d["ref"], rtol=1e-10, atol=0)
