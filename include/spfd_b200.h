@@ -42,6 +42,10 @@ extern "C" {
 #define SPFD_ECUDA      6 /* RuntimeError (CUDA failure)                             */
 #define SPFD_ENCCL      7 /* RuntimeError (NCCL failure)                             */
 #define SPFD_ENOMEM     8 /* MemoryError                                             */
+#define SPFD_EINCOMPAT  9 /* IncompatibleFluxError (gauging.py:167-171)             */
+#define SPFD_EPROJECTION 10 /* ProjectionError (field_source.py:319-329)            */
+#define SPFD_ELATTICE  11 /* LatticeError (field_source.py:228-232)                 */
+#define SPFD_ESINGULAR 12 /* SingularPointError (field_source.py:187-188)           */
 
 const char *spfd_last_error(void);
 /* Library version string and the SM architecture the kernels were built for. */
@@ -252,6 +256,90 @@ int spfd_comm_destroy(spfd_comm_t comm);
  *   node planes [k_r, k_{r+1}). */
 int spfd_amg_distribute(spfd_amg_t amg, spfd_comm_t comm, int64_t replicate_below, int64_t *h_range,
                         void *stream);
+
+/* ---- field sources, cleaning, gauging, statistics ------ */
+
+/* A voxel grid (dims = voxels per axis, StaggeredGrid) or a sampling
+ * lattice (dims = points per axis, field_source.Lattice). */
+typedef struct {
+    int64_t dims[3];
+    double  spacing[3];
+    double  origin[3];
+} spfd_box;
+
+typedef struct spfd_field_s *spfd_field_t;  /* per-grid workspace + cleaning AMG */
+
+/* cfg: AMG / Krylov settings of the divergence-cleaning solve (the
+ * reference passes its SolveConfig, field_source.py:313-316). */
+int spfd_field_create(const spfd_box *h_grid, const spfd_config *h_cfg, spfd_field_t *out);
+int spfd_field_destroy(spfd_field_t f);
+
+/* f3: Biot-Savart field of a closed polyline (coil_field,
+ * field_source.py:163-197).  pts double[n][3], verts double[nseg+1][3],
+ * out double[n][3]; scale = mu0 I / (4 pi).  SPFD_ESINGULAR when a point is
+ * within 1e-12 m of a segment.  Synchronises `stream`. */
+int spfd_coil_field(int64_t n, const double *pts, int nseg, const double *verts, double scale,
+                    double *out, void *stream);
+
+/* f3: face fluxes from lattice samples (interpolate_to_faces,
+ * field_source.py:254-272): trilinear interpolation / linear extrapolation
+ * of the normal component at each face centre times the face area.
+ *   b double[n_points][3] (FieldSampleSet.b, lattice x-fastest),
+ *   flux double[n_faces].  Bit-identical to the reference.
+ * SPFD_ELATTICE for a single-point lattice axis off the query plane. */
+int spfd_field_interpolate(spfd_field_t f, const spfd_box *h_lattice, const double *b, double *flux,
+                           void *stream);
+
+/* f2: cell net outflux div = build_divergence(grid) @ flux
+ * (fit_operators.py:276-286), bit-identical.  div double[n_cells]. */
+int spfd_field_divergence(spfd_field_t f, const double *flux, double *div, void *stream);
+
+typedef struct {
+    double  rel_before;          /* ||div flux|| / ||flux||                  */
+    double  rel_after;           /* after the projection (= before if none)  */
+    int32_t solved;              /* 1 if the projection solve ran            */
+    int32_t iterations;
+    double  solve_rel_residual;
+    double  setup_seconds;       /* AMG setup on div divT (first call only)  */
+} spfd_clean_info;
+
+/* f2: divergence_clean (field_source.py:292-329): out = in if the relative
+ * cell-outflux norm is <= tol, else in - divT phi with
+ * (div divT) phi = div in solved by AMG + Krylov at
+ * rel_tol = min(1e-12, tol/(4 rel)).  The hierarchy on div divT is built on
+ * the first call and kept by the handle.  SPFD_EPROJECTION on
+ * non-convergence or a violated postcondition.  out may alias in. */
+int spfd_field_clean(spfd_field_t f, const double *in, double *out, double tol,
+                     spfd_clean_info *h_info, void *stream);
+
+typedef struct {
+    double  rel_residual;        /* ||C a - flux|| / ||flux||                */
+    int64_t worst_face;          /* argmax |defect| if above tol, else -1    */
+    double  worst_defect;
+} spfd_gauge_info;
+
+/* f1: comb-tree gauging (build_comb_tree + gauge_vector_potential,
+ * gauging.py:34-71,137-172): edge potential a double[n_edges] with zero
+ * tree edges reproducing the face fluxes, by three column prefix scans;
+ * then the circulation residual over all faces is checked against tol
+ * (SPFD_EINCOMPAT, info filled).  Zero fluxes give a = 0. */
+int spfd_field_gauge(spfd_field_t f, const double *flux, double *a, double tol,
+                     spfd_gauge_info *h_info, void *stream);
+
+/* circulation_residual (gauging.py:127-134): defect double[n_faces] */
+int spfd_field_circulation(spfd_field_t f, const double *a, const double *flux, double *defect,
+                           void *stream);
+
+/* f4: exposure statistics (build_exposure_report + percentile99,
+ * dosimetry.py:119-127,195-234) over n voxel values:
+ *   scaled[v] = values[v] * scale (RMS_FACTOR or 1), tissue of v =
+ *   ids_box[vox_index[v]]; per tissue id < n_ids: count, mean, max and the
+ *   nearest-rank 99th percentile (sorted index ceil(0.99 c) - 1); h_global =
+ *   {p99, max} over all values.  p99 and max are exact selections.
+ * Host outputs have n_ids entries.  Synchronises `stream`. */
+int spfd_exposure_stats(const double *values, int64_t n, double scale, const int64_t *vox_index,
+                        const uint16_t *ids_box, int32_t n_ids, double *scaled, int64_t *h_count,
+                        double *h_mean, double *h_max, double *h_p99, double *h_global, void *stream);
 
 /* ---- measurement ---------------------------------------------------------- */
 

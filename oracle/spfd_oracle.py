@@ -25,7 +25,9 @@ __all__ = [
     "voxel_kappa", "edge_conductance", "node_conductive_mask",
     "component_labels", "assemble", "strength_graph", "plain_aggregation",
     "amg_setup", "v_cycle", "fgmres", "pcg", "edge_voltages", "node_field",
-    "voxel_average", "comb_gauge", "uniform_face_fluxes", "node_index",
+    "voxel_average", "comb_gauge", "uniform_face_fluxes", "node_index", "coil_field",
+    "interpolate_to_faces", "divergence_matrix", "divergence_clean", "circulation_residual", "comb_tree_mask",
+    "eliminate_cotree_edges", "percentile99", "exposure_stats",
 ]
 
 
@@ -554,3 +556,209 @@ def comb_gauge(dims, fluxes):
     ax[:, :, 1:] = ax[:, :, :1] + np.cumsum(by, axis=2)
     ay[:, :, 1:] = -np.cumsum(bx, axis=2)
     return np.concatenate([ax.ravel(order="F"), ay.ravel(order="F"), az.ravel(order="F")])
+
+
+# --------------------------------------------------------------------------
+# rows f1-f4: sources, interpolation, cleaning, gauging, statistics
+# --------------------------------------------------------------------------
+
+def face_dims(dims, axis):
+    d = [int(n) for n in dims]
+    d[axis] += 1
+    return tuple(d)
+
+
+def face_center_axes(dims, spacing, origin, axis):
+    """fit_operators.py:156-165."""
+    d = face_dims(dims, axis)
+    out = []
+    for a in range(3):
+        if a == axis:
+            out.append(origin[a] + np.arange(d[a]) * spacing[a])
+        else:
+            out.append(origin[a] + (np.arange(d[a]) + 0.5) * spacing[a])
+    return out
+
+
+def coil_field(verts, current_a, points):
+    """Biot-Savart of a closed polyline (field_source.py:163-197)."""
+    pts = np.atleast_2d(np.asarray(points, np.float64))
+    p1 = verts[:-1]
+    seg = verts[1:] - p1
+    seg_len2 = np.einsum("sj,sj->s", seg, seg)
+    a = pts[:, None, :] - p1[None, :, :]
+    b = a - seg[None, :, :]
+    la = np.sqrt(np.einsum("nsj,nsj->ns", a, a))
+    lb = np.sqrt(np.einsum("nsj,nsj->ns", b, b))
+    cross = np.cross(a, b)
+    denom = la * lb * ((la + lb) ** 2 - seg_len2[None, :])
+    coeff = 2.0 * (la + lb) / denom
+    return (4e-7 * np.pi * current_a / (4.0 * np.pi)) * np.einsum("ns,nsj->nj", coeff, cross)
+
+
+def _axis_params(coords, origin, spacing, n):
+    """field_source.py:218-233."""
+    u = (coords - origin) / spacing
+    if n == 1:
+        return np.zeros(coords.shape, np.int64), np.zeros_like(coords), 0
+    i0 = np.clip(np.floor(u).astype(np.int64), 0, n - 2)
+    return i0, u - i0, 1
+
+
+def interpolate_to_faces(dims, spacing, origin, lat_dims, lat_spacing, lat_origin, b):
+    """Trilinear midpoint face fluxes (field_source.py:235-272)."""
+    out = []
+    for axis in range(3):
+        comp = b[:, axis].reshape(tuple(lat_dims), order="F")
+        xs, ys, zs = face_center_axes(dims, spacing, origin, axis)
+        ix, tx, sx = _axis_params(xs, lat_origin[0], lat_spacing[0], lat_dims[0])
+        iy, ty, sy = _axis_params(ys, lat_origin[1], lat_spacing[1], lat_dims[1])
+        iz, tz, sz = _axis_params(zs, lat_origin[2], lat_spacing[2], lat_dims[2])
+        vals = np.zeros((xs.size, ys.size, zs.size))
+        for dx in (0, 1):
+            wx = (tx if dx else 1.0 - tx)[:, None, None]
+            for dy in (0, 1):
+                wy = (ty if dy else 1.0 - ty)[None, :, None]
+                for dz in (0, 1):
+                    wz = (tz if dz else 1.0 - tz)[None, None, :]
+                    corner = comp[(ix + dx * sx)[:, None, None], (iy + dy * sy)[None, :, None],
+                                  (iz + dz * sz)[None, None, :]]
+                    vals += wx * wy * wz * corner
+        t = [a for a in range(3) if a != axis]
+        out.append((vals * (spacing[t[0]] * spacing[t[1]])).ravel(order="F"))
+    return np.concatenate(out)
+
+
+def divergence_matrix(dims):
+    """Cell net-outflux operator (fit_operators.py:227-244,276-286)."""
+    nx, ny, nz = [int(n) for n in dims]
+    i, j, k = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    i, j, k = i.ravel(order="F"), j.ravel(order="F"), k.ravel(order="F")
+    fx, fy = (nx + 1) * ny * nz, nx * (ny + 1) * nz
+    fi = lambda a, ii, jj, kk: ([0, fx, fx + fy][a] + ii + face_dims(dims, a)[0] * (jj + face_dims(dims, a)[1] * kk))
+    faces = np.stack([fi(0, i + 1, j, k), fi(0, i, j, k), fi(1, i, j + 1, k), fi(1, i, j, k),
+                      fi(2, i, j, k + 1), fi(2, i, j, k)], axis=1)
+    signs = np.tile(np.array([1, -1, 1, -1, 1, -1], np.float64), (faces.shape[0], 1))
+    nc = nx * ny * nz
+    nf = fx + fy + nx * ny * (nz + 1)
+    m = sp.coo_matrix((signs.ravel(), (np.repeat(np.arange(nc), 6), faces.ravel())), shape=(nc, nf)).tocsr()
+    m.sort_indices()
+    return m
+
+
+def divergence_clean(dims, fluxes, tol=1e-10):
+    """l2-minimal solenoidal projection (field_source.py:292-329) with a
+    direct sparse solve of (div divT) phi = div f (test oracle)."""
+    from scipy.sparse.linalg import spsolve
+    div = divergence_matrix(dims)
+    fn = float(np.linalg.norm(fluxes))
+    if fn == 0.0:
+        return fluxes.copy()
+    defect = div @ fluxes
+    if float(np.linalg.norm(defect)) / fn <= tol:
+        return fluxes.copy()
+    phi = spsolve((div @ div.T).tocsc(), defect)
+    return fluxes - div.T @ phi
+
+
+def face_edge_incidence(dims):
+    """(edges, signs) per face, right-handed (fit_operators.py:186-224)."""
+    nx, ny, nz = [int(n) for n in dims]
+    eoff = edge_offsets(dims)[0]
+    all_e, all_s = [], []
+    for axis in range(3):
+        e1, e2 = (axis + 1) % 3, (axis + 2) % 3
+        d = face_dims(dims, axis)
+        i, j, k = np.meshgrid(np.arange(d[0]), np.arange(d[1]), np.arange(d[2]), indexing="ij")
+        base = [i.ravel(order="F"), j.ravel(order="F"), k.ravel(order="F")]
+
+        def eidx(a, c):
+            ed = edge_dims(dims, a)
+            return eoff[a] + c[0] + ed[0] * (c[1] + ed[1] * c[2])
+
+        def sh(c, a):
+            c = [x.copy() for x in c]
+            c[a] = c[a] + 1
+            return c
+        all_e.append(np.stack([eidx(e1, base), eidx(e2, sh(base, e1)), eidx(e1, sh(base, e2)), eidx(e2, base)], 1))
+        all_s.append(np.tile(np.array([1, 1, -1, -1], np.int8), (all_e[-1].shape[0], 1)))
+    return np.concatenate(all_e), np.concatenate(all_s)
+
+
+def circulation_residual(values, fluxes, dims):
+    """gauging.py:127-134."""
+    edges, signs = face_edge_incidence(dims)
+    return np.einsum("fm,fm->f", values[edges], signs.astype(np.float64)) - fluxes
+
+
+def comb_tree_mask(dims):
+    """Tree edges of the comb tree (gauging.py:34-71)."""
+    nx, ny, nz = [int(n) for n in dims]
+    m = np.zeros(n_edges(dims), bool)
+    eoff = edge_offsets(dims)[0]
+    ex, ey, ez = (edge_dims(dims, a) for a in range(3))
+    m[eoff[0] + np.arange(nx)] = True
+    i, j = np.meshgrid(np.arange(nx + 1), np.arange(ny), indexing="ij")
+    m[eoff[1] + (i + ey[0] * j).ravel()] = True
+    m[eoff[2]:] = True
+    return m
+
+
+def eliminate_cotree_edges(dims, fluxes, known):
+    """FIFO greedy face elimination (_kernels.py:12-76), pure Python loops:
+    small cases only.  Returns (values, undetermined)."""
+    edges, signs = face_edge_incidence(dims)
+    known = known.astype(np.uint8).copy()
+    values = np.zeros(known.size)
+    counts = (4 - known[edges].sum(axis=1)).astype(np.int64)
+    nf = edges.shape[0]
+    incident = [[] for _ in range(known.size)]
+    for f in range(nf):
+        for m in range(4):
+            incident[edges[f, m]].append(f)
+    undetermined = int((known == 0).sum())
+    queue = [f for f in range(nf) if counts[f] == 1]
+    head = 0
+    while head < len(queue):
+        f = queue[head]
+        head += 1
+        if counts[f] != 1:
+            continue
+        acc, ue, us = 0.0, -1, 0.0
+        for m in range(4):
+            e, s = edges[f, m], float(signs[f, m])
+            if known[e]:
+                acc += s * values[e]
+            else:
+                ue, us = e, s
+        values[ue] = (fluxes[f] - acc) / us
+        known[ue] = 1
+        undetermined -= 1
+        for g in incident[ue]:
+            counts[g] -= 1
+            if counts[g] == 1:
+                queue.append(g)
+    return values, undetermined
+
+
+def percentile99(values):
+    """Nearest-rank p99 (dosimetry.py:119-127)."""
+    values = np.asarray(values)
+    n = values.size
+    idx = -((-99 * n) // 100) - 1
+    return float(np.partition(values, idx)[idx])
+
+
+def exposure_stats(values, tissue_of_value, rms=False):
+    """build_exposure_report statistics (dosimetry.py:195-234):
+    scaled values, global (p99, max), {tid: (count, mean, max, p99)}."""
+    v = np.asarray(values, np.float64)
+    if rms:
+        v = v * (1.0 / math.sqrt(2.0))
+    per = {}
+    for tid in np.unique(tissue_of_value):
+        if int(tid) == 0:
+            continue
+        sel = v[tissue_of_value == tid]
+        per[int(tid)] = (int(sel.size), float(sel.mean()), float(sel.max()), percentile99(sel))
+    return v, (percentile99(v), float(v.max())), per

@@ -12,7 +12,7 @@ import os
 
 import torch
 
-from .errors import EmptySystemError, SolverError
+from .errors import EmptySystemError, LatticeError, ProjectionError, SingularPointError, SolverError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libspfd_b200.so")
@@ -26,6 +26,10 @@ SPFD_ENOCONV = 5
 SPFD_ECUDA = 6
 SPFD_ENCCL = 7
 SPFD_ENOMEM = 8
+SPFD_EINCOMPAT = 9
+SPFD_EPROJECTION = 10
+SPFD_ELATTICE = 11
+SPFD_ESINGULAR = 12
 
 EXPORT_EDGE_CONDUCTANCE = 0
 EXPORT_DOF_TO_NODE = 1
@@ -82,6 +86,34 @@ class AmgInfo(ctypes.Structure):
     ]
 
 
+class Box(ctypes.Structure):
+    _fields_ = [("dims", ctypes.c_int64 * 3), ("spacing", ctypes.c_double * 3), ("origin", ctypes.c_double * 3)]
+
+
+def make_box(dims, spacing, origin):
+    b = Box()
+    for a in range(3):
+        b.dims[a] = int(dims[a])
+        b.spacing[a] = float(spacing[a])
+        b.origin[a] = float(origin[a])
+    return b
+
+
+class CleanInfo(ctypes.Structure):
+    _fields_ = [
+        ("rel_before", ctypes.c_double),
+        ("rel_after", ctypes.c_double),
+        ("solved", ctypes.c_int32),
+        ("iterations", ctypes.c_int32),
+        ("solve_rel_residual", ctypes.c_double),
+        ("setup_seconds", ctypes.c_double),
+    ]
+
+
+class GaugeInfo(ctypes.Structure):
+    _fields_ = [("rel_residual", ctypes.c_double), ("worst_face", ctypes.c_int64), ("worst_defect", ctypes.c_double)]
+
+
 class Report(ctypes.Structure):
     _fields_ = [
         ("iterations", ctypes.c_int32),
@@ -128,6 +160,15 @@ _SIGS = {
     "spfd_comm_init_callbacks": (_INT, [_VP, _INT, _INT, _VP]),
     "spfd_comm_destroy": (_INT, [_VP]),
     "spfd_amg_distribute": (_INT, [_VP, _VP, _I64, _VP, _VP]),
+    "spfd_field_create": (_INT, [_VP, _VP, _VP]),
+    "spfd_field_destroy": (_INT, [_VP]),
+    "spfd_coil_field": (_INT, [_I64, _VP, _INT, _VP, _D, _VP, _VP]),
+    "spfd_field_interpolate": (_INT, [_VP, _VP, _VP, _VP, _VP]),
+    "spfd_field_divergence": (_INT, [_VP, _VP, _VP, _VP]),
+    "spfd_field_clean": (_INT, [_VP, _VP, _VP, _D, _VP, _VP]),
+    "spfd_field_gauge": (_INT, [_VP, _VP, _VP, _D, _VP, _VP]),
+    "spfd_field_circulation": (_INT, [_VP, _VP, _VP, _VP, _VP]),
+    "spfd_exposure_stats": (_INT, [_VP, _I64, _D, _VP, _VP, ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
 }
 
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
@@ -192,6 +233,12 @@ def check(rc):
         raise EmptySystemError(msg)
     if rc == SPFD_ENOMEM:
         raise MemoryError(msg)
+    if rc == SPFD_EPROJECTION:
+        raise ProjectionError(msg)
+    if rc == SPFD_ELATTICE:
+        raise LatticeError(msg)
+    if rc == SPFD_ESINGULAR:
+        raise SingularPointError(msg)
     raise RuntimeError(f"spfd_b200 error {rc}: {msg}")
 
 

@@ -5,6 +5,7 @@
 
 #include "amg.cuh"
 #include "comm.cuh"
+#include "field.cuh"
 
 struct spfd_op_s {
     spfd::Operator *op;
@@ -15,6 +16,10 @@ struct spfd_amg_s {
 };
 struct spfd_comm_s {
     spfd::Comm *comm;
+};
+struct spfd_field_s {
+    spfd::Field *f;
+    int64_t n_faces, n_cells, n_edges;
 };
 
 namespace spfd {
@@ -321,6 +326,96 @@ int spfd_bench_kernel(spfd_amg_t h, int which, int reps, int nrhs, double *h_ms,
     return guarded([&] {
         SPFD_CHECK(h && h_ms && h_bytes && which >= 0 && which <= 3, SPFD_EINVAL, "bad argument");
         *h_ms = amg_bench_kernel(*h->amg, which, reps, nrhs, h_bytes, S(stream));
+    });
+}
+
+static void check_box(const spfd_box *b, bool lattice) {
+    SPFD_CHECK(b, SPFD_EINVAL, "null box");
+    for (int a = 0; a < 3; ++a) {
+        SPFD_CHECK(lattice ? b->dims[a] >= 1 : b->dims[a] >= 0, SPFD_EINVAL,
+                   lattice ? "lattice dims must be >= 1" : "dims must be three integers >= 0");
+        SPFD_CHECK(b->spacing[a] > 0.0, SPFD_EINVAL, "spacing must be positive");
+    }
+}
+
+int spfd_field_create(const spfd_box *grid, const spfd_config *cfg, spfd_field_t *out) {
+    return guarded([&] {
+        SPFD_CHECK(out, SPFD_EINVAL, "null argument");
+        check_box(grid, false);
+        check_cfg(cfg);
+        const int64_t nx = grid->dims[0], ny = grid->dims[1], nz = grid->dims[2];
+        auto *h = new spfd_field_s{nullptr, (nx + 1) * ny * nz + nx * (ny + 1) * nz + nx * ny * (nz + 1), nx * ny * nz,
+                                   nx * (ny + 1) * (nz + 1) + (nx + 1) * ny * (nz + 1) + (nx + 1) * (ny + 1) * nz};
+        try {
+            h->f = field_create(*grid, *cfg);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int spfd_field_destroy(spfd_field_t f) {
+    return guarded([&] {
+        if (!f) return;
+        field_destroy(f->f);
+        delete f;
+    });
+}
+
+int spfd_coil_field(int64_t n, const double *pts, int nseg, const double *verts, double scale, double *out,
+                    void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(n >= 0 && nseg >= 1 && (n == 0 || (pts && verts && out)), SPFD_EINVAL, "bad argument");
+        coil_field(n, pts, nseg, verts, scale, out, S(stream));
+    });
+}
+
+int spfd_field_interpolate(spfd_field_t f, const spfd_box *lattice, const double *b, double *flux, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(f && b && flux, SPFD_EINVAL, "null argument");
+        check_box(lattice, true);
+        field_interpolate(*f->f, *lattice, b, flux, S(stream));
+    });
+}
+
+int spfd_field_divergence(spfd_field_t f, const double *flux, double *div, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(f && flux && div, SPFD_EINVAL, "null argument");
+        field_divergence(*f->f, flux, div, S(stream));
+    });
+}
+
+int spfd_field_clean(spfd_field_t f, const double *in, double *out, double tol, spfd_clean_info *info, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(f && in && out && info, SPFD_EINVAL, "null argument");
+        field_clean(*f->f, in, out, tol, info, S(stream));
+    });
+}
+
+int spfd_field_gauge(spfd_field_t f, const double *flux, double *a, double tol, spfd_gauge_info *info, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(f && flux && a && info, SPFD_EINVAL, "null argument");
+        field_gauge_comb(*f->f, flux, a, tol, info, S(stream));
+    });
+}
+
+int spfd_field_circulation(spfd_field_t f, const double *a, const double *flux, double *defect, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(f && a && flux && defect, SPFD_EINVAL, "null argument");
+        field_circulation(*f->f, a, flux, defect, S(stream));
+    });
+}
+
+int spfd_exposure_stats(const double *values, int64_t n, double scale, const int64_t *vox_index,
+                        const uint16_t *ids_box, int32_t n_ids, double *scaled, int64_t *h_count, double *h_mean,
+                        double *h_max, double *h_p99, double *h_global, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(values && vox_index && ids_box && scaled && h_count && h_mean && h_max && h_p99 && h_global,
+                   SPFD_EINVAL, "null argument");
+        exposure_stats(values, n, scale, vox_index, ids_box, n_ids, scaled, h_count, h_mean, h_max, h_p99, h_global,
+                       S(stream));
     });
 }
 

@@ -1,0 +1,700 @@
+// SURVEY §8 rows f1-f4 on the device: the stages either side of the Poisson
+// hot path that turn sampled flux densities into the edge vector potential
+// and the voxel |E| into exposure statistics.
+//
+//   f3  coil_field (Biot-Savart, field_source.py:163-197) and
+//       interpolate_to_faces (trilinear midpoint flux, field_source.py:218-272)
+//   f2  divergence (build_divergence, fit_operators.py:276-286) and
+//       divergence_clean (field_source.py:292-329): the l2-minimal
+//       projection through an AMG-preconditioned solve on div divᵀ, reusing
+//       the hot path's own setup and Krylov solver
+//   f1  comb-tree gauging (gauging.py:34-71,137-172 + _kernels.py:12-76) as
+//       three column prefix scans, plus the circulation residual check
+//   f4  exposure statistics (dosimetry.py:119-127,195-234): nearest-rank
+//       p99 / max / mean, globally and per tissue, via radix sorts
+//
+// Bit-exactness: interpolation, divergence, div-transpose and the gauge scans
+// use explicitly rounded operations in the reference's evaluation order, so
+// they equal numpy bit for bit; p99 and max are exact selections.  Norms
+// (threshold tests only), means and the cleaning solve are floating-point
+// reductions compared within tolerance.
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "amg.cuh"
+#include "common.cuh"
+#include "field.cuh"
+
+namespace spfd {
+namespace {
+
+// ------------------------------------------------------------- geometry --
+struct Box {
+    int64_t n[3];   // grid: voxels per axis; lattice: points per axis
+    double h[3];
+    double o[3];
+};
+
+inline Box box_of(const spfd_box &b) {
+    Box r;
+    for (int a = 0; a < 3; ++a) { r.n[a] = b.dims[a]; r.h[a] = b.spacing[a]; r.o[a] = b.origin[a]; }
+    return r;
+}
+
+__host__ __device__ inline int64_t face_count(const Box &g, int a) {
+    int64_t c = 1;
+    for (int d = 0; d < 3; ++d) c *= g.n[d] + (d == a ? 1 : 0);
+    return c;
+}
+__host__ __device__ inline int64_t edge_count(const Box &g, int a) {
+    int64_t c = 1;
+    for (int d = 0; d < 3; ++d) c *= g.n[d] + (d == a ? 0 : 1);
+    return c;
+}
+
+// face-center coordinate along axis `d` of a face with normal `a`
+// (StaggeredGrid.face_center_axes, fit_operators.py:156-165)
+__host__ __device__ inline double face_coord(const Box &g, int a, int d, int64_t i) {
+#ifdef __CUDA_ARCH__
+    if (d == a) return __dadd_rn(g.o[d], __dmul_rn((double)i, g.h[d]));
+    return __dadd_rn(g.o[d], __dmul_rn(__dadd_rn((double)i, 0.5), g.h[d]));
+#else
+    volatile double t = d == a ? (double)i : (double)i + 0.5;
+    volatile double m = t * g.h[d];
+    return g.o[d] + m;
+#endif
+}
+
+// ----------------------------------------------------- f3: interpolation --
+// _axis_interp_params (field_source.py:218-233): base index, local coordinate
+// and the corner step (0 on a single-point axis).
+struct AxisParam {
+    int64_t i0;
+    double t;
+    int64_t s;
+};
+
+__device__ inline AxisParam axis_param(double c, double origin, double spacing, int64_t n) {
+    const double u = __ddiv_rn(__dsub_rn(c, origin), spacing);
+    if (n == 1) return {0, 0.0, 0};
+    int64_t i0 = (int64_t)floor(u);
+    i0 = i0 < 0 ? 0 : (i0 > n - 2 ? n - 2 : i0);
+    return {i0, __dsub_rn(u, (double)i0), 1};
+}
+
+// fluxes of the faces with normal `a` (_trilinear + interpolate_to_faces,
+// field_source.py:235-272): out = sum over the 8 corners in (dx, dy, dz)
+// order of ((wx*wy)*wz)*corner, then times the face area.
+__global__ void k_interp_faces(Box g, Box lat, int a, const double *__restrict__ b, double area,
+                               double *__restrict__ flux) {
+    int64_t d[3] = {g.n[0], g.n[1], g.n[2]};
+    d[a] += 1;
+    const int64_t nf = d[0] * d[1] * d[2];
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = f % d[0], j = (f / d[0]) % d[1], k = f / (d[0] * d[1]);
+        const AxisParam px = axis_param(face_coord(g, a, 0, i), lat.o[0], lat.h[0], lat.n[0]);
+        const AxisParam py = axis_param(face_coord(g, a, 1, j), lat.o[1], lat.h[1], lat.n[1]);
+        const AxisParam pz = axis_param(face_coord(g, a, 2, k), lat.o[2], lat.h[2], lat.n[2]);
+        double out = 0.0;
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+            const double wx = dx ? px.t : __dsub_rn(1.0, px.t);
+#pragma unroll
+            for (int dy = 0; dy < 2; ++dy) {
+                const double wy = dy ? py.t : __dsub_rn(1.0, py.t);
+                const double wxy = __dmul_rn(wx, wy);
+#pragma unroll
+                for (int dz = 0; dz < 2; ++dz) {
+                    const double wz = dz ? pz.t : __dsub_rn(1.0, pz.t);
+                    const int64_t p = (px.i0 + dx * px.s) + lat.n[0] * ((py.i0 + dy * py.s) + lat.n[1] * (pz.i0 + dz * pz.s));
+                    out = __dadd_rn(out, __dmul_rn(__dmul_rn(wxy, wz), b[3 * p + a]));
+                }
+            }
+        }
+        flux[f] = __dmul_rn(out, area);
+    }
+}
+
+// Biot-Savart field of a closed polyline (coil_field, field_source.py:163-197):
+// exact finite straight-wire expression per segment.  flag[0] is set when a
+// point lies within `eps` of a wire segment (SingularPointError).
+__global__ void k_coil_field(int64_t n, const double *__restrict__ pts, int nseg, const double *__restrict__ verts,
+                             double scale, double eps2, double *__restrict__ out, int *flag) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const double px = pts[3 * q], py = pts[3 * q + 1], pz = pts[3 * q + 2];
+        double bx = 0.0, by = 0.0, bz = 0.0;
+        bool singular = false;
+        for (int s = 0; s < nseg; ++s) {
+            const double x1 = verts[3 * s], y1 = verts[3 * s + 1], z1 = verts[3 * s + 2];
+            const double sx = verts[3 * s + 3] - x1, sy = verts[3 * s + 4] - y1, sz = verts[3 * s + 5] - z1;
+            const double l2 = sx * sx + sy * sy + sz * sz;
+            const double ax = px - x1, ay = py - y1, az = pz - z1;
+            const double cx = ax - sx, cy = ay - sy, cz = az - sz;   // b = a - seg
+            double t = (ax * sx + ay * sy + az * sz) / l2;
+            t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+            const double qx = ax - t * sx, qy = ay - t * sy, qz = az - t * sz;
+            if (qx * qx + qy * qy + qz * qz < eps2) singular = true;
+            const double la = sqrt(ax * ax + ay * ay + az * az);
+            const double lb = sqrt(cx * cx + cy * cy + cz * cz);
+            const double crx = ay * cz - az * cy, cry = az * cx - ax * cz, crz = ax * cy - ay * cx;
+            const double sum = la + lb;
+            const double coeff = 2.0 * sum / (la * lb * (sum * sum - l2));
+            bx += coeff * crx;
+            by += coeff * cry;
+            bz += coeff * crz;
+        }
+        if (singular) atomicExch(flag, 1);
+        out[3 * q] = scale * bx;
+        out[3 * q + 1] = scale * by;
+        out[3 * q + 2] = scale * bz;
+    }
+}
+
+// ------------------------------------------------------ f2: divergence --
+// net outflux per cell = build_divergence(grid) @ fluxes: the six faces in
+// ascending face index (x-, x+, y-, y+, z-, z+) with signs -,+,-,+,-,+,
+// accumulated like scipy's csr_matvec.
+__global__ void k_divergence(Box g, const double *__restrict__ f, double *__restrict__ div) {
+    const int64_t nx = g.n[0], ny = g.n[1], nz = g.n[2];
+    const int64_t nc = nx * ny * nz;
+    const int64_t fx = (nx + 1) * ny * nz, fy = nx * (ny + 1) * nz;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+        const int64_t x0 = i + (nx + 1) * (j + ny * k);
+        const int64_t y0 = fx + i + nx * (j + (ny + 1) * k);
+        const int64_t z0 = fx + fy + c;
+        double s = 0.0;
+        s = __dadd_rn(s, __dmul_rn(-1.0, f[x0]));
+        s = __dadd_rn(s, f[x0 + 1]);
+        s = __dadd_rn(s, __dmul_rn(-1.0, f[y0]));
+        s = __dadd_rn(s, f[y0 + nx]);
+        s = __dadd_rn(s, __dmul_rn(-1.0, f[z0]));
+        s = __dadd_rn(s, f[z0 + nx * ny]);
+        div[c] = s;
+    }
+}
+
+// out = in - divᵀ phi: a face gets +phi of the cell on its low side (it is
+// that cell's "+" face) and -phi of the cell on its high side, accumulated in
+// ascending cell order like scipy's csc_matvec of div.T.
+__global__ void k_sub_div_transpose(Box g, const double *__restrict__ phi, const double *__restrict__ in,
+                                    double *__restrict__ out) {
+    const int64_t nx = g.n[0], ny = g.n[1], nz = g.n[2];
+    const int64_t fx = (nx + 1) * ny * nz, fy = nx * (ny + 1) * nz, fz = nx * ny * (nz + 1);
+    const int64_t nf = fx + fy + fz;
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = -1, hi = -1;
+        if (f < fx) {
+            const int64_t i = f % (nx + 1), r = f / (nx + 1);          // r = j + ny k
+            const int64_t c = i + nx * r;
+            if (i > 0) lo = c - 1;
+            if (i < nx) hi = c;
+        } else if (f < fx + fy) {
+            const int64_t q = f - fx;
+            const int64_t i = q % nx, j = (q / nx) % (ny + 1), k = q / (nx * (ny + 1));
+            const int64_t c = i + nx * (j + ny * k);
+            if (j > 0) lo = c - nx;
+            if (j < ny) hi = c;
+        } else {
+            const int64_t q = f - fx - fy;
+            const int64_t k = q / (nx * ny);
+            if (k > 0) lo = q - nx * ny;
+            if (k < nz) hi = q;
+        }
+        double y = 0.0;
+        if (lo >= 0) y = __dadd_rn(y, phi[lo]);
+        if (hi >= 0) y = __dadd_rn(y, __dmul_rn(-1.0, phi[hi]));
+        out[f] = __dsub_rn(in[f], y);
+    }
+}
+
+// div divᵀ as CSR with sorted columns (the reference sorts before setup,
+// linsolve.py:131-132): diagonal 6, -1 per interior face shared with a
+// neighbour cell.
+__global__ void k_normal_count(Box g, int64_t *cnt) {
+    const int64_t nx = g.n[0], ny = g.n[1], nz = g.n[2], nc = nx * ny * nz;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+        cnt[c] = 1 + (i > 0) + (i < nx - 1) + (j > 0) + (j < ny - 1) + (k > 0) + (k < nz - 1);
+    }
+}
+
+__global__ void k_normal_fill(Box g, const int64_t *__restrict__ ptr, int32_t *__restrict__ col,
+                              double *__restrict__ val) {
+    const int64_t nx = g.n[0], ny = g.n[1], nz = g.n[2], nc = nx * ny * nz;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+        int64_t q = ptr[c];
+        auto put = [&](int64_t cc, double v) { col[q] = (int32_t)cc; val[q] = v; ++q; };
+        if (k > 0) put(c - nx * ny, -1.0);
+        if (j > 0) put(c - nx, -1.0);
+        if (i > 0) put(c - 1, -1.0);
+        put(c, 6.0);
+        if (i < nx - 1) put(c + 1, -1.0);
+        if (j < ny - 1) put(c + nx, -1.0);
+        if (k < nz - 1) put(c + nx * ny, -1.0);
+    }
+}
+
+// --------------------------------------------------------- f1: gauging --
+// Comb tree (gauging.py:34-71): x-edges on the line (., 0, 0), y-edges in the
+// plane (., ., 0) and every z-edge carry 0.  Each remaining edge is fixed by
+// one face circulation, which unrolls into running sums:
+//   a_x(i, j+1, 0) = -sum_{j'<=j} b_z(i, j', 0)
+//   a_x(i, j, k+1) = a_x(i, j, 0) + sum_{k'<=k} b_y(i, j, k')
+//   a_y(i, j, k+1) = -sum_{k'<=k} b_x(i, j, k')
+// Each running sum is sequential in the scan index (numpy cumsum order).
+
+// a_x on the k = 0 plane: one thread per i, scanning j
+__global__ void k_gauge_ax0(int64_t nx, int64_t ny, const double *__restrict__ bz, double *__restrict__ ax) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nx) return;
+    ax[i] = 0.0;
+    double c = 0.0;
+    for (int64_t j = 0; j < ny; ++j) {
+        c = __dadd_rn(c, bz[i + nx * j]);
+        ax[i + nx * (j + 1)] = -c;
+    }
+}
+
+// column scans along k for A*B columns: dst(col, k+1) = base(col) + c_k
+// (NEG: -c_k, base unused), c_k the running sum of src(col, 0..k).  U loads
+// are issued ahead of the dependent adds.
+template <bool NEG, int U>
+__global__ void __launch_bounds__(128) k_gauge_kscan(int64_t ncol, int64_t nk, const double *__restrict__ src,
+                                                     double *__restrict__ dst) {
+    const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (col >= ncol) return;
+    const double base = NEG ? 0.0 : dst[col];
+    if (NEG) dst[col] = 0.0;
+    double c = 0.0;
+    int64_t k = 0;
+    for (; k + U <= nk; k += U) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(src + col + ncol * (k + u));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            c = __dadd_rn(c, v[u]);
+            __stcs(dst + col + ncol * (k + u + 1), NEG ? -c : __dadd_rn(base, c));
+        }
+    }
+    for (; k < nk; ++k) {
+        c = __dadd_rn(c, src[col + ncol * k]);
+        dst[col + ncol * (k + 1)] = NEG ? -c : __dadd_rn(base, c);
+    }
+}
+
+__global__ void k_zero(int64_t n, double *p) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+        p[q] = 0.0;
+}
+
+// per-face circulation defect (gauging.py:127-134, right-handed boundary
+// +e1(base) +e2(base+e1) -e1(base+e2) -e2(base), fit_operators.py:186-224)
+__global__ void k_circulation(Box g, const double *__restrict__ a, const double *__restrict__ flux,
+                              double *__restrict__ defect) {
+    const int64_t nx = g.n[0], ny = g.n[1], nz = g.n[2];
+    const int64_t F0 = (nx + 1) * ny * nz, F1 = nx * (ny + 1) * nz, F2 = nx * ny * (nz + 1);
+    const int64_t E0 = nx * (ny + 1) * (nz + 1), E1 = (nx + 1) * ny * (nz + 1);
+    const int64_t nf = F0 + F1 + F2;
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+        int ax;
+        int64_t q;
+        if (f < F0) { ax = 0; q = f; }
+        else if (f < F0 + F1) { ax = 1; q = f - F0; }
+        else { ax = 2; q = f - F0 - F1; }
+        int64_t fd[3] = {nx, ny, nz};
+        fd[ax] += 1;
+        int64_t c[3] = {q % fd[0], (q / fd[0]) % fd[1], q / (fd[0] * fd[1])};
+        auto edge = [&](int e, int64_t i, int64_t j, int64_t k) -> double {
+            int64_t ed[3] = {nx + 1, ny + 1, nz + 1};
+            ed[e] -= 1;
+            const int64_t off = e == 0 ? 0 : (e == 1 ? E0 : E0 + E1);
+            return a[off + i + ed[0] * (j + ed[1] * k)];
+        };
+        const int e1 = (ax + 1) % 3, e2 = (ax + 2) % 3;
+        int64_t s1[3] = {c[0], c[1], c[2]}, s2[3] = {c[0], c[1], c[2]};
+        s1[e1] += 1;
+        s2[e2] += 1;
+        double circ = edge(e1, c[0], c[1], c[2]);
+        circ += edge(e2, s1[0], s1[1], s1[2]);
+        circ -= edge(e1, s2[0], s2[1], s2[2]);
+        circ -= edge(e2, c[0], c[1], c[2]);
+        defect[f] = circ - flux[f];
+    }
+}
+
+// ------------------------------------------------- deterministic norms --
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 148 * 4;
+
+__global__ void __launch_bounds__(kRedThreads) k_sumsq_partial(int64_t n, const double *__restrict__ x,
+                                                               double *__restrict__ part) {
+    __shared__ double red[32];
+    double v[1] = {0.0};
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+        v[0] = fma(x[q], x[q], v[0]);
+    block_sum<1>(v, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+}
+
+// lowest index of the largest |x| (np.argmax(np.abs(x)))
+__global__ void __launch_bounds__(kRedThreads) k_argmax_partial(int64_t n, const double *__restrict__ x,
+                                                                double *__restrict__ pv, int64_t *__restrict__ pi) {
+    __shared__ double sv[kRedThreads];
+    __shared__ int64_t si[kRedThreads];
+    double bv = -1.0;
+    int64_t bi = -1;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const double a = fabs(x[q]);
+        if (a > bv) { bv = a; bi = q; }
+    }
+    sv[threadIdx.x] = bv;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int o = kRedThreads / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            const double ov = sv[threadIdx.x + o];
+            const int64_t oi = si[threadIdx.x + o];
+            if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi >= 0 && (si[threadIdx.x] < 0 || oi < si[threadIdx.x]))) {
+                sv[threadIdx.x] = ov;
+                si[threadIdx.x] = oi;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { pv[blockIdx.x] = sv[0]; pi[blockIdx.x] = si[0]; }
+}
+
+// --------------------------------------------------- f4: statistics --
+__global__ void k_stats_prep(int64_t n, const double *__restrict__ values, double scale,
+                             const int64_t *__restrict__ vox_index, const uint16_t *__restrict__ ids_box, int32_t n_ids,
+                             double *__restrict__ scaled, int32_t *__restrict__ ids, int64_t *__restrict__ counts) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        scaled[q] = __dmul_rn(values[q], scale);
+        int32_t id = ids_box[vox_index[q]];
+        ids[q] = id;
+        if (id >= n_ids) id = n_ids;   // overflow slot: reported as an error
+        atomicAdd(reinterpret_cast<unsigned long long *>(counts + id), 1ull);
+    }
+}
+
+// per-id nearest-rank p99 (index ceil(0.99 c) - 1) and max of the
+// value-sorted segments; row n_ids holds the global statistics
+__global__ void k_stats_pick(int32_t n_ids, const int64_t *__restrict__ off, const int64_t *__restrict__ cnt,
+                             const double *__restrict__ seg_vals, const double *__restrict__ sorted_vals, int64_t n,
+                             double *__restrict__ p99, double *__restrict__ mx) {
+    const int32_t id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id > n_ids) return;
+    const int64_t c = id < n_ids ? cnt[id] : n;
+    const double *v = id < n_ids ? seg_vals + off[id] : sorted_vals;
+    if (c == 0) { p99[id] = 0.0; mx[id] = 0.0; return; }
+    const int64_t rank = (99 * c + 99) / 100;   // ceil(0.99 c) = -((-99 c) // 100)
+    p99[id] = v[rank - 1];
+    mx[id] = v[c - 1];
+}
+
+}  // namespace
+
+// ======================================================================= host
+
+struct Field {
+    Box g;
+    spfd_config cfg;
+    DevBuf<double> part;      // reduction partials
+    DevBuf<int64_t> parti;
+    DevBuf<double> wc, wf;    // cell / face workspaces
+    Amg *clean_amg = nullptr; // AMG on div divᵀ (built on first use)
+    double clean_setup_seconds = 0.0;
+    ~Field() { delete clean_amg; }
+    int64_t n_cells() const { return g.n[0] * g.n[1] * g.n[2]; }
+    int64_t n_faces() const { return face_count(g, 0) + face_count(g, 1) + face_count(g, 2); }
+    int64_t n_edges() const { return edge_count(g, 0) + edge_count(g, 1) + edge_count(g, 2); }
+};
+
+namespace {
+
+double sumsq(Field &F, const double *x, int64_t n, cudaStream_t s) {
+    if (n == 0) return 0.0;
+    k_sumsq_partial<<<kRedBlocks, kRedThreads, 0, s>>>(n, x, F.part.get());
+    SPFD_LAUNCH_CHECK();
+    std::vector<double> h(kRedBlocks);
+    SPFD_CUDA(cudaMemcpyAsync(h.data(), F.part.get(), kRedBlocks * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    double t = 0.0;
+    for (double v : h) t += v;  // fixed order
+    return t;
+}
+
+int64_t argmax_abs(Field &F, const double *x, int64_t n, double *h_val, cudaStream_t s) {
+    k_argmax_partial<<<kRedBlocks, kRedThreads, 0, s>>>(n, x, F.part.get(), F.parti.get());
+    SPFD_LAUNCH_CHECK();
+    std::vector<double> v(kRedBlocks);
+    std::vector<int64_t> ix(kRedBlocks);
+    SPFD_CUDA(cudaMemcpyAsync(v.data(), F.part.get(), kRedBlocks * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaMemcpyAsync(ix.data(), F.parti.get(), kRedBlocks * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    double bv = -1.0;
+    int64_t bi = -1;
+    for (int b = 0; b < kRedBlocks; ++b)
+        if (ix[b] >= 0 && (v[b] > bv || (v[b] == bv && ix[b] < bi))) { bv = v[b]; bi = ix[b]; }
+    if (bi >= 0 && h_val) SPFD_CUDA(cudaMemcpy(h_val, x + bi, sizeof(double), cudaMemcpyDeviceToHost));
+    return bi;
+}
+
+inline int blocks(int64_t n, int t = 256) { return grid_for(n, t, 148 * 32); }
+
+}  // namespace
+
+Field *field_create(const spfd_box &grid, const spfd_config &cfg) {
+    auto *F = new Field();
+    F->g = box_of(grid);
+    F->cfg = cfg;
+    F->part.alloc(kRedBlocks);
+    F->parti.alloc(kRedBlocks);
+    return F;
+}
+
+void field_destroy(Field *F) { delete F; }
+
+void field_check_lattice(const Field &F, const spfd_box &lat) {
+    const Box L = box_of(lat);
+    for (int a = 0; a < 3; ++a) {
+        SPFD_CHECK(L.n[a] >= 1, SPFD_EINVAL, "lattice dims must be >= 1");
+        SPFD_CHECK(L.h[a] > 0.0, SPFD_EINVAL, "lattice spacing must be positive");
+    }
+    // a single-point lattice axis supports only queries on that plane
+    for (int d = 0; d < 3; ++d) {
+        if (L.n[d] != 1) continue;
+        for (int a = 0; a < 3; ++a) {
+            const int64_t m = F.g.n[d] + (d == a ? 1 : 0);
+            for (int64_t i = 0; i < m; ++i)
+                SPFD_CHECK(std::fabs(face_coord(F.g, a, d, i) - L.o[d]) <= 1e-9, SPFD_ELATTICE,
+                           "lattice has a single point along an axis that requires interpolation");
+        }
+    }
+}
+
+void field_interpolate(Field &F, const spfd_box &lat, const double *b, double *flux, cudaStream_t s) {
+    field_check_lattice(F, lat);
+    const Box L = box_of(lat);
+    int64_t off = 0;
+    for (int a = 0; a < 3; ++a) {
+        const int t0 = a == 0 ? 1 : 0, t1 = a == 2 ? 1 : 2;
+        const double area = F.g.h[t0] * F.g.h[t1];
+        const int64_t nf = face_count(F.g, a);
+        if (nf) {
+            k_interp_faces<<<blocks(nf), 256, 0, s>>>(F.g, L, a, b, area, flux + off);
+            SPFD_LAUNCH_CHECK();
+        }
+        off += nf;
+    }
+}
+
+void coil_field(int64_t n, const double *pts, int nseg, const double *verts, double scale, double *out,
+                cudaStream_t s) {
+    DevBuf<int> flag;
+    flag.alloc(1);
+    SPFD_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), s));
+    if (n) {
+        k_coil_field<<<blocks(n, 128), 128, 0, s>>>(n, pts, nseg, verts, scale, 1e-24, out, flag.get());
+        SPFD_LAUNCH_CHECK();
+    }
+    int h = 0;
+    SPFD_CUDA(cudaMemcpyAsync(&h, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    SPFD_CHECK(!h, SPFD_ESINGULAR, "evaluation point lies on the coil wire");
+}
+
+void field_divergence(Field &F, const double *flux, double *div, cudaStream_t s) {
+    const int64_t nc = F.n_cells();
+    if (!nc) return;
+    k_divergence<<<blocks(nc), 256, 0, s>>>(F.g, flux, div);
+    SPFD_LAUNCH_CHECK();
+}
+
+static void ensure_clean_amg(Field &F, cudaStream_t s) {
+    if (F.clean_amg) return;
+    const int64_t nc = F.n_cells();
+    DevBuf<int64_t> ptr;
+    ptr.alloc(nc + 1);
+    k_normal_count<<<blocks(nc), 256, 0, s>>>(F.g, ptr.get() + 1);
+    SPFD_LAUNCH_CHECK();
+    SPFD_CUDA(cudaMemsetAsync(ptr.get(), 0, sizeof(int64_t), s));
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb, ptr.get() + 1, ptr.get() + 1, nc, s);
+    DevBuf<unsigned char> tmp;
+    tmp.alloc(tb);
+    cub::DeviceScan::InclusiveSum(tmp.get(), tb, ptr.get() + 1, ptr.get() + 1, nc, s);
+    SPFD_LAUNCH_CHECK();
+    int64_t nnz = 0;
+    SPFD_CUDA(cudaMemcpyAsync(&nnz, ptr.get() + nc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    DevBuf<int32_t> col;
+    DevBuf<double> val;
+    col.alloc(nnz);
+    val.alloc(nnz);
+    k_normal_fill<<<blocks(nc), 256, 0, s>>>(F.g, ptr.get(), col.get(), val.get());
+    SPFD_LAUNCH_CHECK();
+    spfd_config c = F.cfg;
+    c.max_nrhs = 1;
+    F.clean_amg = amg_setup_csr(nc, nnz, ptr.get(), col.get(), val.get(), c, s);
+    F.clean_setup_seconds = F.clean_amg->setup_seconds;
+}
+
+void field_clean(Field &F, const double *in, double *out, double tol, spfd_clean_info *info, cudaStream_t s) {
+    const int64_t nc = F.n_cells(), nf = F.n_faces();
+    *info = spfd_clean_info{};
+    if (out != in) SPFD_CUDA(cudaMemcpyAsync(out, in, nf * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    const double fnorm = std::sqrt(sumsq(F, in, nf, s));
+    if (fnorm == 0.0 || nc == 0) return;
+    if (F.wc.n < (size_t)nc) F.wc.alloc(nc);
+    field_divergence(F, in, F.wc.get(), s);
+    const double rel = std::sqrt(sumsq(F, F.wc.get(), nc, s)) / fnorm;
+    info->rel_before = rel;
+    info->rel_after = rel;
+    if (rel <= tol) return;
+    ensure_clean_amg(F, s);
+    spfd_config c = F.cfg;
+    c.rel_tol = std::min(1e-12, 0.25 * tol / rel);
+    c.max_nrhs = 1;
+    Amg &h = *F.clean_amg;
+    spfd_report rep = krylov_solve(h, F.wc.get(), h.kx.get(), 1, c, nullptr, s);
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    info->solved = 1;
+    info->iterations = rep.iterations;
+    info->solve_rel_residual = rep.rel_residual[0];
+    info->setup_seconds = F.clean_setup_seconds;
+    SPFD_CHECK(rep.status != SPFD_ENONFINITE, SPFD_ENONFINITE, "non-finite value in the projection solve");
+    if (!rep.converged) {
+        char msg[160];
+        snprintf(msg, sizeof msg, "divergence projection did not converge (residual %.3e)", rep.rel_residual[0]);
+        throw Error(SPFD_EPROJECTION, msg);
+    }
+    k_sub_div_transpose<<<blocks(nf), 256, 0, s>>>(F.g, h.kx.get(), in, out);
+    SPFD_LAUNCH_CHECK();
+    field_divergence(F, out, F.wc.get(), s);
+    info->rel_after = std::sqrt(sumsq(F, F.wc.get(), nc, s)) / fnorm;
+    if (info->rel_after > tol) {
+        char msg[160];
+        snprintf(msg, sizeof msg, "divergence cleaning left relative defect %.3e > %.3e", info->rel_after, tol);
+        throw Error(SPFD_EPROJECTION, msg);
+    }
+}
+
+void field_circulation(Field &F, const double *a, const double *flux, double *defect, cudaStream_t s) {
+    const int64_t nf = F.n_faces();
+    if (!nf) return;
+    k_circulation<<<blocks(nf), 256, 0, s>>>(F.g, a, flux, defect);
+    SPFD_LAUNCH_CHECK();
+}
+
+void field_gauge_comb(Field &F, const double *flux, double *a, double tol, spfd_gauge_info *info, cudaStream_t s) {
+    const int64_t nx = F.g.n[0], ny = F.g.n[1], nz = F.g.n[2];
+    const int64_t F0 = face_count(F.g, 0), F1 = face_count(F.g, 1);
+    const int64_t E0 = edge_count(F.g, 0), E1 = edge_count(F.g, 1), E2 = edge_count(F.g, 2);
+    const int64_t nf = F.n_faces();
+    *info = spfd_gauge_info{};
+    info->worst_face = -1;
+    double *ax = a, *ay = a + E0, *az = a + E0 + E1;
+    const double fnorm = std::sqrt(sumsq(F, flux, nf, s));
+    if (fnorm == 0.0) {
+        k_zero<<<blocks(E0 + E1 + E2), 256, 0, s>>>(E0 + E1 + E2, a);
+        SPFD_LAUNCH_CHECK();
+        return;
+    }
+    const double *bx = flux, *by = flux + F0, *bz = flux + F0 + F1;
+    // a_x: k = 0 plane, then the k scans (nx * (ny+1) columns)
+    if (nx > 0) {
+        k_gauge_ax0<<<(int)((nx + 127) / 128), 128, 0, s>>>(nx, ny, bz, ax);
+        SPFD_LAUNCH_CHECK();
+        const int64_t ncol = nx * (ny + 1);
+        k_gauge_kscan<false, 16><<<(int)((ncol + 127) / 128), 128, 0, s>>>(ncol, nz, by, ax);
+        SPFD_LAUNCH_CHECK();
+    }
+    if (ny > 0) {
+        const int64_t ncol = (nx + 1) * ny;
+        k_gauge_kscan<true, 16><<<(int)((ncol + 127) / 128), 128, 0, s>>>(ncol, nz, bx, ay);
+        SPFD_LAUNCH_CHECK();
+    }
+    if (E2) {
+        k_zero<<<blocks(E2), 256, 0, s>>>(E2, az);
+        SPFD_LAUNCH_CHECK();
+    }
+    // postcondition: circulation residual over every face (gauging.py:167-171)
+    if (F.wf.n < (size_t)nf) F.wf.alloc(nf);
+    field_circulation(F, a, flux, F.wf.get(), s);
+    info->rel_residual = std::sqrt(sumsq(F, F.wf.get(), nf, s)) / fnorm;
+    if (info->rel_residual > tol) {
+        info->worst_face = argmax_abs(F, F.wf.get(), nf, &info->worst_defect, s);
+        char msg[200];
+        snprintf(msg, sizeof msg, "incompatible fluxes: relative circulation residual %.3e (worst face %lld, defect %.3e)",
+                 info->rel_residual, (long long)info->worst_face, info->worst_defect);
+        throw Error(SPFD_EINCOMPAT, msg);
+    }
+}
+
+void exposure_stats(const double *values, int64_t n, double scale, const int64_t *vox_index, const uint16_t *ids_box,
+                    int32_t n_ids, double *scaled, int64_t *h_count, double *h_mean, double *h_max, double *h_p99,
+                    double *h_global, cudaStream_t s) {
+    SPFD_CHECK(n >= 1, SPFD_EINVAL, "percentile of an empty array");
+    SPFD_CHECK(n_ids >= 1 && n_ids <= 65536, SPFD_EINVAL, "n_ids must be in [1, 65536]");
+    DevBuf<int32_t> ids, ids_sorted, seg_ids;
+    DevBuf<double> sorted, seg_vals, sums, p99, mx;
+    DevBuf<int64_t> cnt, off;
+    ids.alloc(n); ids_sorted.alloc(n); seg_ids.alloc(n);
+    sorted.alloc(n); seg_vals.alloc(n);
+    cnt.alloc(n_ids + 1); off.alloc(n_ids + 1);
+    sums.alloc(n_ids); p99.alloc(n_ids + 1); mx.alloc(n_ids + 1);
+    SPFD_CUDA(cudaMemsetAsync(cnt.get(), 0, (n_ids + 1) * sizeof(int64_t), s));
+    k_stats_prep<<<blocks(n), 256, 0, s>>>(n, values, scale, vox_index, ids_box, n_ids, scaled, ids.get(), cnt.get());
+    SPFD_LAUNCH_CHECK();
+    int end_bit = 1;
+    while ((1 << end_bit) < n_ids) ++end_bit;
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, scaled, sorted.get(), ids.get(), ids_sorted.get(), n, 0, 64, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, ids_sorted.get(), seg_ids.get(), sorted.get(), seg_vals.get(), n, 0,
+                                    end_bit, s);
+    cub::DeviceSegmentedReduce::Sum(nullptr, t3, seg_vals.get(), sums.get(), n_ids, off.get(), off.get() + 1, s);
+    DevBuf<unsigned char> tmp;
+    tmp.alloc(std::max(t1, std::max(t2, t3)));
+    size_t tb = tmp.bytes();
+    // 1) by value (global p99 / max); 2) stable by tissue id -> per-id value-sorted segments
+    SPFD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, scaled, sorted.get(), ids.get(), ids_sorted.get(), n, 0,
+                                              64, s));
+    tb = tmp.bytes();
+    SPFD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, ids_sorted.get(), seg_ids.get(), sorted.get(),
+                                              seg_vals.get(), n, 0, end_bit, s));
+    count_launch();
+    std::vector<int64_t> hc(n_ids + 1), ho(n_ids + 1, 0);
+    SPFD_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), (n_ids + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    SPFD_CHECK(hc[n_ids] == 0, SPFD_EINVAL, "tissue id >= n_ids");
+    for (int32_t i = 0; i < n_ids; ++i) ho[i + 1] = ho[i] + hc[i];
+    SPFD_CUDA(cudaMemcpyAsync(off.get(), ho.data(), (n_ids + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    tb = tmp.bytes();
+    SPFD_CUDA(cub::DeviceSegmentedReduce::Sum(tmp.get(), tb, seg_vals.get(), sums.get(), n_ids, off.get(),
+                                              off.get() + 1, s));
+    k_stats_pick<<<(n_ids + 1 + 127) / 128, 128, 0, s>>>(n_ids, off.get(), cnt.get(), seg_vals.get(), sorted.get(), n,
+                                                         p99.get(), mx.get());
+    SPFD_LAUNCH_CHECK();
+    std::vector<double> hs(n_ids), hp(n_ids + 1), hm(n_ids + 1);
+    SPFD_CUDA(cudaMemcpyAsync(hs.data(), sums.get(), n_ids * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaMemcpyAsync(hp.data(), p99.get(), (n_ids + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaMemcpyAsync(hm.data(), mx.get(), (n_ids + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    for (int32_t i = 0; i < n_ids; ++i) {
+        h_count[i] = hc[i];
+        h_mean[i] = hc[i] ? hs[i] / (double)hc[i] : 0.0;
+        h_max[i] = hm[i];
+        h_p99[i] = hp[i];
+    }
+    h_global[0] = hp[n_ids];
+    h_global[1] = hm[n_ids];
+}
+
+}  // namespace spfd

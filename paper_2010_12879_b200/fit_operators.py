@@ -106,6 +106,55 @@ class StaggeredGrid:
         t = [a for a in range(3) if a != axis]
         return s[t[0]] * s[t[1]]
 
+    # -- faces (fit_operators.py:72-165) -------------------------------------
+
+    def face_dims(self, axis: int):
+        d = list(self.dims)
+        d[axis] = self.dims[axis] + 1
+        return tuple(d)
+
+    @cached_property
+    def face_counts(self):
+        return tuple(int(np.prod(self.face_dims(a))) for a in range(3))
+
+    @cached_property
+    def face_offsets(self):
+        fx, fy, _ = self.face_counts
+        return (0, fx, fx + fy)
+
+    @property
+    def n_faces(self) -> int:
+        return sum(self.face_counts)
+
+    def face_index(self, axis: int, i, j, k):
+        d = self.face_dims(axis)
+        return self.face_offsets[axis] + i + d[0] * (j + d[1] * np.asarray(k))
+
+    def face_blocks(self, vec):
+        out = []
+        for a in range(3):
+            lo = self.face_offsets[a]
+            out.append(vec[lo:lo + self.face_counts[a]].reshape(self.face_dims(a), order="F"))
+        return tuple(out)
+
+    def merge_face_blocks(self, blocks) -> np.ndarray:
+        return np.concatenate([np.asarray(b).ravel(order="F") for b in blocks])
+
+    def face_center_axes(self, axis: int):
+        """Per-axis 1-d center coordinates of the faces with the given normal."""
+        d = self.face_dims(axis)
+        out = []
+        for a in range(3):
+            if a == axis:
+                out.append(self.origin[a] + np.arange(d[a]) * self.spacing[a])
+            else:
+                out.append(self.origin[a] + (np.arange(d[a]) + 0.5) * self.spacing[a])
+        return tuple(out)
+
+    def box(self):
+        """The grid as a C-ABI `spfd_box`."""
+        return _lib.make_box(self.dims, self.spacing, self.origin)
+
 
 # ---------------------------------------------------------------------------
 # device operator

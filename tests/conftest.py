@@ -28,7 +28,9 @@ def rng():
 def golden_cases(kind="model"):
     names = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
     if kind == "model":
-        return [n for n in names if not n.startswith("laplacian")]
+        return [n for n in names if not n.startswith(("laplacian", "field"))]
+    if kind == "field":
+        return [n for n in names if n.startswith("field")]
     return [n for n in names if n.startswith("laplacian")]
 
 

@@ -191,6 +191,79 @@ def laplacian_3d(n):
             + sp.kron(sp.kron(eye, eye), d)).tocsr()
 
 
+def field_case(name):
+    """Rows f1-f4 through the reference: coil Biot-Savart samples on a lattice
+    that does not cover the grid (extrapolation), face interpolation, the
+    divergence and its cleaning, comb-tree gauging (FIFO elimination), the
+    circulation residual, the cleaning hierarchy's aggregates, and the
+    exposure report of a voxel field."""
+    grid = ro.StaggeredGrid((12, 10, 8), (0.002, 0.0025, 0.003), (0.001, -0.002, 0.0005))
+    axis = (0.2, 0.1, 1.0)
+    coil = rf.CoilSpec(center=(0.012, 0.01, -0.02), axis=axis, radius_m=0.03, current_a=5.0, segments=64)
+    lattice = rf.Lattice((0.004, -0.001, 0.002), (0.006, 0.007, 0.008), (4, 4, 3))
+    samples = rf.sample_on_lattice(coil, lattice, FREQ)
+    d = {"grid_dims": np.array(grid.dims, np.int64), "grid_spacing": np.array(grid.spacing),
+         "grid_origin": np.array(grid.origin), "lat_dims": np.array(lattice.dims, np.int64),
+         "lat_spacing": np.array(lattice.spacing), "lat_origin": np.array(lattice.origin),
+         "coil_center": np.array(coil.center), "coil_axis": np.array(axis),
+         "coil_radius": np.array(coil.radius_m), "coil_current": np.array(coil.current_a),
+         "coil_segments": np.array(coil.segments), "coil_vertices": coil.vertices(),
+         "points": samples.positions, "b": samples.b}
+    flux = rf.interpolate_to_faces(samples, grid)
+    div = ro.build_divergence(grid)
+    d["flux"] = flux
+    d["div"] = div @ flux
+    clean = rf.divergence_clean(flux, grid, 1e-10)
+    d["clean"] = clean
+    d["clean_div_rel"] = np.array(np.linalg.norm(div @ clean) / np.linalg.norm(flux))
+    tree = rg.build_tree(grid, "comb")
+    a = rg.gauge_vector_potential(clean, grid, tree, 1e-10)
+    d["a"] = a
+    d["tree_mask"] = tree.edge_mask
+    d["circ"] = rg.circulation_residual(a, clean, grid)
+    try:
+        rg.gauge_vector_potential(flux, grid, tree, 1e-10)
+        d["uncleaned_raises"] = np.array(0)
+    except Exception:
+        d["uncleaned_raises"] = np.array(1)
+    normal = (div @ div.T).tocsr()
+    cfg = rl.SolveConfig()
+    h = rl.amg_setup(normal, cfg)
+    d["normal_sizes"] = np.array(h.level_sizes, np.int64)
+    for l, agg in enumerate(aggregates(h, cfg)):
+        d[f"normal_agg{l}"] = agg
+    csr_parts("normal", h.levels[0].matrix, d)
+    # a uniform field: the cleaning is a no-op and the gauge is exact
+    usamp = rf.sample_on_lattice(rf.UniformField((0.3e-6, -0.2e-6, 1e-6)), rf.Lattice.covering(grid, (2, 2, 2)), FREQ)
+    uflux = rf.interpolate_to_faces(usamp, grid)
+    d["uniform_flux"] = uflux
+    d["uniform_a"] = rg.gauge_vector_potential(uflux, grid, tree, 1e-10)
+    # exposure report of a voxel field with ties, three tissues + free space
+    rng = np.random.default_rng(7)
+    m = rv.make_phantom("layered-block", (10, 9, 8), 0.002, layers=3, kappa_spm=[0.2, 0.05, 0.4],
+                        size_m=(0.016, 0.014, 0.012))
+    ids = m.tissue_ids.ravel(order="F")
+    idx = np.flatnonzero(ids > 0)
+    vals = np.round(rng.gamma(2.0, 1.5, idx.size), 2)
+    rep = rd.build_exposure_report(vals, idx, m, FREQ, dof_count=123, rms=True)
+    d["st_ids"] = ids.astype(np.uint16)
+    d["st_dims"] = np.array(m.dims, np.int64)
+    d["st_idx"] = idx.astype(np.int64)
+    d["st_vals"] = vals
+    d["st_scaled"] = rep.voxel_field
+    d["st_p99"] = np.array(rep.percentile99_vpm)
+    d["st_max"] = np.array(rep.max_vpm)
+    tids = sorted(rep.per_tissue)
+    d["st_tids"] = np.array(tids, np.int64)
+    d["st_count"] = np.array([rep.per_tissue[t].count for t in tids], np.int64)
+    d["st_mean"] = np.array([rep.per_tissue[t].mean for t in tids])
+    d["st_tmax"] = np.array([rep.per_tissue[t].max for t in tids])
+    d["st_tp99"] = np.array([rep.per_tissue[t].p99 for t in tids])
+    d["p99_plain"] = np.array(rd.percentile99(vals))
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(name, "faces", grid.n_faces, "normal levels", h.level_sizes)
+
+
 def main():
     rng = np.random.default_rng(20240817)
     m = block((6, 6, 6))
@@ -216,6 +289,11 @@ def main():
 
     matrix_case("laplacian12", laplacian_3d(12))
 
+    field_case("field_coil")
+
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "field":
+        field_case("field_coil")
+    else:
+        main()
