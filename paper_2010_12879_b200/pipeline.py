@@ -150,3 +150,232 @@ class _OpRef:
     def __init__(self, op: DeviceOperator):
         self._spfd_op = op
         self.shape = (op.n_dofs, op.n_dofs)
+
+
+# ---------------------------------------------------------------------------
+# end-to-end pipeline (pipeline.py:46-195 of the reference) on the device
+# ---------------------------------------------------------------------------
+
+from dataclasses import dataclass, replace  # noqa: E402
+from dataclasses import field as dataclass_field  # noqa: E402
+
+STEP_NAMES = ("interpolate", "gauge", "assemble", "solve", "efield", "report")
+
+
+@dataclass
+class PipelineConfig:
+    """Inputs and knobs for one exposure computation (pipeline.py:46-84).
+    Exactly one field source (`field_path`, `coil`, `uniform_b`) and exactly
+    one phantom (`phantom_path`, `model`)."""
+
+    phantom_path: str | None = None
+    model: object = None
+    field_path: str | None = None
+    coil: object = None
+    uniform_b: tuple | None = None
+    frequency_hz: float = 85e3
+    solve: SolveConfig = dataclass_field(default_factory=SolveConfig)
+    clean_fluxes: bool = True
+    clean_tol: float = 1e-10
+    gauge_tol: float = 1e-10
+    tree_kind: str = "comb"
+    coil_lattice_dims: tuple = (17, 17, 17)
+    out_report: str | None = None
+    out_field: str | None = None
+    latency_budget_s: float = 5.0
+    report_rms: bool = False
+
+    def __post_init__(self):
+        if not self.latency_budget_s > 0.0:
+            raise ValueError("latency budget must be positive")
+        if not self.frequency_hz > 0.0:
+            raise ValueError("frequency must be positive")
+        if sum(x is not None for x in (self.field_path, self.coil, self.uniform_b)) != 1:
+            raise ValueError("exactly one of field_path, coil, uniform_b must be set")
+        if (self.phantom_path is None) == (self.model is None):
+            raise ValueError("exactly one of phantom_path, model must be set")
+
+
+@dataclass
+class PipelineTiming:
+    """Per-stage seconds (device work synchronised at every stage end)."""
+
+    interpolate: float = 0.0
+    gauge: float = 0.0
+    assemble: float = 0.0
+    solve: float = 0.0
+    efield: float = 0.0
+    report: float = 0.0
+    total: float = 0.0
+    budget_met: bool = True
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name in STEP_NAMES}
+
+
+def _load_inputs(cfg: PipelineConfig):
+    from .field_source import Lattice, UniformField, sample_on_lattice
+    from .fit_operators import StaggeredGrid
+    from .formats import load_model, load_samples
+    model = cfg.model if cfg.model is not None else load_model(cfg.phantom_path)
+    grid = StaggeredGrid.from_model(model)
+    if cfg.field_path is not None:
+        samples = load_samples(cfg.field_path)
+    elif cfg.uniform_b is not None:
+        samples = sample_on_lattice(UniformField(cfg.uniform_b), Lattice.covering(grid, (2, 2, 2)), cfg.frequency_hz)
+    else:
+        samples = sample_on_lattice(cfg.coil, Lattice.covering(grid, cfg.coil_lattice_dims), cfg.frequency_hz)
+    return model, grid, samples
+
+
+class _Stage:
+    def __init__(self, timing: PipelineTiming, step: str):
+        self.timing, self.step = timing, step
+
+    def __enter__(self):
+        self.t0 = time.perf_counter()
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        if exc is None:
+            torch.cuda.synchronize()
+        setattr(self.timing, self.step, time.perf_counter() - self.t0)
+        if exc is not None and not isinstance(exc, PipelineError):
+            from .errors import SpfdError
+            if isinstance(exc, (SpfdError, ValueError, OSError)):
+                raise PipelineError(self.step, str(exc)) from exc
+        return False
+
+
+class PipelineState:
+    """Device state a repeated pipeline reuses: the operator of the phantom
+    and its AMG hierarchy (the reference hoists only the hierarchy,
+    pipeline.py:277-288; the operator depends on phantom and frequency only)."""
+
+    def __init__(self, model, frequency_hz: float, cfg: SolveConfig):
+        self.op = DeviceOperator(model, frequency_hz, pin=True)
+        self.hierarchy = amg_setup(_OpRef(self.op), replace(cfg, max_nrhs=1))
+        self.vox_index = self.op.export(_lib.EXPORT_VOXEL_INDICES)
+
+
+def run_pipeline(cfg: PipelineConfig, *, _hierarchy=None, _state: PipelineState | None = None):
+    """Execute the full chain on the device; returns (ExposureReport,
+    PipelineTiming) like pipeline.py:158-195.  Stage failures are re-raised
+    as PipelineError carrying the stage name."""
+    from .dosimetry import build_exposure_report
+    from .errors import SpfdError
+    from .field_source import field_ops
+    from .formats import write_field_dump, write_report
+    from .gauging import build_tree
+    from .linsolve import solve as _solve
+    try:
+        model, grid, samples = _load_inputs(cfg)
+    except (SpfdError, ValueError, OSError) as exc:
+        raise PipelineError("load", str(exc)) from exc
+    timing = PipelineTiming()
+    ops = field_ops(grid, cfg.solve)
+    with _Stage(timing, "interpolate"):
+        flux = ops.interpolate(samples.lattice, samples.b)
+        if cfg.clean_fluxes:
+            flux = ops.clean(flux, cfg.clean_tol)
+    with _Stage(timing, "gauge"):
+        build_tree(grid, cfg.tree_kind)
+        a = ops.gauge(flux, cfg.gauge_tol)
+    with _Stage(timing, "assemble"):
+        state = _state if _state is not None else PipelineState(model, cfg.frequency_hz, cfg.solve)
+        rhs = state.op.rhs(a)
+    with _Stage(timing, "solve"):
+        h = _hierarchy if _hierarchy is not None else state.hierarchy
+        psi, rep = _solve(None, rhs, h, cfg.solve)
+        if not rep.converged:
+            raise PipelineError("solve", f"solver did not converge: residual {rep.rel_residual:.3e} "
+                                         f"after {rep.iterations} iterations")
+    with _Stage(timing, "efield"):
+        omega = 2.0 * math.pi * cfg.frequency_hz
+        vox = state.op.efield_voxavg(a, psi, omega)[0]
+    with _Stage(timing, "report"):
+        report = build_exposure_report(vox, state.vox_index, model, cfg.frequency_hz, dof_count=state.op.n_dofs,
+                                       solver=rep, rms=cfg.report_rms, rel_tol=cfg.solve.rel_tol)
+        if cfg.out_report:
+            write_report(report, cfg.out_report)
+        if cfg.out_field:
+            write_field_dump(model, report.voxel_field, report.voxel_indices, cfg.out_field)
+    timing.total = sum(timing.as_dict().values())
+    timing.budget_met = timing.total <= cfg.latency_budget_s
+    return report, timing
+
+
+@dataclass(frozen=True)
+class StepStats:
+    mean: float
+    stddev: float
+    min: float
+    max: float
+
+
+def summarize_runs(samples: dict) -> dict:
+    """Per-step mean / sample stddev (n-1) / min / max (pipeline.py:209-222)."""
+    out = {}
+    for step, values in samples.items():
+        arr = np.asarray(values, dtype=np.float64)
+        if arr.size < 2:
+            raise ValueError(f"step '{step}' needs at least 2 runs, got {arr.size}")
+        out[step] = StepStats(float(arr.mean()), float(arr.std(ddof=1)), float(arr.min()), float(arr.max()))
+    return out
+
+
+@dataclass
+class BenchmarkResult:
+    steps: dict
+    runs: int
+    setup_seconds: float
+    iterations: list
+    report: object = None
+
+    def to_csv(self) -> str:
+        rows = ["step,mean_s,stddev_s,min_s,max_s"]
+        for name in (*STEP_NAMES, "total"):
+            s = self.steps[name]
+            rows.append(f"{name},{s.mean:.9f},{s.stddev:.9f},{s.min:.9f},{s.max:.9f}")
+        return "\n".join(rows) + "\n"
+
+    def to_text(self) -> str:
+        w = max(len(n) for n in (*STEP_NAMES, "total"))
+        rows = [f"{'step':<{w}}  {'mean [s]':>12}  {'stddev [s]':>12}  {'min [s]':>12}  {'max [s]':>12}"]
+        for name in (*STEP_NAMES, "total"):
+            s = self.steps[name]
+            rows.append(f"{name:<{w}}  {s.mean:>12.6f}  {s.stddev:>12.6f}  {s.min:>12.6f}  {s.max:>12.6f}")
+        rows.append(f"amg setup (once): {self.setup_seconds:.6f} s")
+        rows.append(f"solver iterations per run: {self.iterations}")
+        return "\n".join(rows)
+
+
+def run_benchmark(cfg: PipelineConfig, runs: int = 5, timings_override: dict | None = None):
+    """Repeat the timed stages `runs` times on identical inputs with the
+    operator and hierarchy built once up front (pipeline.py:256-306)."""
+    if runs < 2:
+        raise ValueError("need at least 2 runs for a sample standard deviation")
+    if timings_override is not None:
+        samples = dict(timings_override)
+        if "total" not in samples:
+            n = len(next(iter(samples.values())))
+            samples["total"] = [sum(samples[s][i] for s in samples if s != "total") for i in range(n)]
+        return BenchmarkResult(summarize_runs(samples), runs, 0.0, [])
+    bench_cfg = replace(cfg, out_report=None, out_field=None)
+    model, _, _ = _load_inputs(bench_cfg)
+    in_memory = replace(bench_cfg, model=model, phantom_path=None)
+    t0 = time.perf_counter()
+    state = PipelineState(model, cfg.frequency_hz, cfg.solve)
+    torch.cuda.synchronize()
+    setup_seconds = time.perf_counter() - t0
+    run_pipeline(in_memory, _state=state)          # warm-up (cleaning hierarchy, caches)
+    samples: dict = {name: [] for name in (*STEP_NAMES, "total")}
+    iterations = []
+    report = None
+    for _ in range(runs):
+        report, timing = run_pipeline(in_memory, _state=state)
+        for name in STEP_NAMES:
+            samples[name].append(getattr(timing, name))
+        samples["total"].append(timing.total)
+        iterations.append(report.solver.iterations)
+    return BenchmarkResult(summarize_runs(samples), runs, setup_seconds, iterations, report)

@@ -264,6 +264,46 @@ def field_case(name):
     print(name, "faces", grid.n_faces, "normal levels", h.level_sizes)
 
 
+def pipeline_case(name):
+    """The reference's run_pipeline end to end (coil source sampled on a
+    5x5x5 lattice, cleaning, comb gauge, solve, E-field, report) plus the
+    byte images of its file formats."""
+    import tempfile
+    from spfd import pipeline as rp
+    m = two_blobs()
+    coil = rf.CoilSpec(center=(0.014, 0.011, -0.01), axis=(0.3, -0.2, 1.0), radius_m=0.02, current_a=20.0, segments=48)
+    cfg = rp.PipelineConfig(model=m, coil=coil, frequency_hz=FREQ, coil_lattice_dims=(5, 5, 5), report_rms=True)
+    rep, _ = rp.run_pipeline(cfg)
+    d = {"coil_center": np.array(coil.center), "coil_axis": np.array((0.3, -0.2, 1.0)),
+         "coil_radius": np.array(coil.radius_m), "coil_current": np.array(coil.current_a),
+         "coil_segments": np.array(coil.segments), "vox": rep.voxel_field, "vox_idx": rep.voxel_indices,
+         "p99": np.array(rep.percentile99_vpm), "max": np.array(rep.max_vpm), "dofs": np.array(rep.dof_count),
+         "iters": np.array(rep.solver.iterations)}
+    tids = sorted(rep.per_tissue)
+    d["tids"] = np.array(tids, np.int64)
+    d["t_count"] = np.array([rep.per_tissue[t].count for t in tids], np.int64)
+    d["t_mean"] = np.array([rep.per_tissue[t].mean for t in tids])
+    d["t_max"] = np.array([rep.per_tissue[t].max for t in tids])
+    d["t_p99"] = np.array([rep.per_tissue[t].p99 for t in tids])
+    uni = rp.PipelineConfig(model=m, uniform_b=(0.0, 0.0, 1e-6), frequency_hz=FREQ)
+    urep, _ = rp.run_pipeline(uni)
+    d["u_vox"] = urep.voxel_field
+    d["u_p99"] = np.array(urep.percentile99_vpm)
+    # file formats: phantom, samples, report and field dump bytes
+    with tempfile.TemporaryDirectory() as tmp:
+        rv.save_model(m, os.path.join(tmp, "m.phantom"))
+        samples = rf.sample_on_lattice(coil, rf.Lattice.covering(ro.StaggeredGrid.from_model(m), (3, 3, 2)), FREQ)
+        rf.save_samples(samples, os.path.join(tmp, "s.txt"))
+        rd.write_report(rep, os.path.join(tmp, "r.txt"))
+        rd.write_field_dump(m, rep.voxel_field, rep.voxel_indices, os.path.join(tmp, "f.dump"))
+        for key, fn in (("phantom_bytes", "m.phantom"), ("samples_bytes", "s.txt"), ("report_bytes", "r.txt"),
+                        ("dump_bytes", "f.dump")):
+            with open(os.path.join(tmp, fn), "rb") as fh:
+                d[key] = np.frombuffer(fh.read(), np.uint8)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(name, "dofs", rep.dof_count, "iters", rep.solver.iterations, "p99", rep.percentile99_vpm)
+
+
 def main():
     rng = np.random.default_rng(20240817)
     m = block((6, 6, 6))
@@ -290,10 +330,12 @@ def main():
     matrix_case("laplacian12", laplacian_3d(12))
 
     field_case("field_coil")
+    pipeline_case("field_pipeline")
 
 
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "field":
         field_case("field_coil")
+        pipeline_case("field_pipeline")
     else:
         main()
