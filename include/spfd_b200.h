@@ -350,6 +350,16 @@ int spfd_exposure_stats(const double *values, int64_t n, double scale, const int
  * h_ms: ms per launch; h_bytes: algorithmic bytes per launch (0 for 3). */
 int spfd_bench_kernel(spfd_amg_t amg, int which, int reps, int nrhs, double *h_ms, double *h_bytes,
                       void *stream);
+/* Tuning knob (not part of the reference API): select the fine-level
+ * stencil kernel used by every later solve / V-cycle in this process.
+ * kind = -1 default (environment SPFD_SPAN_KERNEL, else the z-march
+ * kernel), 2 flat per-position kernel, 4 z-march register-pipeline kernel.
+ * Both give bit-identical results; this exists for A/B parity tests. */
+int spfd_set_fine_kernel(int kind);
+/* Tuning knob: run PCG as one CUDA graph with a device-side WHILE node
+ * (mode 1, the default) or as the host-driven loop (mode 0); -1 restores the
+ * default / environment (SPFD_PCG_GRAPH).  Same arithmetic, same bits. */
+int spfd_set_pcg_graph(int mode);
 /* Number of kernels this library has launched so far (process-wide). */
 int64_t spfd_launch_count(void);
 /* Synchronous copy between any host/device pointers (host transports). */

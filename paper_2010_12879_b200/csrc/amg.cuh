@@ -66,6 +66,13 @@ struct Amg {
     Dist *dist = nullptr;     // set by amg_distribute (owned)
     cudaStream_t side = nullptr;            // PCG x-update overlap stream
     cudaEvent_t ev_alpha = nullptr, ev_x = nullptr;
+    // PCG as one CUDA graph per rhs count: a device-side WHILE node over the
+    // iteration body (convergence tested on the device, no host round trip)
+    cudaStream_t cap = nullptr;             // private capture stream
+    cudaGraphExec_t pcg_exec[3] = {nullptr, nullptr, nullptr};
+    int64_t pcg_body_launches[3] = {0, 0, 0};
+    DevBuf<double> pcg_trace;               // [cap_iters * 2] per-iteration residual estimates
+    int64_t pcg_trace_cap = 0;
     Amg() = default;
     Amg(const Amg &) = delete;
     Amg &operator=(const Amg &) = delete;

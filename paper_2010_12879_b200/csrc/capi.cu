@@ -24,6 +24,8 @@ struct spfd_field_s {
 
 namespace spfd {
 
+extern int g_fine_kind_override;
+extern int g_pcg_graph_override;
 static thread_local std::string g_last_error;
 static std::atomic<int64_t> g_launches{0};
 int64_t launch_count() { return g_launches.load(); }
@@ -326,6 +328,20 @@ int spfd_bench_kernel(spfd_amg_t h, int which, int reps, int nrhs, double *h_ms,
     return guarded([&] {
         SPFD_CHECK(h && h_ms && h_bytes && which >= 0 && which <= 3, SPFD_EINVAL, "bad argument");
         *h_ms = amg_bench_kernel(*h->amg, which, reps, nrhs, h_bytes, S(stream));
+    });
+}
+
+int spfd_set_fine_kernel(int kind) {
+    return guarded([&] {
+        SPFD_CHECK(kind == -1 || kind == 2 || kind == 4 || kind == 5, SPFD_EINVAL, "fine kernel kind must be -1, 2, 4 or 5");
+        g_fine_kind_override = kind;
+    });
+}
+
+int spfd_set_pcg_graph(int mode) {
+    return guarded([&] {
+        SPFD_CHECK(mode >= -1 && mode <= 1, SPFD_EINVAL, "pcg graph mode must be -1, 0 or 1");
+        g_pcg_graph_override = mode;
     });
 }
 

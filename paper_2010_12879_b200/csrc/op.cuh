@@ -41,6 +41,9 @@ struct Operator {
     DevBuf<int32_t> vrow_off;        // [ny*nz+1] conductive-voxel offsets per voxel row
     DevBuf<int32_t> nnz_row;         // [N+1] CSR row pointer cache (int32 counts, built lazily)
     DevBuf<double> ws_a, ws_b;       // span workspaces [L*2]
+    // z-march work items {j, i0, k0, k1} (built lazily by the solver)
+    mutable DevBuf<int4> zm_items;
+    mutable int64_t n_zm_items = -1;
 
     int64_t device_bytes() const {
         return rows.bytes() + tile_row.bytes() + items.bytes() + wx.bytes() + wy.bytes() + wz.bytes() +

@@ -24,7 +24,10 @@ constexpr int kDotThreads = 256;
 // device scalar slots (per rhs k)
 enum {
     S_RHO = 0, S_PQ = 2, S_RR = 4, S_ALPHA = 6, S_BETA = 8, S_BB = 10, S_RZ = 12, S_ACTIVE = 14,
-    S_TMP = 16, S_LOC = 20, S_H = 32  // S_LOC: per-rank partial scalars; FGMRES Hessenberg column from S_H
+    S_TMP = 16, S_LOC = 20, S_H = 32,  // S_LOC: per-rank partial scalars; FGMRES Hessenberg column from S_H
+    S_G = S_H + 256,                    // graph PCG: tol, max_iters, iteration, init flag, status
+    S_G_TOL = S_G, S_G_MAXIT = S_G + 1, S_G_IT = S_G + 2, S_G_INIT = S_G + 3, S_G_STATUS = S_G + 4,
+    S_END = S_G + 8
 };
 
 __device__ __forceinline__ bool mbit(const uint32_t *m, int64_t p) { return (m[p >> 5] >> (p & 31)) & 1u; }
@@ -229,6 +232,92 @@ __device__ __forceinline__ double2 shfl_dn1<double2>(double2 v) {
     return make_double2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
 }
 
+#include "zmarch.cuh"
+
+// Flat per-position kernel with the -x/+x neighbours (input and weight) taken
+// from the adjacent lanes: a warp holds 32 consecutive span positions, so
+// p-1 / p+1 of the same row sit in lane-1 / lane+1 and only the first/last
+// lane of a run gathers them.  Same arithmetic and order as k_span.
+template <int R, int MODE, bool DOT, bool RANGED = false>
+__global__ void __launch_bounds__(kSpanThreads, 5) k_spx(SpanView v, SpanArgs a) {
+    using W = V<R>;
+    using T = typename W::T;
+    constexpr unsigned FULL = 0xffffffffu;
+    __shared__ double red[32 * R];
+    const int lane = threadIdx.x & 31;
+    const int t = RANGED ? a.tile0 + blockIdx.x : blockIdx.x;
+    const int64_t pend = RANGED ? (a.pe < v.L ? a.pe : v.L) : v.L;
+    const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
+    double dot[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) dot[c] = 0.0;
+    int row = r0;
+    for (int u = 0; u < kTile / kSpanThreads; ++u) {
+        const int p = t * kTile + u * kSpanThreads + threadIdx.x;
+        if (__all_sync(FULL, p >= pend)) break;  // warp-uniform
+        const bool act = p < pend && !(RANGED && p < a.pb);
+        int pxm = -1, pxp = -1, pym = -1, pyp = -1, pzm = -1, pzp = -1;
+        double wxp = 0.0, wyp = 0.0, wzp = 0.0;
+        T xc = W::zero();
+        if (act) {
+            row = frow(v.rows, row, r1, p);
+            const int4 q = v.rows[row];
+            const int i = q.y + (p - q.x), j = q.w;
+            pxm = (i > q.y) ? p - 1 : -1;
+            pxp = (i + 1 < q.z) ? p + 1 : -1;
+            pym = (j > 0) ? spos(v.rows, row - 1, i) : -1;
+            pyp = (j + 1 < v.NY) ? spos(v.rows, row + 1, i) : -1;
+            pzm = (row >= v.NY) ? spos(v.rows, row - v.NY, i) : -1;
+            pzp = (row + v.NY < v.n_rows) ? spos(v.rows, row + v.NY, i) : -1;
+            wxp = v.wx[p]; wyp = v.wy[p]; wzp = v.wz[p];
+            xc = xin<R, MODE>(a, p);
+        }
+        const bool left = __shfl_up_sync(FULL, act, 1) && lane > 0;    // lane-1 holds p-1
+        const bool right = __shfl_down_sync(FULL, act, 1) && lane < 31; // lane+1 holds p+1
+        const T xl = shfl_up1(xc), xr = shfl_dn1(xc);
+        const double wl = __shfl_up_sync(FULL, wxp, 1);
+        if (!act) continue;
+        const double wxm = pxm >= 0 ? (left ? wl : v.wx[pxm]) : 0.0;
+        const double wym = pym >= 0 ? v.wy[pym] : 0.0;
+        const double wzm = pzm >= 0 ? v.wz[pzm] : 0.0;
+        // reference diagonal order: tail edges x, y, z then head edges x, y, z
+        const double diag = add_rn(add_rn(add_rn(add_rn(add_rn(wxp, wyp), wzp), wxm), wym), wzm);
+        T s = W::zero();
+        if (pzm >= 0) s = W::axpy(-wzm, xin<R, MODE>(a, pzm), s);
+        if (pym >= 0) s = W::axpy(-wym, xin<R, MODE>(a, pym), s);
+        if (pxm >= 0) s = W::axpy(-wxm, left ? xl : xin<R, MODE>(a, pxm), s);
+        s = W::axpy(diag, xc, s);
+        if (pxp >= 0) s = W::axpy(-wxp, right ? xr : xin<R, MODE>(a, pxp), s);
+        if (pyp >= 0) s = W::axpy(-wyp, xin<R, MODE>(a, pyp), s);
+        if (pzp >= 0) s = W::axpy(-wzp, xin<R, MODE>(a, pzp), s);
+        T out;
+        if (MODE == 0) out = s;
+        else if (MODE == 1) out = W::sub(W::ld(a.r, p), s);
+        else if (MODE == 2) out = W::sub(W::ld(a.r, p), s);
+        else if (MODE == 3) out = W::add(xc, W::scale(a.od[p], W::sub(W::ld(a.r, p), s)));
+        else {
+            const T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
+            out = W::sub(W::add(b, xc), W::scale(a.od[p], s));
+        }
+        if (!mbit(v.mask, p)) out = W::zero();
+        W::st(a.y, p, out);
+        if (DOT) {
+#pragma unroll
+            for (int c = 0; c < R; ++c) {
+                if (MODE == 0) dot[c] += W::dot(xc, out, c);
+                else if (MODE == 3) dot[c] += W::dot(W::ld(a.r, p), out, c);
+                else dot[c] += W::dot(out, out, c);
+            }
+        }
+    }
+    if (DOT) {
+        block_sum<R>(dot, red);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int c = 0; c < R; ++c) a.partials[blockIdx.x * R + c] = dot[c];
+    }
+}
+
 // Row-chunk kernel: each warp takes work items of 32 consecutive positions
 // of ONE row, so the row record and the four neighbour-row records are
 // warp-uniform (broadcast) loads, every neighbour access is a contiguous
@@ -328,7 +417,19 @@ __global__ void k_agg_sum(const int64_t *mptr, const int32_t *mpos, int64_t n_ag
     using W = V<R>;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_agg; g += (int64_t)gridDim.x * blockDim.x) {
         typename W::T s = W::zero();
-        for (int64_t q = mptr[g]; q < mptr[g + 1]; ++q) s = W::add(s, W::ld(u, mpos[q]));
+        const int64_t q1 = mptr[g + 1];
+        // 4 members in flight; the sum keeps the ascending member order
+        for (int64_t q = mptr[g]; q < q1; q += 4) {
+            int pp[4];
+            typename W::T uv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) pp[k] = q + k < q1 ? mpos[q + k] : -1;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) uv[k] = pp[k] >= 0 ? W::ld(u, pp[k]) : W::zero();
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (pp[k] >= 0) s = W::add(s, uv[k]);
+        }
         W::st(rc, g, s);
         if (x0_c) W::st(x0_c, g, W::scale(od_c[g], s));
     }
@@ -359,12 +460,28 @@ __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__r
         const bool valid = row < m.rows;
         T acc = W::zero();
         if (valid) {
+            // 4 entries per lane in flight (all loads issued before the FMAs,
+            // which keep the sequential per-lane order)
+            constexpr int U = 4;
             const int64_t q1 = m.ptr[row + 1];
-            for (int64_t q = m.ptr[row] + lane; q < q1; q += G) {
-                const int col = m.col[q];
-                const double a = m.val[q];
-                const T xv = MODE == 2 ? W::scale(od[col], W::ld(r, col)) : W::ld(x, col);
-                acc = W::fma_(a, xv, acc);
+            for (int64_t q = m.ptr[row] + lane; q < q1; q += U * G) {
+                int col[U];
+                double a[U];
+                T xv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool in = q + u * G < q1;
+                    col[u] = in ? m.col[q + u * G] : -1;
+                    a[u] = in ? m.val[q + u * G] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (col[u] >= 0) xv[u] = MODE == 2 ? W::scale(od[col[u]], W::ld(r, col[u])) : W::ld(x, col[u]);
+                    else xv[u] = W::zero();
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (col[u] >= 0) acc = W::fma_(a[u], xv[u], acc);
             }
         }
         double ac[R];
@@ -572,7 +689,7 @@ __global__ void k_xpby(int64_t n, const double *scal, const double *z, double *p
 }
 
 // Sum per-CTA partials in index order; then apply `what`.
-enum { F_STORE = 0, F_ALPHA = 1, F_BETA_INIT = 2, F_BETA = 3 };
+enum { F_STORE = 0, F_ALPHA = 1, F_BETA_INIT = 2, F_BETA = 3, F_BETA_AUTO = 4 };
 template <int R>
 __global__ void k_finalize(const double *partials, int nblocks, double *scal, int slot, int what, double tol) {
     __shared__ double red[32 * R];
@@ -587,6 +704,10 @@ __global__ void k_finalize(const double *partials, int nblocks, double *scal, in
         for (int c = 0; c < R; ++c) s[c] += partials[b * R + c];
     block_sum<R>(s, red);
     if (threadIdx.x == 0) {
+        if (what == F_BETA_AUTO) {  // graph PCG: the first iteration after a (re)start initialises rho
+            what = scal[S_G_INIT] != 0.0 ? F_BETA_INIT : F_BETA;
+            scal[S_G_INIT] = 0.0;
+        }
 #pragma unroll
         for (int c = 0; c < R; ++c) {
             scal[slot + c] = s[c];
@@ -605,6 +726,30 @@ __global__ void k_finalize(const double *partials, int nblocks, double *scal, in
         }
         (void)tol;
     }
+}
+
+// Graph PCG convergence test (the host loop's test, on the device): counts
+// the iteration, records the residual estimates, updates the per-rhs active
+// flags and ends the WHILE node on convergence, non-finite residual or the
+// iteration cap.
+__global__ void k_check(double *scal, int R, double *trace, cudaGraphConditionalHandle hnd) {
+    const int it = (int)scal[S_G_IT] + 1;
+    scal[S_G_IT] = it;
+    const double tol = scal[S_G_TOL];
+    const int maxit = (int)scal[S_G_MAXIT];
+    bool done = true, bad = false;
+    for (int c = 0; c < R; ++c) {
+        const double bb = scal[S_BB + c], rr = scal[S_RR + c];
+        const double bn = sqrt(bb);
+        const double est = bn > 0 ? sqrt(rr) / bn : 0.0;
+        if (!isfinite(est)) bad = true;
+        if (it <= maxit) trace[(int64_t)(it - 1) * R + c] = est;
+        if (est > tol) done = false;
+        const bool conv = bb == 0.0 || sqrt(rr) <= tol * bn;
+        scal[S_ACTIVE + c] = conv ? 0.0 : 1.0;
+    }
+    if (bad) scal[S_G_STATUS] = 1.0;
+    if (done || bad || it >= maxit) cudaGraphSetConditional(hnd, 0);
 }
 
 __global__ void k_set_active(double *scal, int R, double tol) {
@@ -653,7 +798,7 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
     if (h.structured) np = std::max<int64_t>(np, h.op->n_tiles);
     np = std::max<int64_t>(np, 148 * 16);
     h.partials.alloc(np * 2 + 64);
-    h.scal.alloc(S_H + 256);
+    h.scal.alloc(S_END);
     SPFD_CUDA(cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking));
     SPFD_CUDA(cudaEventCreateWithFlags(&h.ev_alpha, cudaEventDisableTiming));
     SPFD_CUDA(cudaEventCreateWithFlags(&h.ev_x, cudaEventDisableTiming));
@@ -665,9 +810,17 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
 
 namespace {
 
-// 0 = row-chunk items, 1 = 2.5-D plane, 2 = flat per-position (default: the
-// highest occupancy and the best measured HBM throughput)
+}  // namespace
+
+// fine-kernel override from the C-ABI tuning knob (-1 = environment/default)
+int g_fine_kind_override = -1;
+
+namespace {
+
+// 0 = row-chunk items, 1 = 2.5-D plane, 2 = flat per-position, 3 = tile,
+// 4 = z-march (register pipeline along z)
 int fine_kernel_kind() {
+    if (g_fine_kind_override >= 0) return g_fine_kind_override;
     static int v = -1;
     if (v < 0) {
         // the 2.5-D plane kernel is experimental (latency-bound at 1-2
@@ -677,6 +830,8 @@ int fine_kernel_kind() {
         if (e && std::string(e) == "plane") v = 1;
         if (e && std::string(e) == "items") v = 0;
         if (e && std::string(e) == "tile") v = 3;
+        if (e && std::string(e) == "zm") v = 4;
+        if (e && std::string(e) == "spx") v = 5;
     }
     return v;
 }
@@ -688,6 +843,52 @@ PlaneGeo plane_geometry(const Operator &op) {
     if (cps > 8) cps = 8;
     if (cps < 1) cps = 1;
     return plane_geo(op, cps);
+}
+
+// Work items of the z-march kernel: for every chunk of kc planes and every
+// node row j, the union [ilo, ihi) of the row's spans over the chunk is cut
+// into 32-wide segments; items are ordered (chunk, segment, j) so that a
+// CTA's warps stream adjacent rows of the same planes (their -y/+y gathers
+// hit L1).  Returns false (flat kernel) when the grid would exceed the dot
+// partials buffer.
+bool zm_build(const Operator &op) {
+    if (op.n_zm_items >= 0) return op.n_zm_items > 0;
+    op.n_zm_items = 0;
+    const int NY = (int)op.NY, NZ = (int)op.NZ;
+    if (op.n_rows <= 0 || NY <= 0 || NZ <= 0) return false;
+    std::vector<int4> rows((size_t)op.n_rows);
+    SPFD_CUDA(cudaMemcpy(rows.data(), op.rows.get(), rows.size() * sizeof(int4), cudaMemcpyDeviceToHost));
+    int64_t s1 = 0;
+    for (const int4 &q : rows) s1 += (q.z - q.y + 31) / 32;
+    int kc = (int)std::min<int64_t>(16, std::max<int64_t>(4, s1 / (148 * 8 * 8)));
+    if (const char *e = getenv("SPFD_ZM_KC")) kc = std::max(1, atoi(e));
+    std::vector<int4> items;
+    std::vector<int> ilo(NY), nseg(NY);
+    for (int k0 = 0; k0 < NZ; k0 += kc) {
+        const int k1 = std::min(NZ, k0 + kc);
+        int smax = 0;
+        const int nb = (NY + kZmRows - 1) / kZmRows;
+        for (int b = 0; b < nb; ++b) {
+            int lo = INT32_MAX, hi = INT32_MIN;
+            for (int j = b * kZmRows; j < std::min(NY, (b + 1) * kZmRows); ++j)
+                for (int k = k0; k < k1; ++k) {
+                    const int4 q = rows[(size_t)k * NY + j];
+                    if (q.y < q.z) { lo = std::min(lo, q.y); hi = std::max(hi, q.z); }
+                }
+            ilo[b] = lo;
+            nseg[b] = lo < hi ? (hi - lo + 31) / 32 : 0;
+            smax = std::max(smax, nseg[b]);
+        }
+        for (int sg = 0; sg < smax; ++sg)
+            for (int b = 0; b < nb; ++b)
+                if (sg < nseg[b]) items.push_back(make_int4(b * kZmRows, ilo[b] + 32 * sg, k0, k1));
+    }
+    const int64_t grid = (int64_t)items.size();
+    if (items.empty() || grid > std::max<int64_t>(op.n_tiles, 148 * 16)) return false;
+    op.zm_items.alloc(items.size());
+    SPFD_CUDA(cudaMemcpy(op.zm_items.get(), items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    op.n_zm_items = (int64_t)items.size();
+    return true;
 }
 
 // Launch one fine-level stencil pass (flat span kernel; the 2.5-D plane
@@ -719,6 +920,18 @@ int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
         SPFD_LAUNCH_CHECK();
         return grid;
     }
+    if (kind == 4 && a.pb == 0 && a.pe >= op.L && zm_build(op)) {
+        const int g = (int)op.n_zm_items;
+        constexpr size_t smem = zm_smem<R, MODE>();
+        static bool attr = false;
+        if (!attr) {
+            SPFD_CUDA(cudaFuncSetAttribute(k_zm<R, MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        k_zm<R, MODE, DOT><<<g, kZmThreads, smem, s>>>(v, op.zm_items.get(), a);
+        SPFD_LAUNCH_CHECK();
+        return g;
+    }
     if (kind == 0) {
         int g = grid_for(op.n_items * 32, 256, 148 * 16);
         k_items<R, MODE, DOT><<<g, 256, 0, s>>>(v, a);
@@ -732,6 +945,12 @@ int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
         b.tile0 = t0;
         int g = t1 - t0;
         if (g > 0) k_span<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, b);
+        SPFD_LAUNCH_CHECK();
+        return g;
+    }
+    if (kind == 5) {
+        int g = (int)op.n_tiles;
+        if (g > 0) k_spx<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
         SPFD_LAUNCH_CHECK();
         return g;
     }
@@ -1094,6 +1313,178 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
     return rep;
 }
 
+// ---- PCG as one CUDA graph ------------------------------------------------
+// The iteration is rotated so the convergence test ends the body:
+//   x += alpha p (side branch, previous alpha)  |  z = M r, beta (rho on the
+//   first pass after a (re)start)  ->  p = z + beta p  ->  q = A p, alpha  ->
+//   r -= alpha q, r.r  ->  k_check (sets the WHILE condition)
+// which is the host loop's arithmetic in the same order.  The body is
+// captured once per rhs count into the WHILE node of a graph; a solve is
+// restart prologue + one graph launch (+ the last x update), and the host
+// reads the scalars once per launch instead of once per iteration.
+
+}  // namespace
+int g_pcg_graph_override = -1;  // C-ABI tuning knob (-1 = environment/default)
+namespace {
+
+bool pcg_graph_enabled() {
+    if (g_pcg_graph_override >= 0) return g_pcg_graph_override == 1;
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_PCG_GRAPH");
+        v = (e && std::string(e) == "0") ? 0 : 1;
+    }
+    return v == 1;
+}
+
+template <int R>
+void pcg_body(Amg &h, cudaGraphConditionalHandle hnd, cudaStream_t s) {
+    const int64_t n = h.lv[0].nvec;
+    double *r = h.kr.get(), *z = h.kz.get(), *p = h.kp.get(), *q = h.kq.get(), *x = h.kx.get();
+    double *sc = h.scal.get();
+    // x += alpha p with the previous iteration's alpha, overlapping the V-cycle
+    SPFD_CUDA(cudaEventRecord(h.ev_alpha, s));
+    SPFD_CUDA(cudaStreamWaitEvent(h.side, h.ev_alpha, 0));
+    k_update_x<R><<<grid_for(n, 256, 148 * 8), 256, 0, h.side>>>(n, sc, x, p);
+    SPFD_LAUNCH_CHECK();
+    SPFD_CUDA(cudaEventRecord(h.ev_x, h.side));
+    amg_vcycle(h, r, z, R, s);
+    if (h.vc_partials > 0) finalize<R>(h, h.vc_partials, S_RZ, F_BETA_AUTO, s);
+    else dot<R>(h, n, r, z, S_RZ, F_BETA_AUTO, s);
+    SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
+    k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p);
+    SPFD_LAUNCH_CHECK();
+    const int g = level0_apply<R>(h, 0, true, p, nullptr, q, s);  // q = A p, p.q
+    finalize<R>(h, g, S_PQ, F_ALPHA, s);
+    k_update_r<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, r, q, h.partials.get());
+    SPFD_LAUNCH_CHECK();
+    finalize<R>(h, kDotGrid, S_RR, F_STORE, s);
+    k_check<<<1, 1, 0, s>>>(sc, R, h.pcg_trace.get(), hnd);
+    SPFD_LAUNCH_CHECK();
+}
+
+template <int R>
+void pcg_graph_build(Amg &h, int64_t max_iters) {
+    if (!h.cap) SPFD_CUDA(cudaStreamCreateWithFlags(&h.cap, cudaStreamNonBlocking));
+    if (h.pcg_trace_cap < max_iters) {
+        for (auto &e : h.pcg_exec)
+            if (e) { cudaGraphExecDestroy(e); e = nullptr; }
+        h.pcg_trace_cap = std::max<int64_t>(max_iters, 1024);
+        h.pcg_trace.alloc(h.pcg_trace_cap * 2);
+    }
+    if (h.pcg_exec[R]) return;
+    cudaGraph_t g = nullptr;
+    SPFD_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hnd;
+    SPFD_CUDA(cudaGraphConditionalHandleCreate(&hnd, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = hnd;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    SPFD_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    const int64_t l0 = launch_count();
+    SPFD_CUDA(cudaStreamBeginCaptureToGraph(h.cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    try {
+        pcg_body<R>(h, hnd, h.cap);
+    } catch (...) {
+        cudaGraph_t dummy;
+        cudaStreamEndCapture(h.cap, &dummy);
+        cudaGraphDestroy(g);
+        throw;
+    }
+    cudaGraph_t out = nullptr;
+    SPFD_CUDA(cudaStreamEndCapture(h.cap, &out));
+    h.pcg_body_launches[R] = launch_count() - l0;
+    cudaGraphExec_t exec = nullptr;
+    SPFD_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    cudaGraphDestroy(g);
+    h.pcg_exec[R] = exec;
+}
+
+template <int R>
+spfd_report pcg_graph(Amg &h, const double *b, double *x_out, const spfd_config &cfg, double *h_trace,
+                      cudaStream_t s) {
+    spfd_report rep{};
+    const int64_t n = h.lv[0].nvec;
+    double *r = h.kr.get(), *p = h.kp.get(), *q = h.kq.get(), *x = h.kx.get();
+    double *sc = h.scal.get();
+    SPFD_CUDA(cudaMemsetAsync(x, 0, n * R * sizeof(double), s));
+    SPFD_CUDA(cudaMemsetAsync(sc, 0, S_END * sizeof(double), s));
+    dot<R>(h, n, b, b, S_BB, F_STORE, s);
+    double hs[S_END];
+    SPFD_CUDA(cudaMemcpyAsync(hs, sc, S_END * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    double bnorm[2] = {std::sqrt(hs[S_BB]), R > 1 ? std::sqrt(hs[S_BB + 1]) : 0.0};
+    for (int c = 0; c < R; ++c)
+        if (!std::isfinite(bnorm[c])) { rep.status = SPFD_ENONFINITE; return rep; }
+    bool all_zero = true;
+    for (int c = 0; c < R; ++c) all_zero = all_zero && bnorm[c] == 0.0;
+    if (all_zero) {
+        SPFD_CUDA(cudaMemsetAsync(x_out, 0, n * R * sizeof(double), s));
+        rep.converged = 1;
+        return rep;
+    }
+    pcg_graph_build<R>(h, cfg.max_iters);
+    const double tol = cfg.rel_tol;
+    int it = 0;
+    while (true) {
+        // (re)start: r = b - A x, p = 0, alpha = 0, rho initialised by the first body
+        level0_apply<R>(h, 1, false, x, b, r, s);
+        SPFD_CUDA(cudaMemsetAsync(p, 0, n * R * sizeof(double), s));
+        double init[S_END - S_G] = {tol, (double)cfg.max_iters, (double)it, 1.0, 0.0, 0.0, 0.0, 0.0};
+        const double zero2[2] = {0.0, 0.0}, ones[2] = {1.0, 1.0};
+        SPFD_CUDA(cudaMemcpyAsync(sc + S_G, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        SPFD_CUDA(cudaMemcpyAsync(sc + S_ALPHA, zero2, R * sizeof(double), cudaMemcpyHostToDevice, s));
+        SPFD_CUDA(cudaMemcpyAsync(sc + S_ACTIVE, ones, R * sizeof(double), cudaMemcpyHostToDevice, s));
+        SPFD_CUDA(cudaEventRecord(h.ev_alpha, s));          // the graph runs on the private capture
+        SPFD_CUDA(cudaStreamWaitEvent(h.cap, h.ev_alpha, 0)); // stream ordered after this prologue
+        SPFD_CUDA(cudaGraphLaunch(h.pcg_exec[R], h.cap));
+        SPFD_CUDA(cudaEventRecord(h.ev_x, h.cap));
+        SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
+        // the last iteration's x += alpha p
+        k_update_x<R><<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, sc, x, p);
+        SPFD_LAUNCH_CHECK();
+        SPFD_CUDA(cudaMemcpyAsync(hs, sc, S_END * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPFD_CUDA(cudaStreamSynchronize(s));
+        const int nit = (int)hs[S_G_IT];
+        for (int64_t k = 0; k < (int64_t)(nit - it) * h.pcg_body_launches[R]; ++k) count_launch();
+        if (h_trace && nit > it) {
+            const int hi = std::min(nit, cfg.max_iters);
+            if (hi > it)
+                SPFD_CUDA(cudaMemcpy(h_trace + (int64_t)it * R, h.pcg_trace.get() + (int64_t)it * R,
+                                     (size_t)(hi - it) * R * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        it = nit;
+        if (hs[S_G_STATUS] != 0.0) {
+            rep.status = SPFD_ENONFINITE;
+            rep.iterations = it;
+            return rep;
+        }
+        // true residual check (linsolve.py:296-298 semantics)
+        const int gt = level0_apply<R>(h, 1, true, x, b, q, s);
+        finalize<R>(h, gt, S_TMP, F_STORE, s);
+        SPFD_CUDA(cudaMemcpyAsync(hs, sc, S_H * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPFD_CUDA(cudaStreamSynchronize(s));
+        bool ok = true;
+        for (int c = 0; c < R; ++c) {
+            const double rel = bnorm[c] > 0 ? std::sqrt(hs[S_TMP + c]) / bnorm[c] : 0.0;
+            rep.rel_residual[c] = rel;
+            if (!(rel <= tol)) ok = false;
+        }
+        if (ok || it >= cfg.max_iters) {
+            rep.converged = ok ? 1 : 0;
+            break;
+        }
+        // recursive residual drifted: restart from the true residual
+    }
+    if (x_out != x) SPFD_CUDA(cudaMemcpyAsync(x_out, x, n * R * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    rep.iterations = it;
+    return rep;
+}
+
 }  // namespace
 
 #include "dist.cuh"
@@ -1113,6 +1504,9 @@ void dist_info(const Amg &h, int64_t *out) {
 
 Amg::~Amg() {
     delete dist;
+    for (auto &e : pcg_exec)
+        if (e) cudaGraphExecDestroy(e);
+    if (cap) cudaStreamDestroy(cap);
     if (side) cudaStreamDestroy(side);
     if (ev_alpha) cudaEventDestroy(ev_alpha);
     if (ev_x) cudaEventDestroy(ev_x);
@@ -1343,7 +1737,12 @@ spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spf
     } else if (h.dist) {
         rep = nrhs == 1 ? pcg_dist<1>(h, b, x, cfg, h_trace, s) : pcg_dist<2>(h, b, x, cfg, h_trace, s);
     } else {
-        rep = nrhs == 1 ? pcg<1>(h, b, x, cfg, h_trace, s) : pcg<2>(h, b, x, cfg, h_trace, s);
+        // (the z-march kernel's >48 KB dynamic shared memory inside a WHILE
+        // body crashes graph instantiation on this driver: host loop for it)
+        if (pcg_graph_enabled() && cfg.max_iters > 0 && fine_kernel_kind() != 4)
+            rep = nrhs == 1 ? pcg_graph<1>(h, b, x, cfg, h_trace, s) : pcg_graph<2>(h, b, x, cfg, h_trace, s);
+        else
+            rep = nrhs == 1 ? pcg<1>(h, b, x, cfg, h_trace, s) : pcg<2>(h, b, x, cfg, h_trace, s);
     }
     SPFD_CUDA(cudaEventRecord(e1, s));
     SPFD_CUDA(cudaEventSynchronize(e1));

@@ -1,0 +1,142 @@
+"""GPU A/B of the fine-level stencil kernels (flat per-position k_span, its
+lane-shuffle variant k_spx and the z-march plane-ring kernel k_zm).
+
+Every stencil mode must be bit-identical between the two kernels, so a
+V-cycle (pre-smooth+defect, restriction input, matrix-free prolongation,
+post-smooth: modes 1-4) gives the same bits.  A Krylov solve is compared to
+tolerance only: its dot products are reduced per CTA, and the two kernels
+cut the positions into CTAs differently (fixed order within each kernel, so
+each is bitwise reproducible on its own).  Cases: every golden phantom
+(spheres, cylinders, cavities, separate bodies), C1 and C2, with sweep
+variants."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_cases, golden_model, load_golden
+
+pytestmark = pytest.mark.gpu
+
+FLAT, ZMARCH, SPX = 2, 4, 5
+
+
+def _set_kernel(kind):
+    from paper_2010_12879_b200 import _lib
+    _lib.check(_lib.lib().spfd_set_fine_kernel(kind))
+
+
+@pytest.fixture(autouse=True)
+def _restore():
+    yield
+    _set_kernel(-1)
+
+
+def _hier(model, freq, a, cfg):
+    import paper_2010_12879_b200 as p
+    grid = p.StaggeredGrid.from_model(model)
+    system = p.assemble_poisson(model, grid, a, freq)
+    return system, p.amg_setup(system.matrix, cfg)
+
+
+@pytest.mark.parametrize("case", golden_cases("model"))
+@pytest.mark.parametrize("sweeps", [(1, 1), (2, 2), (1, 0)])
+def test_vcycle_bitwise(case, sweeps, rng):
+    import paper_2010_12879_b200 as p
+    d = load_golden(case)
+    cfg = p.SolveConfig(rel_tol=1e-10, pre_sweeps=sweeps[0], post_sweeps=sweeps[1])
+    system, h = _hier(golden_model(d), float(d["freq"]), d["a"], cfg)
+    r = rng.standard_normal((2, h.n))
+    out = []
+    for kind in (FLAT, ZMARCH, SPX):
+        _set_kernel(kind)
+        out.append(p.v_cycle(h, r))
+    assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
+
+
+@pytest.mark.parametrize("case", golden_cases("model"))
+@pytest.mark.parametrize("method", ["pcg", "fgmres"])
+def test_solve_agrees(case, method):
+    import paper_2010_12879_b200 as p
+    d = load_golden(case)
+    cfg = p.SolveConfig(rel_tol=1e-12, method=method)
+    system, h = _hier(golden_model(d), float(d["freq"]), d["a"], cfg)
+    if not np.any(system.rhs):
+        pytest.skip("zero rhs")
+    res = []
+    for kind in (FLAT, ZMARCH, SPX):
+        _set_kernel(kind)
+        x, rep = p.solve(system.matrix, system.rhs, h, cfg)
+        assert rep.converged
+        res.append((rep.iterations, x))
+    for k in (1, 2):
+        assert abs(res[0][0] - res[k][0]) <= 1
+        assert np.linalg.norm(res[0][1] - res[k][1]) <= 1e-10 * np.linalg.norm(res[0][1])
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_configs_vcycle_bitwise_and_snapshot(name, rng):
+    import paper_2010_12879_b200 as p
+    from paper_2010_12879_b200 import Session, workloads
+    w = getattr(workloads, name)()
+    cfg = p.SolveConfig(rel_tol=1e-8)
+    system, h = _hier(w.model, w.frequency_hz, w.a[0], cfg)
+    r = rng.standard_normal((2, h.n))
+    z = []
+    snaps = []
+    for kind in (FLAT, ZMARCH, SPX):
+        _set_kernel(kind)
+        z.append(p.v_cycle(h, r))
+        sess = Session(w.model, w.frequency_hz, cfg)
+        vox, rep, _ = sess.snapshot(torch.from_numpy(w.a).cuda(), keep_psi=True)
+        snaps.append((rep.iterations, vox.cpu().numpy()))
+    assert np.array_equal(z[0], z[1]) and np.array_equal(z[0], z[2])
+    for k in (1, 2):
+        assert abs(snaps[0][0] - snaps[k][0]) <= 1
+        e = np.abs(snaps[0][1] - snaps[k][1]).max() / np.abs(snaps[0][1]).max()
+        assert e <= 1e-6, e
+
+
+def _set_graph(mode):
+    from paper_2010_12879_b200 import _lib
+    _lib.check(_lib.lib().spfd_set_pcg_graph(mode))
+
+
+@pytest.mark.parametrize("case", golden_cases("model"))
+def test_pcg_graph_matches_host_loop(case):
+    """The graph-captured PCG (device-side WHILE node) runs the host loop's
+    kernels in the same order: same iteration count, same bits, same trace."""
+    import paper_2010_12879_b200 as p
+    d = load_golden(case)
+    out = []
+    try:
+        for mode in (0, 1):
+            _set_graph(mode)
+            import io
+            trace = io.StringIO()
+            cfg = p.SolveConfig(rel_tol=1e-11, method="pcg", trace=trace)
+            system, h = _hier(golden_model(d), float(d["freq"]), d["a"], cfg)
+            if not np.any(system.rhs):
+                pytest.skip("zero rhs")
+            b = np.stack([system.rhs, 0.25 * system.rhs[::-1].copy()])
+            x, rep = p.solve(system.matrix, b, h, cfg)
+            out.append((rep.iterations, x, trace.getvalue(), rep.converged))
+    finally:
+        _set_graph(-1)
+    assert out[0][0] == out[1][0] and out[0][3] and out[1][3]
+    assert np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
+
+
+def test_pcg_graph_max_iters_and_restart():
+    import paper_2010_12879_b200 as p
+    d = load_golden(golden_cases("model")[0])
+    for mode in (0, 1):
+        _set_graph(mode)
+        try:
+            cfg = p.SolveConfig(rel_tol=1e-14, max_iters=3, method="pcg")
+            system, h = _hier(golden_model(d), float(d["freq"]), d["a"], cfg)
+            x, rep = p.solve(system.matrix, system.rhs, h, cfg)
+            assert rep.iterations == 3 and not rep.converged
+        finally:
+            _set_graph(-1)
