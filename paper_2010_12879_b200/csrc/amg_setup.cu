@@ -619,7 +619,9 @@ int pick_group(int64_t nnz, int64_t rows) {
     }
     if (forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
     double avg = rows > 0 ? (double)nnz / (double)rows : 1.0;
-    int g = avg <= 12.0 ? 4 : (avg <= 48.0 ? 8 : 16);
+    // (measured on C3: the level-1 operator, ~30 nnz/row, runs fastest with
+    // 4 lanes -- fewer shuffle levels, more rows in flight per warp)
+    int g = avg <= 40.0 ? 4 : (avg <= 48.0 ? 8 : 16);
     // small coarse matrices: widen the groups until the launch fills the
     // machine (latency, not bandwidth, bounds those levels)
     while (g < 32 && rows * (int64_t)g < (int64_t)148 * 32 * 64) g *= 2;
@@ -872,6 +874,8 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
             L.r_group = pick_group(L.R.nnz, L.R.rows);
         }
         if (!(l == 0 && h->structured)) L.a_group = pick_group(L.A.nnz, L.A.rows);
+        if (const char *e = getenv("SPFD_CSR_GROUP_A1"))  // tuning: level-1 smoother lanes per row
+            if (l == 1) L.a_group = atoi(e);
         L.vr.alloc(L.nvec * R);
         L.vx.alloc(L.nvec * R);
         L.vd.alloc(L.nvec * R);
