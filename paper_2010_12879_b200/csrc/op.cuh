@@ -41,6 +41,12 @@ struct Operator {
     DevBuf<int32_t> vrow_off;        // [ny*nz+1] conductive-voxel offsets per voxel row
     DevBuf<int32_t> nnz_row;         // [N+1] CSR row pointer cache (int32 counts, built lazily)
     DevBuf<double> ws_a, ws_b;       // span workspaces [L*2]
+    // per-position neighbour code (bit0 DOF, bits1-6 -x,+x,-y,+y,-z,+z present)
+    // and per-row position deltas to the -y,+y,-z,+z neighbour rows (built
+    // lazily by the solver for the coded stencil kernel)
+    mutable DevBuf<uint8_t> ncode;
+    mutable DevBuf<int4> rdelta;
+    mutable bool coded = false;
     // z-march work items {j, i0, k0, k1} (built lazily by the solver)
     mutable DevBuf<int4> zm_items;
     mutable int64_t n_zm_items = -1;

@@ -318,6 +318,117 @@ __global__ void __launch_bounds__(kSpanThreads, 5) k_spx(SpanView v, SpanArgs a)
     }
 }
 
+// ---- coded flat kernel ---------------------------------------------------
+// Same per-position mapping and arithmetic as k_span, but the neighbour
+// structure comes from one byte per position (DOF bit + which of the six
+// neighbours exist) and one int4 per row (position deltas to the -y/+y/-z/+z
+// neighbour rows) instead of four neighbour-row records per position: the
+// index traffic through L1 drops from ~80 B to ~17 B per position.
+
+__global__ void k_build_rdelta(const int4 *rows, int64_t n_rows, int NY, int4 *rd) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int4 q = rows[r];
+        const int base = q.x - q.y;
+        auto del = [&](int64_t rn, bool ok) { return ok ? (rows[rn].x - rows[rn].y) - base : 0; };
+        rd[r] = make_int4(del(r - 1, q.w > 0), del(r + 1, q.w + 1 < NY), del(r - NY, r >= NY), del(r + NY, r + NY < n_rows));
+    }
+}
+
+__global__ void k_build_ncode(SpanView v, uint8_t *code) {
+    const int t = blockIdx.x;
+    const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
+    int row = r0;
+    for (int u = 0; u < kTile / kSpanThreads; ++u) {
+        const int p = t * kTile + u * kSpanThreads + threadIdx.x;
+        if (p >= v.L) break;
+        row = frow(v.rows, row, r1, p);
+        const int4 q = v.rows[row];
+        const int i = q.y + (p - q.x), j = q.w;
+        uint8_t c = mbit(v.mask, p) ? 1 : 0;
+        if (i > q.y) c |= 2;
+        if (i + 1 < q.z) c |= 4;
+        if (j > 0 && spos(v.rows, row - 1, i) >= 0) c |= 8;
+        if (j + 1 < v.NY && spos(v.rows, row + 1, i) >= 0) c |= 16;
+        if (row >= v.NY && spos(v.rows, row - v.NY, i) >= 0) c |= 32;
+        if (row + v.NY < v.n_rows && spos(v.rows, row + v.NY, i) >= 0) c |= 64;
+        code[p] = c;
+    }
+}
+
+template <int R, int MODE, bool DOT, bool RANGED = false>
+__global__ void __launch_bounds__(kSpanThreads, 6) k_spc(SpanView v, const uint8_t *__restrict__ code,
+                                                        const int4 *__restrict__ rd, SpanArgs a) {
+    using W = V<R>;
+    using T = typename W::T;
+    __shared__ double red[32 * R];
+    const int t = RANGED ? a.tile0 + blockIdx.x : blockIdx.x;
+    const int64_t pend = RANGED ? (a.pe < v.L ? a.pe : v.L) : v.L;
+    const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
+    double dot[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) dot[c] = 0.0;
+    int row = r0;
+    for (int u = 0; u < kTile / kSpanThreads; ++u) {
+        const int p = t * kTile + u * kSpanThreads + threadIdx.x;
+        if (p >= pend) break;
+        if (RANGED && p < a.pb) continue;
+        row = frow(v.rows, row, r1, p);
+        const unsigned c = code[p];
+        const int4 d = rd[row];
+        Nbr n;
+        n.pxm = (c & 2) ? p - 1 : -1;
+        n.pxp = (c & 4) ? p + 1 : -1;
+        n.pym = (c & 8) ? p + d.x : -1;
+        n.pyp = (c & 16) ? p + d.y : -1;
+        n.pzm = (c & 32) ? p + d.z : -1;
+        n.pzp = (c & 64) ? p + d.w : -1;
+        n.wxp = v.wx[p]; n.wyp = v.wy[p]; n.wzp = v.wz[p];
+        n.wxm = n.pxm >= 0 ? v.wx[n.pxm] : 0.0;
+        n.wym = n.pym >= 0 ? v.wy[n.pym] : 0.0;
+        n.wzm = n.pzm >= 0 ? v.wz[n.pzm] : 0.0;
+        // reference diagonal order: tail edges x, y, z then head edges x, y, z
+        n.diag = add_rn(add_rn(add_rn(add_rn(add_rn(n.wxp, n.wyp), n.wzp), n.wxm), n.wym), n.wzm);
+        T out;
+        if (MODE == 2) {
+            const double *od = a.od, *rr = a.r;
+            T s = apply_row<R>(n, p, [&](int pp) { return W::scale(od[pp], W::ld(rr, pp)); });
+            out = W::sub(W::ld(rr, p), s);
+        } else if (MODE == 4) {
+            const double *ec = a.ec;
+            const int32_t *ag = a.aggp;
+            auto eat = [&](int pp) {
+                int g1 = ag[pp];  // aggregate id + 1, 0 = none
+                return g1 > 0 ? W::ld(ec, g1 - 1) : W::zero();
+            };
+            T s = apply_row<R>(n, p, eat);
+            T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
+            out = W::sub(W::add(b, eat(p)), W::scale(a.od[p], s));
+        } else {
+            const double *xx = a.x;
+            T s = apply_row<R>(n, p, [&](int pp) { return W::ld(xx, pp); });
+            if (MODE == 0) out = s;
+            else if (MODE == 1) out = W::sub(W::ld(a.r, p), s);
+            else out = W::add(W::ld(xx, p), W::scale(a.od[p], W::sub(W::ld(a.r, p), s)));
+        }
+        if (!(c & 1)) out = W::zero();
+        W::st(a.y, p, out);
+        if (DOT) {
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) {
+                if (MODE == 0) dot[cc] += W::dot(W::ld(a.x, p), out, cc);
+                else if (MODE == 3) dot[cc] += W::dot(W::ld(a.r, p), out, cc);
+                else dot[cc] += W::dot(out, out, cc);
+            }
+        }
+    }
+    if (DOT) {
+        block_sum<R>(dot, red);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) a.partials[blockIdx.x * R + cc] = dot[cc];
+    }
+}
+
 // Row-chunk kernel: each warp takes work items of 32 consecutive positions
 // of ONE row, so the row record and the four neighbour-row records are
 // warp-uniform (broadcast) loads, every neighbour access is a contiguous
@@ -832,6 +943,8 @@ int fine_kernel_kind() {
         if (e && std::string(e) == "tile") v = 3;
         if (e && std::string(e) == "zm") v = 4;
         if (e && std::string(e) == "spx") v = 5;
+        if (e && std::string(e) == "flat") v = 2;
+        if (e && std::string(e) == "coded") v = 6;
     }
     return v;
 }
@@ -945,6 +1058,32 @@ int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
         b.tile0 = t0;
         int g = t1 - t0;
         if (g > 0) k_span<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, b);
+        SPFD_LAUNCH_CHECK();
+        return g;
+    }
+    if (kind == 6) {
+        if (!op.coded) {  // lazily: neighbour codes and row deltas (one pass each)
+            op.ncode.alloc(op.L);
+            op.rdelta.alloc(op.n_rows);
+            k_build_rdelta<<<grid_for(op.n_rows, 256), 256, 0, s>>>(op.rows.get(), op.n_rows, (int)op.NY,
+                                                                    op.rdelta.get());
+            SPFD_LAUNCH_CHECK();
+            if (op.n_tiles > 0) k_build_ncode<<<(int)op.n_tiles, kSpanThreads, 0, s>>>(v, op.ncode.get());
+            SPFD_LAUNCH_CHECK();
+            op.coded = true;
+        }
+        if (a.pb > 0 || a.pe < op.L) {
+            const int64_t pe = a.pe < op.L ? a.pe : op.L;
+            const int t0 = (int)(a.pb / kTile), t1 = (int)((pe + kTile - 1) / kTile);
+            SpanArgs b = a;
+            b.tile0 = t0;
+            const int g = t1 - t0;
+            if (g > 0) k_spc<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, op.ncode.get(), op.rdelta.get(), b);
+            SPFD_LAUNCH_CHECK();
+            return g;
+        }
+        const int g = (int)op.n_tiles;
+        if (g > 0) k_spc<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, op.ncode.get(), op.rdelta.get(), a);
         SPFD_LAUNCH_CHECK();
         return g;
     }
@@ -1363,8 +1502,10 @@ void pcg_body(Amg &h, cudaGraphConditionalHandle hnd, cudaStream_t s) {
     SPFD_LAUNCH_CHECK();
 }
 
+// Returns false (host-loop PCG) when the body cannot be captured; the reason
+// goes to stderr with SPFD_DEBUG=1.
 template <int R>
-void pcg_graph_build(Amg &h, int64_t max_iters) {
+bool pcg_graph_build(Amg &h, int64_t max_iters) {
     if (!h.cap) SPFD_CUDA(cudaStreamCreateWithFlags(&h.cap, cudaStreamNonBlocking));
     if (h.pcg_trace_cap < max_iters) {
         for (auto &e : h.pcg_exec)
@@ -1372,7 +1513,8 @@ void pcg_graph_build(Amg &h, int64_t max_iters) {
         h.pcg_trace_cap = std::max<int64_t>(max_iters, 1024);
         h.pcg_trace.alloc(h.pcg_trace_cap * 2);
     }
-    if (h.pcg_exec[R]) return;
+    if (h.pcg_exec[R]) return true;
+    if (h.pcg_body_launches[R] < 0) return false;  // capture failed before: stay on the host loop
     cudaGraph_t g = nullptr;
     SPFD_CUDA(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle hnd;
@@ -1386,22 +1528,33 @@ void pcg_graph_build(Amg &h, int64_t max_iters) {
     SPFD_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
     cudaGraph_t body = np.conditional.phGraph_out[0];
     const int64_t l0 = launch_count();
-    SPFD_CUDA(cudaStreamBeginCaptureToGraph(h.cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    // relaxed: lazily loaded kernels may be loaded during the capture
+    SPFD_CUDA(cudaStreamBeginCaptureToGraph(h.cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    std::string why;
     try {
         pcg_body<R>(h, hnd, h.cap);
-    } catch (...) {
-        cudaGraph_t dummy;
-        cudaStreamEndCapture(h.cap, &dummy);
-        cudaGraphDestroy(g);
-        throw;
+    } catch (const std::exception &e) {
+        why = e.what();
     }
     cudaGraph_t out = nullptr;
-    SPFD_CUDA(cudaStreamEndCapture(h.cap, &out));
-    h.pcg_body_launches[R] = launch_count() - l0;
+    cudaError_t ec = cudaStreamEndCapture(h.cap, &out);
     cudaGraphExec_t exec = nullptr;
-    SPFD_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    if (why.empty() && ec == cudaSuccess) {
+        ec = cudaGraphInstantiate(&exec, g, 0);
+        if (ec != cudaSuccess) why = std::string("instantiate: ") + cudaGetErrorString(ec);
+    } else if (why.empty()) {
+        why = std::string("end capture: ") + cudaGetErrorString(ec);
+    }
+    cudaGetLastError();  // clear a sticky capture error
+    if (!why.empty()) {
+        if (getenv("SPFD_DEBUG")) fprintf(stderr, "[spfd] PCG graph capture failed (%s): host loop\n", why.c_str());
+        h.pcg_body_launches[R] = -1;
+        return false;  // (the graph is leaked rather than destroyed half-built)
+    }
+    h.pcg_body_launches[R] = launch_count() - l0;
     cudaGraphDestroy(g);
     h.pcg_exec[R] = exec;
+    return true;
 }
 
 template <int R>
@@ -1427,12 +1580,14 @@ spfd_report pcg_graph(Amg &h, const double *b, double *x_out, const spfd_config 
         rep.converged = 1;
         return rep;
     }
-    pcg_graph_build<R>(h, cfg.max_iters);
     const double tol = cfg.rel_tol;
     int it = 0;
     while (true) {
         // (re)start: r = b - A x, p = 0, alpha = 0, rho initialised by the first body
         level0_apply<R>(h, 1, false, x, b, r, s);
+        // capture after the first fine-level launch: lazily built kernel data
+        // (neighbour codes, z-march items) must not be built inside the graph
+        if (!pcg_graph_build<R>(h, cfg.max_iters)) return pcg<R>(h, b, x_out, cfg, h_trace, s);
         SPFD_CUDA(cudaMemsetAsync(p, 0, n * R * sizeof(double), s));
         double init[S_END - S_G] = {tol, (double)cfg.max_iters, (double)it, 1.0, 0.0, 0.0, 0.0, 0.0};
         const double zero2[2] = {0.0, 0.0}, ones[2] = {1.0, 1.0};
@@ -1737,9 +1892,7 @@ spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spf
     } else if (h.dist) {
         rep = nrhs == 1 ? pcg_dist<1>(h, b, x, cfg, h_trace, s) : pcg_dist<2>(h, b, x, cfg, h_trace, s);
     } else {
-        // (the z-march kernel's >48 KB dynamic shared memory inside a WHILE
-        // body crashes graph instantiation on this driver: host loop for it)
-        if (pcg_graph_enabled() && cfg.max_iters > 0 && fine_kernel_kind() != 4)
+        if (pcg_graph_enabled() && cfg.max_iters > 0)
             rep = nrhs == 1 ? pcg_graph<1>(h, b, x, cfg, h_trace, s) : pcg_graph<2>(h, b, x, cfg, h_trace, s);
         else
             rep = nrhs == 1 ? pcg<1>(h, b, x, cfg, h_trace, s) : pcg<2>(h, b, x, cfg, h_trace, s);

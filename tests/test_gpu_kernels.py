@@ -1,5 +1,6 @@
 """GPU A/B of the fine-level stencil kernels (flat per-position k_span, its
-lane-shuffle variant k_spx and the z-march plane-ring kernel k_zm).
+lane-shuffle variant k_spx, the neighbour-coded k_spc and the z-march
+plane-ring kernel k_zm).
 
 Every stencil mode must be bit-identical between the two kernels, so a
 V-cycle (pre-smooth+defect, restriction input, matrix-free prolongation,
@@ -18,7 +19,8 @@ from conftest import golden_cases, golden_model, load_golden
 
 pytestmark = pytest.mark.gpu
 
-FLAT, ZMARCH, SPX = 2, 4, 5
+FLAT, ZMARCH, SPX, CODED = 2, 4, 5, 6
+KINDS = (FLAT, ZMARCH, SPX, CODED)
 
 
 def _set_kernel(kind):
@@ -48,10 +50,11 @@ def test_vcycle_bitwise(case, sweeps, rng):
     system, h = _hier(golden_model(d), float(d["freq"]), d["a"], cfg)
     r = rng.standard_normal((2, h.n))
     out = []
-    for kind in (FLAT, ZMARCH, SPX):
+    for kind in KINDS:
         _set_kernel(kind)
         out.append(p.v_cycle(h, r))
-    assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
+    for k in range(1, len(KINDS)):
+        assert np.array_equal(out[0], out[k]), KINDS[k]
 
 
 @pytest.mark.parametrize("case", golden_cases("model"))
@@ -64,12 +67,12 @@ def test_solve_agrees(case, method):
     if not np.any(system.rhs):
         pytest.skip("zero rhs")
     res = []
-    for kind in (FLAT, ZMARCH, SPX):
+    for kind in KINDS:
         _set_kernel(kind)
         x, rep = p.solve(system.matrix, system.rhs, h, cfg)
         assert rep.converged
         res.append((rep.iterations, x))
-    for k in (1, 2):
+    for k in range(1, len(KINDS)):
         assert abs(res[0][0] - res[k][0]) <= 1
         assert np.linalg.norm(res[0][1] - res[k][1]) <= 1e-10 * np.linalg.norm(res[0][1])
 
@@ -84,14 +87,15 @@ def test_configs_vcycle_bitwise_and_snapshot(name, rng):
     r = rng.standard_normal((2, h.n))
     z = []
     snaps = []
-    for kind in (FLAT, ZMARCH, SPX):
+    for kind in KINDS:
         _set_kernel(kind)
         z.append(p.v_cycle(h, r))
         sess = Session(w.model, w.frequency_hz, cfg)
         vox, rep, _ = sess.snapshot(torch.from_numpy(w.a).cuda(), keep_psi=True)
         snaps.append((rep.iterations, vox.cpu().numpy()))
-    assert np.array_equal(z[0], z[1]) and np.array_equal(z[0], z[2])
-    for k in (1, 2):
+    for k in range(1, len(KINDS)):
+        assert np.array_equal(z[0], z[k]), KINDS[k]
+    for k in range(1, len(KINDS)):
         assert abs(snaps[0][0] - snaps[k][0]) <= 1
         e = np.abs(snaps[0][1] - snaps[k][1]).max() / np.abs(snaps[0][1]).max()
         assert e <= 1e-6, e
