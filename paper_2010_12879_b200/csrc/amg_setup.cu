@@ -623,8 +623,10 @@ int pick_group(int64_t nnz, int64_t rows) {
     // 4 lanes -- fewer shuffle levels, more rows in flight per warp)
     int g = avg <= 40.0 ? 4 : (avg <= 48.0 ? 8 : 16);
     // small coarse matrices: widen the groups until the launch fills the
-    // machine (latency, not bandwidth, bounds those levels)
-    while (g < 32 && rows * (int64_t)g < (int64_t)148 * 32 * 64) g *= 2;
+    // machine (latency, not bandwidth, bounds those levels); rows of several
+    // hundred entries get up to a whole CTA (k_csr_wide)
+    const int gmax = avg >= 128.0 ? 256 : 32;
+    while (g < gmax && rows * (int64_t)g < (int64_t)148 * 32 * 64 && g * 2 <= 2 * avg) g *= 2;
     return g;
 }
 

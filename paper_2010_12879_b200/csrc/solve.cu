@@ -634,8 +634,104 @@ __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__r
 }
 
 constexpr int kCsrThreads = 256;
+
+// Wide rows (small coarse levels: a few thousand rows of several hundred
+// entries): G = 64 / 128 / 256 lanes of one CTA per row.  Each warp reduces
+// its lanes with a fixed xor tree, the row's leader adds the warp partials
+// in warp order -- deterministic.  Same MODEs as k_csr.
+template <int G, int R, int MODE, bool DOT>
+__global__ void __launch_bounds__(kCsrThreads) k_csr_wide(CsrView m, const double *__restrict__ x,
+                                                         const double *__restrict__ r, const double *__restrict__ od,
+                                                         const double *__restrict__ base, double *__restrict__ y,
+                                                         double *__restrict__ partials,
+                                                         const double *__restrict__ od_aux, double *__restrict__ aux,
+                                                         const int32_t *__restrict__ rowmap) {
+    static_assert(G >= 64 && G <= kCsrThreads, "wide rows only");
+    using W = V<R>;
+    using T = typename W::T;
+    constexpr int RPB = kCsrThreads / G, WPR = G / 32;
+    __shared__ double wp[kCsrThreads / 32][R];
+    __shared__ double red[32 * R];
+    const int li = threadIdx.x % G, rr = threadIdx.x / G, wid = threadIdx.x >> 5;
+    double dot[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) dot[c] = 0.0;
+    const int64_t iters = (m.rows + (int64_t)gridDim.x * RPB - 1) / ((int64_t)gridDim.x * RPB);
+    for (int64_t itr = 0; itr < iters; ++itr) {
+        const int64_t row = (itr * gridDim.x + blockIdx.x) * RPB + rr;
+        const bool valid = row < m.rows;
+        T acc = W::zero();
+        if (valid) {
+            constexpr int U = 4;
+            const int64_t q1 = m.ptr[row + 1];
+            for (int64_t q = m.ptr[row] + li; q < q1; q += U * G) {
+                int col[U];
+                double a[U];
+                T xv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool in = q + u * G < q1;
+                    col[u] = in ? m.col[q + u * G] : -1;
+                    a[u] = in ? m.val[q + u * G] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (col[u] >= 0) xv[u] = MODE == 2 ? W::scale(od[col[u]], W::ld(r, col[u])) : W::ld(x, col[u]);
+                    else xv[u] = W::zero();
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (col[u] >= 0) acc = W::fma_(a[u], xv[u], acc);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            double v = W::comp(acc, c);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if ((threadIdx.x & 31) == 0) wp[wid][c] = v;
+        }
+        __syncthreads();
+        if (valid && li == 0) {
+            double ac[R];
+#pragma unroll
+            for (int c = 0; c < R; ++c) {
+                ac[c] = 0.0;
+                for (int k = 0; k < WPR; ++k) ac[c] += wp[rr * WPR + k][c];
+            }
+            const int64_t gr = rowmap ? (int64_t)rowmap[row] : row;
+            T sum;
+            if constexpr (R == 1) sum = ac[0];
+            else sum = make_double2(ac[0], ac[1]);
+            T out;
+            if (MODE == 0) out = sum;
+            else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(r, gr), sum);
+            else if (MODE == 3) out = W::add(W::ld(x, gr), W::scale(od[gr], W::sub(W::ld(r, gr), sum)));
+            else if (MODE == 4) out = W::add(W::scale(od[gr], W::ld(r, gr)), sum);
+            else out = W::add(W::ld(base, gr), sum);
+            W::st(y, gr, out);
+            if (MODE == 0 && aux) W::st(aux, gr, W::scale(od_aux[gr], out));
+            if (DOT) {
+#pragma unroll
+                for (int c = 0; c < R; ++c) {
+                    if (MODE == 0) dot[c] += W::dot(W::ld(x, gr), out, c);
+                    else if (MODE == 3) dot[c] += W::dot(W::ld(r, gr), out, c);
+                    else dot[c] += W::dot(out, out, c);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (DOT) {
+        block_sum<R>(dot, red);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int c = 0; c < R; ++c) partials[blockIdx.x * R + c] = dot[c];
+    }
+}
+
 inline int csr_grid(int64_t rows, int G) {
-    int64_t groups = (int64_t)kCsrThreads / G;
+    int64_t groups = G >= kCsrThreads ? 1 : (int64_t)kCsrThreads / G;
     int64_t g = (rows + groups - 1) / groups;
     if (g < 1) g = 1;
     if (g > 148 * 16) g = 148 * 16;
@@ -646,7 +742,11 @@ template <int G, int R, int MODE, bool DOT>
 void launch_csr_g(const Csr &m, const double *x, const double *r, const double *od, const double *base, double *y,
                   double *partials, cudaStream_t s, int grid, const double *od_aux, double *aux,
                   const int32_t *rowmap) {
-    k_csr<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials, od_aux, aux, rowmap);
+    if constexpr (G > 32)
+        k_csr_wide<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials, od_aux, aux,
+                                                                 rowmap);
+    else
+        k_csr<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials, od_aux, aux, rowmap);
 }
 
 template <int R, int MODE, bool DOT>
@@ -658,6 +758,9 @@ int launch_csr(const Csr &m, int G, const double *x, const double *r, const doub
         case 4: launch_csr_g<4, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
         case 8: launch_csr_g<8, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
         case 16: launch_csr_g<16, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
+        case 64: launch_csr_g<64, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
+        case 128: launch_csr_g<128, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
+        case 256: launch_csr_g<256, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
         default: launch_csr_g<32, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
     }
     SPFD_LAUNCH_CHECK();
@@ -1191,7 +1294,7 @@ void run_tail(Amg &h, int l0, const double *r, double *z, cudaStream_t s) {
         T.r = i == 0 ? const_cast<double *>(r) : L.vr.get();
         T.x = i == 0 ? z : L.vx.get();
         T.d = L.vd.get();
-        T.gA = L.a_group; T.gP = L.p_group; T.gR = L.r_group;
+        T.gA = std::min(L.a_group, 32); T.gP = std::min(L.p_group, 32); T.gR = std::min(L.r_group, 32);
     }
     Level &C = h.lv[nl - 1];
     t.cinv = h.cinv.get();
