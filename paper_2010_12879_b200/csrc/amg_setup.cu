@@ -789,7 +789,7 @@ void alloc_krylov(Amg &h, int64_t nvec0, int max_nrhs);
 static void finish_level(Level &L, const Csr &A, double omega, cudaStream_t s) {
     const int T = 256;
     L.dinv.alloc(L.nvec);
-    L.odinv.alloc(L.nvec);
+    L.odinv.alloc(L.nvec + 4);
     DevBuf<int> bad;
     bad.alloc(1);
     SPFD_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
@@ -841,7 +841,7 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
         if (st0) {
             // dinv / odinv in span layout from the operator's exact diagonal
             L.dinv.alloc(L.nvec);
-            L.odinv.alloc(L.nvec);
+            L.odinv.alloc(L.nvec + 4);
             SPFD_CUDA(cudaMemcpyAsync(L.dinv.get(), h->op->dinv.get(), L.nvec * sizeof(double),
                                       cudaMemcpyDeviceToDevice, s));
             // odinv = omega * dinv computed on the DOF CSR then mapped
@@ -859,7 +859,7 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
                 // matrix-free transfers: aggregate per span position and the
                 // member lists of T^T (ascending positions); P/R kept in DOF
                 // numbering only for export
-                L.agg_pos.alloc(L.nvec);
+                L.agg_pos.alloc(L.nvec + 4);
                 k_agg_pos<<<grid_for(L.nvec, T), T, 0, s>>>(h->op->pos_to_dof.get(), L.nvec, L.agg.get(),
                                                             L.agg_pos.get());
                 SPFD_LAUNCH_CHECK();

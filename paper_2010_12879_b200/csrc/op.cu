@@ -515,7 +515,7 @@ Operator *op_create(const int64_t *dims, const double *spacing, const uint16_t *
 
         // span arrays
         int64_t L = op->L;
-        op->wx.alloc(L); op->wy.alloc(L); op->wz.alloc(L);
+        op->wx.alloc(L + 4); op->wy.alloc(L + 4); op->wz.alloc(L + 4);  // +4: aligned bulk-copy supersets
         op->diag.alloc(L); op->dinv.alloc(L);
         op->pos_to_dof.alloc(L);
         op->dofmask.alloc((L + 31) / 32 + 1);

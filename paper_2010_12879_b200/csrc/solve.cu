@@ -233,6 +233,7 @@ __device__ __forceinline__ double2 shfl_dn1<double2>(double2 v) {
 }
 
 #include "zmarch.cuh"
+#include "zmt.cuh"
 
 // Flat per-position kernel with the -x/+x neighbours (input and weight) taken
 // from the adjacent lanes: a warp holds 32 consecutive span positions, so
@@ -1048,6 +1049,7 @@ int fine_kernel_kind() {
         if (e && std::string(e) == "spx") v = 5;
         if (e && std::string(e) == "flat") v = 2;
         if (e && std::string(e) == "coded") v = 6;
+        if (e && std::string(e) == "zt") v = 7;
     }
     return v;
 }
@@ -1163,6 +1165,20 @@ int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
         if (g > 0) k_span<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, b);
         SPFD_LAUNCH_CHECK();
         return g;
+    }
+    if constexpr (R == 2) {
+        if (kind == 7 && a.pb == 0 && a.pe >= op.L && zm_build(op)) {
+            const int g = (int)op.n_zm_items;
+            constexpr size_t smem = zt_smem<MODE>();
+            static bool attr = false;
+            if (!attr) {
+                SPFD_CUDA(cudaFuncSetAttribute(k_zt<MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                attr = true;
+            }
+            k_zt<MODE, DOT><<<g, kZtThreads, smem, s>>>(v, op.zm_items.get(), a);
+            SPFD_LAUNCH_CHECK();
+            return g;
+        }
     }
     if (kind == 6) {
         if (!op.coded) {  // lazily: neighbour codes and row deltas (one pass each)

@@ -1,6 +1,6 @@
 """GPU A/B of the fine-level stencil kernels (flat per-position k_span, its
-lane-shuffle variant k_spx, the neighbour-coded k_spc and the z-march
-plane-ring kernel k_zm).
+lane-shuffle variant k_spx, the neighbour-coded k_spc, the z-march
+cp.async plane-ring kernel k_zm and its bulk-copy (TMA) variant k_zt).
 
 Every stencil mode must be bit-identical between the two kernels, so a
 V-cycle (pre-smooth+defect, restriction input, matrix-free prolongation,
@@ -19,8 +19,8 @@ from conftest import golden_cases, golden_model, load_golden
 
 pytestmark = pytest.mark.gpu
 
-FLAT, ZMARCH, SPX, CODED = 2, 4, 5, 6
-KINDS = (FLAT, ZMARCH, SPX, CODED)
+FLAT, ZMARCH, SPX, CODED, ZTMA = 2, 4, 5, 6, 7
+KINDS = (FLAT, ZMARCH, SPX, CODED, ZTMA)
 
 
 def _set_kernel(kind):

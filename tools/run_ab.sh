@@ -10,7 +10,7 @@ for k in ${KINDS:-flat zm}; do
 done
 for k in ${NCU_KINDS:-zm}; do
 SPFD_SPAN_KERNEL=$k timeout 900 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "timed/" \
-   -k regex:"k_span|k_zm" -c 4 -o gpurun_out/${tag}_full_$k \
+   -k regex:"k_span|k_zm|k_zt" -c 4 -o gpurun_out/${tag}_full_$k \
    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${tag}_ncu_$k.log 2>&1
 tail -2 gpurun_out/${tag}_ncu_$k.log
 done
