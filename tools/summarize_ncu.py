@@ -32,7 +32,7 @@ for r in rows[2:]:
                  f"{float(r[cols['lts__throughput.avg.pct_of_peak_sustained_elapsed']]):.0f} | "
                  f"{float(r[cols['sm__warps_active.avg.pct_of_peak_sustained_active']]):.0f} | "
                  f"{r[cols['launch__registers_per_thread']]} | {r[cols['launch__grid_size']]} |")
-    if name.startswith("k_span<2, 0, 1>") and "C3_fine_spmv_dram_bytes" not in traffic:
+    if name.startswith("k_span<2, 0, 1") and "C3_fine_spmv_dram_bytes" not in traffic:
         traffic["C3_fine_spmv_dram_bytes"] = rd + wr
         traffic["C3_fine_spmv_ncu_us"] = us
 open(out_md, "w").write("\n".join(lines) + "\n")
