@@ -846,9 +846,10 @@ __device__ __forceinline__ double axis_comp(double vt, bool mt, double vh, bool 
     double evt = mt ? __ddiv_rn(mul_rn(vt, 1.0), sa) : 0.0;
     double evh = mh ? __ddiv_rn(mul_rn(vh, 1.0), sa) : 0.0;
     double num = add_rn(add_rn(0.0, evt), evh);
-    double den = add_rn(add_rn(0.0, mt ? 1.0 : 0.0), mh ? 1.0 : 0.0);
-    if (den == 0.0) return 0.0;
-    return __ddiv_rn(num, fmax(den, 1.0));
+    // num / max(cnt, 1) with cnt in {0, 1, 2}: dividing by 1 or 2 is exact
+    // as the identity / a multiply by 0.5 (same IEEE result, no divide)
+    if (!mt && !mh) return 0.0;
+    return (mt && mh) ? mul_rn(num, 0.5) : num;
 }
 
 __device__ __forceinline__ double field_mag(double cx, double cy, double cz) {
@@ -949,20 +950,21 @@ void op_voxel_average(const Operator &op, const double *node, double *vox, int n
 // voxel average reading the span node field.  Bit-identical to the three
 // separate stages (inactive edges contribute exact zeros).
 template <int R>
-__global__ void __launch_bounds__(kSpanThreads) k_node_field_span(SpanView v, EdgeIdx e, const double *__restrict__ a,
+__global__ void __launch_bounds__(kSpanThreads, 4) k_node_field_span(SpanView v, EdgeIdx e, const double *__restrict__ a,
                                                                   int64_t E, const double *__restrict__ psi,
                                                                   double omega, double sx, double sy, double sz,
                                                                   double *__restrict__ node, PosRange pr) {
     int t = pr.tile0 + blockIdx.x;
     int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
+    int r = r0;
     for (int u = 0; u < kTile / kSpanThreads; ++u) {
         int p = t * kTile + u * kSpanThreads + threadIdx.x;
         if (p >= pr.pe) break;
         if (p < pr.pb) continue;
-        int r = find_row(v.rows, r0, r1, p);
+        r = find_row(v.rows, r, r1, p);  // positions grow with u: search from the last row
         int4 q = v.rows[r];
         int i = q.y + (p - q.x);
-        int j = r % v.NY, k = r / v.NY;
+        int j = q.w, k = (r - j) / v.NY;
         MinusW m = minus_edges(v, p, r, i, q);
         double wxp = v.wx[p], wyp = v.wy[p], wzp = v.wz[p];
         int pxp = (wxp > 0.0) ? p + 1 : -1;
