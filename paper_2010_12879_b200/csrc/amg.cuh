@@ -41,6 +41,8 @@ struct Level {
     DevBuf<double> odinv;     // [nvec] omega * dinv
     DevBuf<double> vr, vx, vd, vt;  // workspaces [nvec * max_nrhs]
     int p_group = 4, r_group = 32, a_group = 32;  // lanes per row in CSR kernels
+    Csr AP;                   // coarse levels, V(1,1): A_l P_l for the fused prolongation + post-smooth
+    int ap_group = 4;
 };
 
 struct Dist;   // z-slab decomposition (dist.cuh)

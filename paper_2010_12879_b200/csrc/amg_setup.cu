@@ -780,7 +780,7 @@ int64_t Amg::device_bytes() const {
                 partials.bytes() + scal.bytes() + fg_basis.bytes() + fg_prec.bytes();
     for (auto &l : lv)
         b += l.A.bytes() + l.P.bytes() + l.R.bytes() + l.P_dof.bytes() + l.R_dof.bytes() + l.agg.bytes() +
-             l.dinv.bytes() + l.odinv.bytes() + l.agg_pos.bytes() + l.mem_ptr.bytes() + l.mem_pos.bytes() + l.vr.bytes() + l.vx.bytes() + l.vd.bytes() + l.vt.bytes();
+             l.dinv.bytes() + l.odinv.bytes() + l.agg_pos.bytes() + l.mem_ptr.bytes() + l.mem_pos.bytes() + l.vr.bytes() + l.vx.bytes() + l.vd.bytes() + l.vt.bytes() + l.AP.bytes();
     return b;
 }
 
@@ -878,6 +878,17 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
         if (!(l == 0 && h->structured)) L.a_group = pick_group(L.A.nnz, L.A.rows);
         if (const char *e = getenv("SPFD_CSR_GROUP_A1"))  // tuning: level-1 smoother lanes per row
             if (l == 1) L.a_group = atoi(e);
+        // V(1,1) on a coarse level: z = x1 + od (d - (A P) e) with d the pre-smoothing
+        // defect replaces "x1 = x0 + P e; z = x1 + od (r - A x1)" -- one pass over
+        // P and A P (whose gathers hit the small coarse vector) instead of P and A
+        static const bool use_ap = !(getenv("SPFD_AP") && std::string(getenv("SPFD_AP")) == "0");
+        if (use_ap && l >= 1 && l < nl - 1 && h->pre == 1 && h->post == 1) {
+            spgemm(view(L.A), view(L.P), L.P.cols, L.AP, false, s);
+            // only where A P is no larger than A (C3: levels 2-3; on level 1
+            // the product holds ~1.3x A's entries and measured no faster)
+            if (L.AP.nnz > L.A.nnz) L.AP = Csr{};
+            else L.ap_group = pick_group(L.AP.nnz, L.AP.rows);
+        }
         L.vr.alloc(L.nvec * R);
         L.vx.alloc(L.nvec * R);
         L.vd.alloc(L.nvec * R);

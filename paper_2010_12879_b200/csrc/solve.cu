@@ -636,6 +636,68 @@ __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__r
 
 constexpr int kCsrThreads = 256;
 
+// Fused coarse-level prolongation + post-smooth (V(1,1)):
+//   x1 = od r + P e,   z = x1 + od (d - (A P) e)
+// with d = r - A (od r) the pre-smoothing defect.  Equal to the two-pass
+// "x1 = x0 + P e; z = x1 + od (r - A x1)" up to rounding (A x1 = A x0 +
+// (A P) e); the gathers of both rows hit the small coarse vector e.
+template <int G, int R>
+__global__ void __launch_bounds__(kCsrThreads) k_csr_pp(CsrView P, CsrView M, const double *__restrict__ e,
+                                                       const double *__restrict__ r, const double *__restrict__ od,
+                                                       const double *__restrict__ d, double *__restrict__ z) {
+    using W = V<R>;
+    using T = typename W::T;
+    const int lane = threadIdx.x % G;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int GPW = 32 / G;
+    for (int64_t rbase = warp * GPW; rbase < P.rows; rbase += nwarp * GPW) {
+        const int64_t row = rbase + (threadIdx.x & 31) / G;
+        const bool valid = row < P.rows;
+        T ap = W::zero(), am = W::zero();
+        if (valid) {
+            const int64_t p1 = P.ptr[row + 1], m1 = M.ptr[row + 1];
+            for (int64_t q = P.ptr[row] + lane; q < p1; q += G) ap = W::fma_(P.val[q], W::ld(e, P.col[q]), ap);
+            constexpr int U = 4;
+            for (int64_t q = M.ptr[row] + lane; q < m1; q += U * G) {
+                int col[U];
+                double a[U];
+                T xv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool in = q + u * G < m1;
+                    col[u] = in ? M.col[q + u * G] : -1;
+                    a[u] = in ? M.val[q + u * G] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) xv[u] = col[u] >= 0 ? W::ld(e, col[u]) : W::zero();
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (col[u] >= 0) am = W::fma_(a[u], xv[u], am);
+            }
+        }
+        double sp[R], sm[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            sp[c] = W::comp(ap, c);
+            sm[c] = W::comp(am, c);
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) {
+                sp[c] += __shfl_xor_sync(0xffffffffu, sp[c], o, G);
+                sm[c] += __shfl_xor_sync(0xffffffffu, sm[c], o, G);
+            }
+        }
+        if (valid && lane == 0) {
+            T pe, me;
+            if constexpr (R == 1) { pe = sp[0]; me = sm[0]; }
+            else { pe = make_double2(sp[0], sp[1]); me = make_double2(sm[0], sm[1]); }
+            const double o = od[row];
+            const T x1 = W::add(W::scale(o, W::ld(r, row)), pe);
+            W::st(z, row, W::add(x1, W::scale(o, W::sub(W::ld(d, row), me))));
+        }
+    }
+}
+
 // Wide rows (small coarse levels: a few thousand rows of several hundred
 // entries): G = 64 / 128 / 256 lanes of one CTA per row.  Each warp reduces
 // its lanes with a fixed xor tree, the row's leader adds the warp partials
@@ -1437,6 +1499,18 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
     launch_csr<R, 0, false>(L.R, L.r_group, d, nullptr, nullptr, nullptr, C.vr.get(), nullptr, s, C.odinv.get(),
                             x0 ? C.vt.get() : nullptr);
     vcycle_level<R>(h, l + 1, C.vr.get(), C.vx.get(), s);
+    if (L.AP.rows > 0 && h.pre == 1 && h.post == 1) {
+        // fused prolongation + post-smooth from the pre-smoothing defect d
+        const int grid = csr_grid(L.P.rows, std::min(L.ap_group, 32));
+        switch (std::min(L.ap_group, 32)) {
+            case 4: k_csr_pp<4, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z); break;
+            case 8: k_csr_pp<8, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z); break;
+            case 16: k_csr_pp<16, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z); break;
+            default: k_csr_pp<32, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z); break;
+        }
+        SPFD_LAUNCH_CHECK();
+        return;
+    }
     // x1 = x + P e (linsolve.py:194) -> d
     if (xbase) launch_csr<R, 5, false>(L.P, L.p_group, C.vx.get(), r, L.odinv.get(), xbase, d, nullptr, s);
     else launch_csr<R, 4, false>(L.P, L.p_group, C.vx.get(), r, L.odinv.get(), nullptr, d, nullptr, s);
