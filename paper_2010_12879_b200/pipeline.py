@@ -44,6 +44,11 @@ class Session:
         self.comm = None
         self.dof_range = (0, self.op.n_dofs)
         self.vox_range = (0, self.op.n_cond_voxels)
+        # node planes holding conductive nodes: only their edges are ever read
+        # (RHS and E-field touch edges of conductive nodes only), so the host
+        # path copies just those edge ranges
+        zc = np.flatnonzero(np.asarray(model.voxel_kappa(self.frequency_hz) > 0).any(axis=(0, 1)))
+        self.plane_range = (int(zc[0]), int(zc[-1]) + 2) if zc.size else (0, 0)
 
     def distribute(self, comm, replicate_below: int = 100_000):
         """Split the solve into z-slabs over `comm` (a distributed.Communicator):
@@ -59,13 +64,14 @@ class Session:
         return self
 
     def edge_slices(self):
-        """Edge-index ranges this rank reads (all edges on one GPU): x- and
-        y-edges of its node planes, z-edges of its planes and the one below."""
+        """Edge-index ranges this rank reads: x- and y-edges of its node planes
+        (one GPU: the planes holding conductive nodes), z-edges of those
+        planes and the one below."""
         nx, ny, nz = self.op.dims
         NX, NY = nx + 1, ny + 1
-        if self.comm is None:
-            return [(0, self.op.n_edges)]
         kb, ke = self.plane_range
+        if ke <= kb:
+            return [(0, self.op.n_edges)]
         ex, ey = nx * NY * (nz + 1), NX * ny * (nz + 1)
         return [(nx * NY * kb, nx * NY * ke),
                 (ex + NX * ny * kb, ex + NX * ny * ke),
@@ -128,7 +134,8 @@ class Session:
             self._a_dev = torch.empty(a_t.shape, dtype=torch.float64, device="cuda")
         nb = a_t.is_pinned()
         for e0, e1 in self.edge_slices():   # only the edges this rank's slab reads
-            self._a_dev[:, e0:e1].copy_(a_t[:, e0:e1], non_blocking=nb)
+            for c in range(a_t.shape[0]):   # contiguous 1-D ranges (a 2-D column slice is strided)
+                self._a_dev[c, e0:e1].copy_(a_t[c, e0:e1], non_blocking=nb)
         vox, rep, _ = self.snapshot(self._a_dev)
         v0, v1 = self.vox_range
         if out is None:

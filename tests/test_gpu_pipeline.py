@@ -74,3 +74,33 @@ def test_run_benchmark(g):
     assert res.runs == 3 and len(res.iterations) == 3 and len(set(res.iterations)) == 1
     assert set(res.steps) == set(STEP_NAMES) | {"total"}
     assert "amg setup" in res.to_text() and res.to_csv().startswith("step,mean_s")
+
+
+@pytest.mark.parametrize("case", ["c1", "sphere8_uniform", "layered_dipole", "two_blobs"])
+def test_snapshot_host_matches_device(case):
+    """The host path copies only the edge ranges of the planes that hold
+    conductive nodes; its result equals the device-resident snapshot's bit
+    for bit (the untouched edges are never read), with the plane range
+    covering every conductive voxel."""
+    import torch
+    from conftest import golden_model
+    from paper_2010_12879_b200 import Session, SolveConfig, workloads
+    if case == "c1":
+        w = workloads.c1(24)
+        model, freq, a = w.model, w.frequency_hz, w.a
+    else:
+        d = load_golden(case)
+        model, freq = golden_model(d), float(d["freq"])
+        a = np.stack([d["a"], 0.5 * d["a"]])
+    sess = Session(model, freq, SolveConfig(rel_tol=1e-10))
+    kb, ke = sess.plane_range
+    zc = np.flatnonzero((model.voxel_kappa(freq) > 0).any(axis=(0, 1)))
+    assert kb == zc[0] and ke == zc[-1] + 2
+    vox_d, rep_d, _ = sess.snapshot(torch.from_numpy(np.ascontiguousarray(a)).cuda())
+    vox_d = vox_d.cpu().numpy().copy()
+    pinned = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    vox_h, rep_h = sess.snapshot_host(pinned)
+    assert rep_h.iterations == rep_d.iterations
+    assert np.array_equal(vox_h, vox_d)
+    h2d, _ = sess.host_bytes(a.shape[0])
+    assert h2d <= a.size * 8
