@@ -876,8 +876,14 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
             L.r_group = pick_group(L.R.nnz, L.R.rows);
         }
         if (!(l == 0 && h->structured)) L.a_group = pick_group(L.A.nnz, L.A.rows);
-        if (const char *e = getenv("SPFD_CSR_GROUP_A1"))  // tuning: level-1 smoother lanes per row
-            if (l == 1) L.a_group = atoi(e);
+        // tuning overrides: SPFD_GROUP_{A,P,R,AP}<level>=lanes
+        auto over = [&](const char *kind, int &g) {
+            const std::string key = std::string("SPFD_GROUP_") + kind + std::to_string(l);
+            if (const char *e = getenv(key.c_str())) g = atoi(e);
+        };
+        over("A", L.a_group);
+        over("P", L.p_group);
+        over("R", L.r_group);
         // V(1,1) on a coarse level: z = x1 + od (d - (A P) e) with d the pre-smoothing
         // defect replaces "x1 = x0 + P e; z = x1 + od (r - A x1)" -- one pass over
         // P and A P (whose gathers hit the small coarse vector) instead of P and A
@@ -888,6 +894,7 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
             // the product holds ~1.3x A's entries and measured no faster)
             if (L.AP.nnz > L.A.nnz) L.AP = Csr{};
             else L.ap_group = pick_group(L.AP.nnz, L.AP.rows);
+            over("AP", L.ap_group);
         }
         L.vr.alloc(L.nvec * R);
         L.vx.alloc(L.nvec * R);
