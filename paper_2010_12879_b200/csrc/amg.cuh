@@ -73,6 +73,7 @@ struct Amg {
     cudaStream_t cap = nullptr;             // private capture stream
     cudaGraphExec_t pcg_exec[3] = {nullptr, nullptr, nullptr};
     int64_t pcg_body_launches[3] = {0, 0, 0};
+    int pcg_kind[3] = {-1, -1, -1};         // fine-kernel kind captured in each graph
     DevBuf<double> pcg_trace;               // [cap_iters * 2] per-iteration residual estimates
     int64_t pcg_trace_cap = 0;
     Amg() = default;

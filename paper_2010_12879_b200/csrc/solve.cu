@@ -1706,6 +1706,11 @@ bool pcg_graph_build(Amg &h, int64_t max_iters) {
         h.pcg_trace_cap = std::max<int64_t>(max_iters, 1024);
         h.pcg_trace.alloc(h.pcg_trace_cap * 2);
     }
+    if (h.pcg_exec[R] && h.pcg_kind[R] != fine_kernel_kind()) {  // kernel selection changed: recapture
+        cudaGraphExecDestroy(h.pcg_exec[R]);
+        h.pcg_exec[R] = nullptr;
+        h.pcg_body_launches[R] = 0;
+    }
     if (h.pcg_exec[R]) return true;
     if (h.pcg_body_launches[R] < 0) return false;  // capture failed before: stay on the host loop
     cudaGraph_t g = nullptr;
@@ -1747,6 +1752,7 @@ bool pcg_graph_build(Amg &h, int64_t max_iters) {
     h.pcg_body_launches[R] = launch_count() - l0;
     cudaGraphDestroy(g);
     h.pcg_exec[R] = exec;
+    h.pcg_kind[R] = fine_kernel_kind();
     return true;
 }
 
