@@ -1782,8 +1782,14 @@ spfd_report pcg_graph(Amg &h, const double *b, double *x_out, const spfd_config 
     const double tol = cfg.rel_tol;
     int it = 0;
     while (true) {
-        // (re)start: r = b - A x, p = 0, alpha = 0, rho initialised by the first body
-        level0_apply<R>(h, 1, false, x, b, r, s);
+        // (re)start: r = b - A x, p = 0, alpha = 0, rho initialised by the first body.
+        // With x = 0 (first start) r = b bit for bit (b - (+0)); the first solve
+        // still runs the stencil once so lazily built kernel data exist before
+        // the capture below
+        if (it == 0 && h.pcg_exec[R] && h.pcg_kind[R] == fine_kernel_kind())
+            SPFD_CUDA(cudaMemcpyAsync(r, b, n * R * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        else
+            level0_apply<R>(h, 1, false, x, b, r, s);
         // capture after the first fine-level launch: lazily built kernel data
         // (neighbour codes, z-march items) must not be built inside the graph
         if (!pcg_graph_build<R>(h, cfg.max_iters)) return pcg<R>(h, b, x_out, cfg, h_trace, s);
