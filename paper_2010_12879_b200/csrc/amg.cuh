@@ -64,6 +64,7 @@ struct Amg {
     DevBuf<double> scal;      // device scalars
     DevBuf<double> fg_basis, fg_prec;  // FGMRES basis (allocated on demand)
     int64_t fg_m = 0;
+    int fg_R = 1;             // rhs count the FGMRES basis was sized for
     int vc_partials = 0;      // r.z partials written by the last V-cycle (0 = none)
     Dist *dist = nullptr;     // set by amg_distribute (owned)
     cudaStream_t side = nullptr;            // PCG x-update overlap stream

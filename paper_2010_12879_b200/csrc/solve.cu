@@ -1074,6 +1074,7 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
     int64_t np = kDotGrid;
     if (h.structured) np = std::max<int64_t>(np, h.op->n_tiles);
     np = std::max<int64_t>(np, 148 * 16);
+    np = std::max<int64_t>(np, (int64_t)kDotGrid * 8);  // batched FGMRES block dots (k_mdot, 8 vectors)
     h.partials.alloc(np * 2 + 64);
     h.scal.alloc(S_END);
     SPFD_CUDA(cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking));
@@ -1901,6 +1902,271 @@ __global__ void k_combine(int64_t n, int j, const double *y, const double *zb, d
     }
 }
 
+// ---- batched FGMRES (both rhs of a pair in one Arnoldi process) ----------
+// Per Arnoldi step: one V-cycle and one SpMV for both rhs (double2), then
+// classical Gram-Schmidt with one re-orthogonalisation (CGS2) as block
+// kernels -- k_mdot (all <V_i, w> for up to 8 basis vectors per launch,
+// fixed-order per-CTA partials), k_mfinal, k_maxpy (w -= sum_i h_i V_i in
+// order i) -- instead of the reference's MGS, which needs 3(j+1) launches
+// per step and re-reads w for every basis vector.  Givens rotations, the
+// least-squares solve and all convergence decisions stay per rhs on the
+// host, as in fgmres1 (linsolve.py:200-298 semantics per rhs).
+constexpr int kMdotNI = 8;
+
+template <int R, int NI>
+__global__ void __launch_bounds__(256) k_mdot(int64_t n, const double *Vb, int i0, int ni, const double *w,
+                                              double *partials) {
+    using W = V<R>;
+    __shared__ double red[32 * NI * R];
+    double acc[NI * R];
+#pragma unroll
+    for (int k = 0; k < NI * R; ++k) acc[k] = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const typename W::T wv = W::ld(w, p);
+#pragma unroll
+        for (int k = 0; k < NI; ++k) {
+            if (k < ni) {
+                const typename W::T v = W::ld(Vb + (int64_t)(i0 + k) * n * R, p);
+#pragma unroll
+                for (int c = 0; c < R; ++c) acc[k * R + c] = fma(W::comp(v, c), W::comp(wv, c), acc[k * R + c]);
+            }
+        }
+    }
+    block_sum<NI * R>(acc, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < NI * R; ++k) partials[(int64_t)blockIdx.x * NI * R + k] = acc[k];
+}
+
+// out[k] = sum over CTAs of partials[.][k], k < nv (one block per value, fixed order)
+__global__ void __launch_bounds__(256) k_mfinal(const double *partials, int nblocks, int stride, double *out) {
+    __shared__ double red[32];
+    const int k = blockIdx.x;
+    double s[1] = {0.0};
+    const int per = (nblocks + blockDim.x - 1) / blockDim.x;
+    const int b0 = threadIdx.x * per, b1 = min(nblocks, b0 + per);
+    for (int b = b0; b < b1; ++b) s[0] += partials[(int64_t)b * stride + k];
+    block_sum<1>(s, red);
+    if (threadIdx.x == 0) out[k] = s[0];
+}
+
+// w -= sum_{i < nv} h[i] V_i  (h: [nv][R] on the device, applied in order i)
+template <int R>
+__global__ void k_maxpy(int64_t n, const double *Vb, int nv, const double *hv, double *w) {
+    using W = V<R>;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        typename W::T acc = W::ld(w, p);
+        for (int i = 0; i < nv; ++i) {
+            double nh[R];
+#pragma unroll
+            for (int c = 0; c < R; ++c) nh[c] = -hv[i * R + c];
+            acc = vfma<R>(nh, W::ld(Vb + (int64_t)i * n * R, p), acc);
+        }
+        W::st(w, p, acc);
+    }
+}
+
+// y = x * mult[c] per component
+template <int R>
+__global__ void k_scale_r(int64_t n, const double *mult, const double *x, double *y) {
+    using W = V<R>;
+    double mu[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) mu[c] = mult[c];
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        typename W::T v = W::ld(x, p);
+        if constexpr (R == 1) v = v * mu[0];
+        else v = make_double2(v.x * mu[0], v.y * mu[1]);
+        W::st(y, p, v);
+    }
+}
+
+// x[:, c] += sum_{k < jc[c]} Z_k[:, c] y[c][k]
+template <int R>
+__global__ void k_combine_r(int64_t n, int m, const int *jc, const double *y, const double *Zb, double *x) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            double acc = 0.0;
+            for (int k = 0; k < jc[c]; ++k) acc += Zb[((int64_t)k * n + p) * R + c] * y[c * m + k];
+            x[p * R + c] += acc;
+        }
+    }
+}
+
+template <int R>
+spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &cfg, double *h_trace,
+                         cudaStream_t s) {
+    spfd_report rep{};
+    const int64_t n = h.lv[0].nvec;
+    const int m = cfg.restart;
+    SPFD_CHECK(m >= 1 && m <= 60, SPFD_EINVAL, "restart must be in [1, 60] for batched FGMRES");
+    if (h.fg_m < m || h.fg_R < R) {
+        h.fg_basis.alloc((int64_t)(m + 1) * n * R);
+        h.fg_prec.alloc((int64_t)m * n * R);
+        h.fg_m = m;
+        h.fg_R = R;
+    }
+    double *Vb = h.fg_basis.get(), *Zb = h.fg_prec.get();
+    double *w = h.kq.get(), *r = h.kr.get();
+    double *sc = h.scal.get();
+    const int G = grid_for(n, 256, 148 * 16);
+    const int SH1 = S_H, SH2 = S_H + 128, SMUL = S_TMP + 2;  // pass-1 / pass-2 columns, scale factors
+    SPFD_CUDA(cudaMemsetAsync(x, 0, n * R * sizeof(double), s));
+    SPFD_CUDA(cudaMemsetAsync(sc, 0, S_END * sizeof(double), s));
+    dot<R>(h, n, b, b, S_BB, F_STORE, s);
+    double hb[R];
+    SPFD_CUDA(cudaMemcpyAsync(hb, sc + S_BB, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    double bnorm[R];
+    bool done[R], all = true;
+    for (int c = 0; c < R; ++c) {
+        bnorm[c] = std::sqrt(hb[c]);
+        if (!std::isfinite(bnorm[c])) { rep.status = SPFD_ENONFINITE; return rep; }
+        done[c] = bnorm[c] == 0.0;
+        all = all && done[c];
+        rep.rel_residual[c] = 0.0;
+    }
+    if (all) { rep.converged = 1; return rep; }
+    std::vector<double> H[R], cs[R], sn[R], g[R];
+    for (int c = 0; c < R; ++c) {
+        H[c].assign((size_t)(m + 1) * m, 0.0);
+        cs[c].assign(m, 0.0); sn[c].assign(m, 0.0); g[c].assign(m + 1, 0.0);
+    }
+    DevBuf<double> ydev;
+    ydev.alloc((int64_t)R * m);
+    DevBuf<int> jcdev;
+    jcdev.alloc(R);
+    const int nparts = kDotGrid;
+    int its = 0;
+    int its_c[R];  // iterations each rhs took part in (fgmres1's count per rhs)
+    for (int c = 0; c < R; ++c) its_c[c] = 0;
+    while (its < cfg.max_iters) {
+        // restart: true residual per rhs (linsolve.py:244-248)
+        level0_apply<R>(h, 1, false, x, b, r, s);
+        dot<R>(h, n, r, r, S_TMP, F_STORE, s);
+        double rr[R];
+        SPFD_CUDA(cudaMemcpyAsync(rr, sc + S_TMP, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPFD_CUDA(cudaStreamSynchronize(s));
+        bool active[R], any = false;
+        double mult[R];
+        for (int c = 0; c < R; ++c) {
+            const double beta = std::sqrt(rr[c]);
+            const double rel = bnorm[c] > 0 ? beta / bnorm[c] : 0.0;
+            if (rel <= cfg.rel_tol) done[c] = true;  // converged on the true residual
+            active[c] = !done[c];
+            any = any || active[c];
+            std::fill(H[c].begin(), H[c].end(), 0.0);
+            std::fill(g[c].begin(), g[c].end(), 0.0);
+            g[c][0] = beta;
+            mult[c] = active[c] ? 1.0 / beta : 0.0;
+        }
+        if (!any) break;
+        SPFD_CUDA(cudaMemcpyAsync(sc + SMUL, mult, R * sizeof(double), cudaMemcpyHostToDevice, s));
+        k_scale_r<R><<<G, 256, 0, s>>>(n, sc + SMUL, r, Vb);
+        int jc[R];
+        for (int c = 0; c < R; ++c) jc[c] = 0;
+        int j = 0;
+        while (j < m && its < cfg.max_iters) {
+            double *vj = Vb + (int64_t)j * n * R, *zj = Zb + (int64_t)j * n * R;
+            amg_vcycle(h, vj, zj, R, s);
+            level0_apply<R>(h, 0, false, zj, nullptr, w, s);
+            auto cgs = [&](int out) {
+                for (int i0 = 0; i0 <= j; i0 += kMdotNI) {
+                    const int ni = std::min(kMdotNI, j + 1 - i0);
+                    k_mdot<R, kMdotNI><<<nparts, 256, 0, s>>>(n, Vb, i0, ni, w, h.partials.get());
+                    k_mfinal<<<ni * R, 256, 0, s>>>(h.partials.get(), nparts, kMdotNI * R, sc + out + i0 * R);
+                }
+                k_maxpy<R><<<G, 256, 0, s>>>(n, Vb, j + 1, sc + out, w);
+                SPFD_LAUNCH_CHECK();
+            };
+            // CGS2: w = A z_j is nearly parallel to v_j (A M^-1 ~ I), so one
+            // classical pass always cancels most of its norm; measured, the
+            // "twice is enough" test re-orthogonalised at every step anyway
+            cgs(SH1);
+            cgs(SH2);
+            dot<R>(h, n, w, w, S_TMP, F_STORE, s);
+            std::vector<double> h1((size_t)(j + 1) * R), h2((size_t)(j + 1) * R);
+            double nn[R];
+            SPFD_CUDA(cudaMemcpyAsync(h1.data(), sc + SH1, h1.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SPFD_CUDA(cudaMemcpyAsync(h2.data(), sc + SH2, h2.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SPFD_CUDA(cudaMemcpyAsync(nn, sc + S_TMP, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SPFD_CUDA(cudaStreamSynchronize(s));
+            ++its;
+            bool more = false;
+            for (int c = 0; c < R; ++c) {
+                if (!active[c]) { mult[c] = 0.0; continue; }
+                ++its_c[c];
+                const double hn = std::sqrt(nn[c]);
+                if (!std::isfinite(hn)) { rep.status = SPFD_ENONFINITE; rep.iterations = its; return rep; }
+                auto &Hc = H[c];
+                for (int i = 0; i <= j; ++i) Hc[(size_t)i * m + j] = h1[(size_t)i * R + c] + h2[(size_t)i * R + c];
+                for (int i = 0; i < j; ++i) {
+                    const double t1 = cs[c][i] * Hc[(size_t)i * m + j] + sn[c][i] * Hc[(size_t)(i + 1) * m + j];
+                    const double t2 = -sn[c][i] * Hc[(size_t)i * m + j] + cs[c][i] * Hc[(size_t)(i + 1) * m + j];
+                    Hc[(size_t)i * m + j] = t1;
+                    Hc[(size_t)(i + 1) * m + j] = t2;
+                }
+                const double den = std::hypot(Hc[(size_t)j * m + j], hn);
+                if (den == 0.0) { cs[c][j] = 1.0; sn[c][j] = 0.0; }
+                else { cs[c][j] = Hc[(size_t)j * m + j] / den; sn[c][j] = hn / den; }
+                Hc[(size_t)j * m + j] = cs[c][j] * Hc[(size_t)j * m + j] + sn[c][j] * hn;
+                g[c][j + 1] = -sn[c][j] * g[c][j];
+                g[c][j] = cs[c][j] * g[c][j];
+                jc[c] = j + 1;
+                const double est = std::fabs(g[c][j + 1]) / bnorm[c];
+                if (h_trace && its <= cfg.max_iters) h_trace[(int64_t)(its - 1) * R + c] = est;
+                if (hn == 0.0 || est <= cfg.rel_tol) {
+                    active[c] = false;
+                    mult[c] = 0.0;
+                } else {
+                    mult[c] = 1.0 / hn;
+                    more = true;
+                }
+            }
+            ++j;
+            if (!more) break;
+            if (j < m) {
+                SPFD_CUDA(cudaMemcpyAsync(sc + SMUL, mult, R * sizeof(double), cudaMemcpyHostToDevice, s));
+                k_scale_r<R><<<G, 256, 0, s>>>(n, sc + SMUL, w, Vb + (int64_t)j * n * R);
+                SPFD_LAUNCH_CHECK();
+            }
+        }
+        // least squares per rhs and the update x += Z y
+        std::vector<double> y((size_t)R * m, 0.0);
+        for (int c = 0; c < R; ++c) {
+            const int jj = jc[c];
+            for (int i = jj - 1; i >= 0; --i) {  // back substitution
+                double acc = g[c][i];
+                for (int k = i + 1; k < jj; ++k) acc -= H[c][(size_t)i * m + k] * y[(size_t)c * m + k];
+                y[(size_t)c * m + i] = acc / H[c][(size_t)i * m + i];
+            }
+            for (int i = 0; i < jj; ++i)
+                if (!std::isfinite(y[(size_t)c * m + i])) { rep.status = SPFD_ENONFINITE; rep.iterations = its; return rep; }
+        }
+        SPFD_CUDA(cudaMemcpyAsync(ydev.get(), y.data(), y.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        SPFD_CUDA(cudaMemcpyAsync(jcdev.get(), jc, R * sizeof(int), cudaMemcpyHostToDevice, s));
+        k_combine_r<R><<<G, 256, 0, s>>>(n, m, jcdev.get(), ydev.get(), Zb, x);
+        SPFD_LAUNCH_CHECK();
+    }
+    // true residual at exit (linsolve.py:296-298)
+    level0_apply<R>(h, 1, false, x, b, r, s);
+    dot<R>(h, n, r, r, S_TMP, F_STORE, s);
+    double rr[R];
+    SPFD_CUDA(cudaMemcpyAsync(rr, sc + S_TMP, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    rep.converged = 1;
+    int itmax = 0;
+    for (int c = 0; c < R; ++c) {
+        const double rel = bnorm[c] > 0 ? std::sqrt(rr[c]) / bnorm[c] : 0.0;
+        rep.rel_residual[c] = rel;
+        if (!(rel <= cfg.rel_tol)) rep.converged = 0;
+        itmax = std::max(itmax, its_c[c]);
+    }
+    rep.iterations = itmax;
+    return rep;
+}
+
 // FGMRES(m) for one rhs in R=1 layout (linsolve.py:200-298).
 spfd_report fgmres1(Amg &h, const double *b, double *x, const spfd_config &cfg, double *h_trace, cudaStream_t s) {
     spfd_report rep{};
@@ -2075,6 +2341,9 @@ spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spf
         int64_t n = h.lv[0].nvec;
         if (nrhs == 1) {
             rep = fgmres1(h, b, x, cfg, h_trace, s);
+        } else if (!(getenv("SPFD_FGMRES_BATCH") && std::string(getenv("SPFD_FGMRES_BATCH")) == "0") &&
+                   cfg.restart <= 60) {
+            rep = fgmres_batch<2>(h, b, x, cfg, h_trace, s);
         } else {
             DevBuf<double> b1, x1;
             b1.alloc(n); x1.alloc(n);

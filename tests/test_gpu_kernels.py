@@ -144,3 +144,31 @@ def test_pcg_graph_max_iters_and_restart():
             assert rep.iterations == 3 and not rep.converged
         finally:
             _set_graph(-1)
+
+
+@pytest.mark.parametrize("case", golden_cases("model"))
+def test_fgmres_batched_pair_matches_single(case):
+    """FGMRES on a rhs pair (one Arnoldi process, batched V-cycle/SpMV, CGS2
+    block orthogonalisation) against two single-rhs solves (the reference's
+    MGS): iteration counts within one, potentials within 1e-9, both true
+    residuals met, trace per rhs."""
+    import io
+    import paper_2010_12879_b200 as p
+    d = load_golden(case)
+    cfg = p.SolveConfig(rel_tol=1e-12, method="fgmres")
+    system, h = _hier(golden_model(d), float(d["freq"]), d["a"], cfg)
+    if not np.any(system.rhs):
+        pytest.skip("zero rhs")
+    b = np.stack([system.rhs, 0.25 * system.rhs[::-1].copy()])
+    tr = io.StringIO()
+    cfg_t = p.SolveConfig(rel_tol=1e-12, method="fgmres", trace=tr)
+    x2, rep2 = p.solve(system.matrix, b, h, cfg_t)
+    assert rep2.converged and rep2.rel_residual <= 1e-12
+    assert tr.getvalue().count("iter") == rep2.iterations
+    its = []
+    for c in range(2):
+        x1, rep1 = p.solve(system.matrix, b[c], h, cfg)
+        assert rep1.converged
+        its.append(rep1.iterations)
+        assert np.linalg.norm(x2[c] - x1) <= 1e-9 * np.linalg.norm(x1)
+    assert abs(rep2.iterations - max(its)) <= 1
