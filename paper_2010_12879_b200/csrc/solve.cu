@@ -1938,6 +1938,37 @@ __global__ void __launch_bounds__(256) k_mdot(int64_t n, const double *Vb, int i
         for (int k = 0; k < NI * R; ++k) partials[(int64_t)blockIdx.x * NI * R + k] = acc[k];
 }
 
+// Dual block dot: for k < ni, <V_{i0+k}, w> and <V_{i0+k}, v> (v = the
+// newest basis vector) in one pass over the basis block.  partials layout
+// [cta][2][NI][R].
+template <int R, int NI>
+__global__ void __launch_bounds__(256) k_mdot2(int64_t n, const double *Vb, int i0, int ni, const double *w,
+                                               const double *v, double *partials) {
+    using W = V<R>;
+    __shared__ double red[32 * 2 * NI * R];
+    double acc[2 * NI * R];
+#pragma unroll
+    for (int k = 0; k < 2 * NI * R; ++k) acc[k] = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const typename W::T wv = W::ld(w, p), vv = W::ld(v, p);
+#pragma unroll
+        for (int k = 0; k < NI; ++k) {
+            if (k < ni) {
+                const typename W::T b = W::ld(Vb + (int64_t)(i0 + k) * n * R, p);
+#pragma unroll
+                for (int c = 0; c < R; ++c) {
+                    acc[k * R + c] = fma(W::comp(b, c), W::comp(wv, c), acc[k * R + c]);
+                    acc[(NI + k) * R + c] = fma(W::comp(b, c), W::comp(vv, c), acc[(NI + k) * R + c]);
+                }
+            }
+        }
+    }
+    block_sum<2 * NI * R>(acc, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < 2 * NI * R; ++k) partials[(int64_t)blockIdx.x * 2 * NI * R + k] = acc[k];
+}
+
 // out[k] = sum over CTAs of partials[.][k], k < nv (one block per value, fixed order)
 __global__ void __launch_bounds__(256) k_mfinal(const double *partials, int nblocks, int stride, double *out) {
     __shared__ double red[32];
@@ -2000,7 +2031,7 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
     spfd_report rep{};
     const int64_t n = h.lv[0].nvec;
     const int m = cfg.restart;
-    SPFD_CHECK(m >= 1 && m <= 60, SPFD_EINVAL, "restart must be in [1, 60] for batched FGMRES");
+    SPFD_CHECK(m >= 1 && m <= 31, SPFD_EINVAL, "restart must be in [1, 31] for batched FGMRES");
     if (h.fg_m < m || h.fg_R < R) {
         h.fg_basis.alloc((int64_t)(m + 1) * n * R);
         h.fg_prec.alloc((int64_t)m * n * R);
@@ -2028,8 +2059,9 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
         rep.rel_residual[c] = 0.0;
     }
     if (all) { rep.converged = 1; return rep; }
-    std::vector<double> H[R], cs[R], sn[R], g[R];
+    std::vector<double> H[R], cs[R], sn[R], g[R], Gm[R];
     for (int c = 0; c < R; ++c) {
+        Gm[c].assign((size_t)(m + 1) * (m + 1), 0.0);
         H[c].assign((size_t)(m + 1) * m, 0.0);
         cs[c].assign(m, 0.0); sn[c].assign(m, 0.0); g[c].assign(m + 1, 0.0);
     }
@@ -2057,6 +2089,7 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
             active[c] = !done[c];
             any = any || active[c];
             std::fill(H[c].begin(), H[c].end(), 0.0);
+            std::fill(Gm[c].begin(), Gm[c].end(), 0.0);
             std::fill(g[c].begin(), g[c].end(), 0.0);
             g[c][0] = beta;
             mult[c] = active[c] ? 1.0 / beta : 0.0;
@@ -2071,25 +2104,44 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
             double *vj = Vb + (int64_t)j * n * R, *zj = Zb + (int64_t)j * n * R;
             amg_vcycle(h, vj, zj, R, s);
             level0_apply<R>(h, 0, false, zj, nullptr, w, s);
-            auto cgs = [&](int out) {
-                for (int i0 = 0; i0 <= j; i0 += kMdotNI) {
-                    const int ni = std::min(kMdotNI, j + 1 - i0);
-                    k_mdot<R, kMdotNI><<<nparts, 256, 0, s>>>(n, Vb, i0, ni, w, h.partials.get());
-                    k_mfinal<<<ni * R, 256, 0, s>>>(h.partials.get(), nparts, kMdotNI * R, sc + out + i0 * R);
-                }
-                k_maxpy<R><<<G, 256, 0, s>>>(n, Vb, j + 1, sc + out, w);
+            // Gram-corrected CGS2 (two passes over the basis instead of four):
+            // one dual block dot gives h1 = V^T w and the new Gram column
+            // G[:, j] = V^T v_j; the re-orthogonalisation coefficients follow
+            // on the host, h2 = V^T (w - V h1) = h1 - G h1, and one block
+            // update forms w - V (h1 + h2) -- CGS2 in exact arithmetic.
+            constexpr int NI2 = 4;
+            for (int i0 = 0; i0 <= j; i0 += NI2) {
+                const int ni = std::min(NI2, j + 1 - i0);
+                k_mdot2<R, NI2><<<nparts, 256, 0, s>>>(n, Vb, i0, ni, w, vj, h.partials.get());
+                k_mfinal<<<2 * NI2 * R, 256, 0, s>>>(h.partials.get(), nparts, 2 * NI2 * R, sc + SH1 + 2 * i0 * R);
                 SPFD_LAUNCH_CHECK();
-            };
-            // CGS2: w = A z_j is nearly parallel to v_j (A M^-1 ~ I), so one
-            // classical pass always cancels most of its norm; measured, the
-            // "twice is enough" test re-orthogonalised at every step anyway
-            cgs(SH1);
-            cgs(SH2);
-            dot<R>(h, n, w, w, S_TMP, F_STORE, s);
+            }
+            // SH1 + 2*i0*R + [ (0|NI2)*R + k*R + c ] -> h1 and the Gram column per block
+            std::vector<double> raw((size_t)2 * ((j + NI2) / NI2) * NI2 * R);
+            SPFD_CUDA(cudaMemcpyAsync(raw.data(), sc + SH1, raw.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SPFD_CUDA(cudaStreamSynchronize(s));
             std::vector<double> h1((size_t)(j + 1) * R), h2((size_t)(j + 1) * R);
+            for (int i = 0; i <= j; ++i) {
+                const int blk = i / NI2, k = i % NI2;
+                for (int c = 0; c < R; ++c) {
+                    h1[(size_t)i * R + c] = raw[(size_t)blk * 2 * NI2 * R + k * R + c];
+                    Gm[c][(size_t)i * (m + 1) + j] = Gm[c][(size_t)j * (m + 1) + i] =
+                        raw[(size_t)blk * 2 * NI2 * R + (NI2 + k) * R + c];
+                }
+            }
+            std::vector<double> hsum((size_t)(j + 1) * R);
+            for (int c = 0; c < R; ++c)
+                for (int i = 0; i <= j; ++i) {
+                    double gh = 0.0;
+                    for (int k = 0; k <= j; ++k) gh += Gm[c][(size_t)i * (m + 1) + k] * h1[(size_t)k * R + c];
+                    h2[(size_t)i * R + c] = h1[(size_t)i * R + c] - gh;
+                    hsum[(size_t)i * R + c] = h1[(size_t)i * R + c] + h2[(size_t)i * R + c];
+                }
+            SPFD_CUDA(cudaMemcpyAsync(sc + SH2, hsum.data(), hsum.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+            k_maxpy<R><<<G, 256, 0, s>>>(n, Vb, j + 1, sc + SH2, w);
+            SPFD_LAUNCH_CHECK();
+            dot<R>(h, n, w, w, S_TMP, F_STORE, s);
             double nn[R];
-            SPFD_CUDA(cudaMemcpyAsync(h1.data(), sc + SH1, h1.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-            SPFD_CUDA(cudaMemcpyAsync(h2.data(), sc + SH2, h2.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
             SPFD_CUDA(cudaMemcpyAsync(nn, sc + S_TMP, R * sizeof(double), cudaMemcpyDeviceToHost, s));
             SPFD_CUDA(cudaStreamSynchronize(s));
             ++its;
@@ -2342,7 +2394,7 @@ spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spf
         if (nrhs == 1) {
             rep = fgmres1(h, b, x, cfg, h_trace, s);
         } else if (!(getenv("SPFD_FGMRES_BATCH") && std::string(getenv("SPFD_FGMRES_BATCH")) == "0") &&
-                   cfg.restart <= 60) {
+                   cfg.restart <= 31) {
             rep = fgmres_batch<2>(h, b, x, cfg, h_trace, s);
         } else {
             DevBuf<double> b1, x1;
