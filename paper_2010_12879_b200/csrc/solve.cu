@@ -2391,10 +2391,15 @@ spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spf
                "the distributed solve supports PCG only");
     if (cfg.method == SPFD_METHOD_FGMRES) {
         int64_t n = h.lv[0].nvec;
-        if (nrhs == 1) {
+        // block (Gram-corrected CGS2) Arnoldi unless disabled or the restart
+        // exceeds its scalar workspace; else the reference's MGS per rhs
+        const bool block = !(getenv("SPFD_FGMRES_BATCH") && std::string(getenv("SPFD_FGMRES_BATCH")) == "0") &&
+                           cfg.restart <= 31;
+        if (nrhs == 1 && block) {
+            rep = fgmres_batch<1>(h, b, x, cfg, h_trace, s);
+        } else if (nrhs == 1) {
             rep = fgmres1(h, b, x, cfg, h_trace, s);
-        } else if (!(getenv("SPFD_FGMRES_BATCH") && std::string(getenv("SPFD_FGMRES_BATCH")) == "0") &&
-                   cfg.restart <= 31) {
+        } else if (block) {
             rep = fgmres_batch<2>(h, b, x, cfg, h_trace, s);
         } else {
             DevBuf<double> b1, x1;

@@ -172,3 +172,21 @@ def test_fgmres_batched_pair_matches_single(case):
         its.append(rep1.iterations)
         assert np.linalg.norm(x2[c] - x1) <= 1e-9 * np.linalg.norm(x1)
     assert abs(rep2.iterations - max(its)) <= 1
+
+
+@pytest.mark.parametrize("case", golden_cases("model"))
+def test_fgmres_block_single_rhs_matches_mgs(case, monkeypatch):
+    """Single-rhs FGMRES: the block (Gram-corrected CGS2) Arnoldi against the
+    reference's modified Gram-Schmidt (SPFD_FGMRES_BATCH=0)."""
+    import paper_2010_12879_b200 as p
+    d = load_golden(case)
+    cfg = p.SolveConfig(rel_tol=1e-12, method="fgmres")
+    system, h = _hier(golden_model(d), float(d["freq"]), d["a"], cfg)
+    if not np.any(system.rhs):
+        pytest.skip("zero rhs")
+    xb, rb = p.solve(system.matrix, system.rhs, h, cfg)
+    monkeypatch.setenv("SPFD_FGMRES_BATCH", "0")
+    xm, rm = p.solve(system.matrix, system.rhs, h, cfg)
+    assert rb.converged and rm.converged
+    assert abs(rb.iterations - rm.iterations) <= 1
+    assert np.linalg.norm(xb - xm) <= 1e-9 * np.linalg.norm(xm)

@@ -1,4 +1,5 @@
-"""Time the FGMRES path (the reference's default solver) on C3 against PCG."""
+"""Time the FGMRES path (the reference's default solver) on C3 against PCG:
+rhs pairs through Session.snapshot and a single rhs through fgmres_solve."""
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -18,4 +19,10 @@ for method in ("pcg", "fgmres"):
     torch.cuda.synchronize()
     print(method, "ms per snapshot pair", (time.perf_counter() - t) / n * 1e3, "iterations", rep.iterations,
           "rel", rep.rel_residuals, flush=True)
+    t = time.perf_counter()
+    for _ in range(n):
+        vox, rep, _ = sess.snapshot(a[:1].contiguous())
+    torch.cuda.synchronize()
+    print(method, "ms per single-rhs snapshot", (time.perf_counter() - t) / n * 1e3, "iterations", rep.iterations,
+          flush=True)
     del sess
