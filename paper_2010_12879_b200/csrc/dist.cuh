@@ -63,6 +63,16 @@ struct Dist {
     DevBuf<double> gsend, grecv;           // allgather scratch
     int64_t dof_b = 0, dof_e = 0, vox_b = 0, vox_e = 0;
     int64_t vrow_b = 0, vrow_e = 0;
+    // interior positions [ib, ie): stencil neighbours all owned -> computed on
+    // a side stream while the halo planes travel
+    int64_t ib = 0, ie = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    ~Dist() {
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (side) cudaStreamDestroy(side);
+    }
 };
 
 // ------------------------------------------------------------- kernels --
@@ -386,6 +396,39 @@ static void range_exchange(Dist &D, double *v, int R, cudaStream_t s) {
     c.end(s);
 }
 
+// One fine-level stencil pass over the owned planes with its input's halo
+// exchange overlapped: the interior planes (all neighbours owned) run on the
+// side stream while `xin`'s boundary planes travel, then the two boundary
+// planes.  Partials (DOT) are written contiguously: interior, low, high.
+template <int R, int MODE, bool DOT>
+int launch_fine_ov(Dist &D, const Operator &op, const SpanArgs &sa, double *xin, cudaStream_t s) {
+    static const bool ov = !(getenv("SPFD_HALO_OVERLAP") && std::string(getenv("SPFD_HALO_OVERLAP")) == "0");
+    if (!ov || D.size == 1 || D.ie <= D.ib) {
+        range_exchange(D, xin, R, s);
+        return launch_fine<R, MODE, DOT>(op, sa, s);
+    }
+    SPFD_CUDA(cudaEventRecord(D.ev_fork, s));
+    SPFD_CUDA(cudaStreamWaitEvent(D.side, D.ev_fork, 0));
+    SpanArgs si = sa;
+    si.pb = D.ib;
+    si.pe = D.ie;
+    const int g1 = launch_fine<R, MODE, DOT>(op, si, D.side);
+    range_exchange(D, xin, R, s);
+    SpanArgs sl = sa;
+    sl.pb = D.pb;
+    sl.pe = D.ib;
+    if (sl.partials) sl.partials += (int64_t)g1 * R;
+    const int g2 = D.ib > D.pb ? launch_fine<R, MODE, DOT>(op, sl, s) : 0;
+    SpanArgs sh = sa;
+    sh.pb = D.ie;
+    sh.pe = D.pe;
+    if (sh.partials) sh.partials += (int64_t)(g1 + g2) * R;
+    const int g3 = D.pe > D.ie ? launch_fine<R, MODE, DOT>(op, sh, s) : 0;
+    SPFD_CUDA(cudaEventRecord(D.ev_join, D.side));
+    SPFD_CUDA(cudaStreamWaitEvent(s, D.ev_join, 0));
+    return g1 + g2 + g3;
+}
+
 void amg_distribute_impl(Amg &h, Comm *comm, int64_t replicate_below, int64_t *range, cudaStream_t s) {
     SPFD_CHECK(h.structured, SPFD_EINVAL, "distribution needs an operator (structured) hierarchy");
     SPFD_CHECK(h.pre <= 1 && h.post == 1, SPFD_EINVAL, "distributed V-cycle supports pre_sweeps <= 1, post_sweeps == 1");
@@ -426,6 +469,11 @@ void amg_distribute_impl(Amg &h, Comm *comm, int64_t replicate_below, int64_t *r
         auto plane = [&](int k, int64_t *r2) { r2[0] = D->plane_pos[k]; r2[1] = D->plane_pos[k + 1]; };
         if (me > 0) { plane(D->kb, D->lo_send); plane(D->kb - 1, D->lo_recv); }
         if (me < size - 1) { plane(D->ke - 1, D->hi_send); plane(D->ke, D->hi_recv); }
+        D->ib = D->plane_pos[D->kb + (me > 0 ? 1 : 0)];
+        D->ie = D->plane_pos[D->ke - (me < size - 1 ? 1 : 0)];
+        SPFD_CUDA(cudaStreamCreateWithFlags(&D->side, cudaStreamNonBlocking));
+        SPFD_CUDA(cudaEventCreateWithFlags(&D->ev_fork, cudaEventDisableTiming));
+        SPFD_CUDA(cudaEventCreateWithFlags(&D->ev_join, cudaEventDisableTiming));
         // DOF and voxel ranges owned (outputs)
         {
             DevBuf<int64_t> cnt;
@@ -614,13 +662,11 @@ int vcycle_dist_fine(Amg &h, double *r, double *z, cudaStream_t s) {
     SpanArgs sa{nullptr, r, od, nullptr, nullptr, nullptr, d, nullptr};
     sa.pb = D.pb;
     sa.pe = D.pe;
-    range_exchange(D, r, R, s);
-    launch_fine<R, 2, false>(op, sa, s);                 // d = r - A(od r)
-    range_exchange(D, d, R, s);
+    launch_fine_ov<R, 2, false>(D, op, sa, r, s);        // d = r - A(od r)
     SpanArgs sb = sa;
     sb.r = d;
     sb.y = u;
-    launch_fine<R, 2, false>(op, sb, s);                 // u = d - A(od d)
+    launch_fine_ov<R, 2, false>(D, op, sb, d, s);        // u = d - A(od d)
     const bool x0 = nl > 2;
     if (D.l1_dist) {
         list_exchange(*D.comm, D.hu, u, R, s);
@@ -641,11 +687,10 @@ int vcycle_dist_fine(Amg &h, double *r, double *z, cudaStream_t s) {
     sc.pb = D.pb;
     sc.pe = D.pe;
     launch_fine<R, 4, false>(op, sc, s);                 // x1 = od r + e - od A e
-    range_exchange(D, d, R, s);
     SpanArgs sd{d, r, od, nullptr, nullptr, nullptr, z, h.partials.get()};
     sd.pb = D.pb;
     sd.pe = D.pe;
-    return launch_fine<R, 3, true>(op, sd, s);           // z = x1 + od (r - A x1), r.z partials
+    return launch_fine_ov<R, 3, true>(D, op, sd, d, s);  // z = x1 + od (r - A x1), r.z partials
 }
 
 // ------------------------------------------------------------- PCG --
@@ -673,12 +718,12 @@ template <int R>
 int apply_dist(Amg &h, int mode, bool dot, double *x, const double *r, double *y, cudaStream_t s) {
     Dist &D = *h.dist;
     const Operator &op = *h.op;
-    range_exchange(D, x, R, s);
     SpanArgs sa{x, r, h.lv[0].odinv.get(), nullptr, nullptr, nullptr, y, h.partials.get()};
     sa.pb = D.pb;
     sa.pe = D.pe;
-    if (mode == 0) return dot ? launch_fine<R, 0, true>(op, sa, s) : launch_fine<R, 0, false>(op, sa, s);
-    return dot ? launch_fine<R, 1, true>(op, sa, s) : launch_fine<R, 1, false>(op, sa, s);
+    if (mode == 0)
+        return dot ? launch_fine_ov<R, 0, true>(D, op, sa, x, s) : launch_fine_ov<R, 0, false>(D, op, sa, x, s);
+    return dot ? launch_fine_ov<R, 1, true>(D, op, sa, x, s) : launch_fine_ov<R, 1, false>(D, op, sa, x, s);
 }
 
 template <int R>
