@@ -88,7 +88,7 @@ class Session:
     def voxel_indices(self):
         return self.op.export(_lib.EXPORT_VOXEL_INDICES)
 
-    def snapshot(self, a, keep_psi: bool = False, stream=None):
+    def snapshot(self, a, keep_psi: bool = False, stream=None, vox_out=None):
         """One snapshot from device-resident edge potentials `a`
         ((nrhs, n_edges) CUDA float64).  Returns (voxel |E| (nrhs, n_vox)
         CUDA tensor, SolveReport, psi or None)."""
@@ -103,10 +103,15 @@ class Session:
         if self._vox is None or self._vox.shape[0] != nrhs:
             self._vox = torch.empty((nrhs, max(self.op.n_cond_voxels, 1)), dtype=torch.float64, device="cuda")
             self._psi = torch.empty((nrhs, max(self.op.n_dofs, 1)), dtype=torch.float64, device="cuda")
+        vbuf = self._vox
+        if vox_out is not None:
+            if vox_out.shape != self._vox.shape or not vox_out.is_cuda or vox_out.dtype != torch.float64:
+                raise ValueError("vox_out must be a CUDA float64 tensor shaped like the voxel field buffer")
+            vbuf = vox_out
         rep = _lib.Report()
         _lib.check(_lib.load().spfd_snapshot(self.op.handle, self.hierarchy.handle, _lib.ptr(a), self.omega,
                                              _lib.ptr(self._psi) if keep_psi else ctypes.c_void_p(0),
-                                             _lib.ptr(self._vox), nrhs, ctypes.byref(self._c), ctypes.byref(rep),
+                                             _lib.ptr(vbuf), nrhs, ctypes.byref(self._c), ctypes.byref(rep),
                                              _lib.stream_ptr(stream)))
         rels = tuple(float(rep.rel_residual[k]) for k in range(nrhs))
         report = SolveReport(iterations=int(rep.iterations), rel_residual=max(rels), converged=bool(rep.converged),
@@ -117,7 +122,7 @@ class Session:
         if not report.converged:
             raise PipelineError("solve", f"solver did not converge: residual {report.rel_residual:.3e} "
                                          f"after {report.iterations} iterations")
-        vox = self._vox[:, :self.op.n_cond_voxels]
+        vox = vbuf[:, :self.op.n_cond_voxels]
         psi = self._psi[:, :self.op.n_dofs] if keep_psi else None
         return vox, report, psi
 
@@ -143,6 +148,70 @@ class Session:
         out.copy_(vox[:, v0:v1], non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return out.numpy(), rep
+
+    def snapshots_host(self, inputs, outs=None):
+        """A stream of snapshots from host memory (the real-time use case,
+        BASELINE config C5), pipelined: the H2D copy of snapshot i+1 and the
+        D2H copy of result i-1 run on copy streams while snapshot i solves.
+        Every snapshot's potentials are copied in and its voxel field copied
+        out.  `inputs`: sequence of (preferably pinned) CPU tensors (nrhs,
+        n_edges); `outs`: optional sequence of pinned CPU tensors (nrhs,
+        n_vox of this rank).  Returns (outs, reports)."""
+        inputs = [a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+                  for a in inputs]
+        inputs = [a.reshape(1, -1) if a.dim() == 1 else a for a in inputs]
+        if not inputs:
+            return [], []
+        shape = tuple(inputs[0].shape)
+        if any(tuple(a.shape) != shape for a in inputs):
+            raise ValueError("all snapshots of a stream must have the same shape")
+        v0, v1 = self.vox_range
+        nrhs = shape[0]
+        if outs is None:
+            outs = [torch.empty((nrhs, v1 - v0), dtype=torch.float64, pin_memory=True) for _ in inputs]
+        if self._vox is None or self._vox.shape[0] != nrhs:
+            self._vox = torch.empty((nrhs, max(self.op.n_cond_voxels, 1)), dtype=torch.float64, device="cuda")
+            self._psi = torch.empty((nrhs, max(self.op.n_dofs, 1)), dtype=torch.float64, device="cuda")
+        if getattr(self, "_stream_bufs", None) is None or self._stream_bufs[0].shape != shape:
+            self._stream_bufs = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(2)]
+            self._stream_vox = [torch.empty_like(self._vox) for _ in range(2)]
+            self._h2d_stream = torch.cuda.Stream()
+            self._d2h_stream = torch.cuda.Stream()
+        bufs, voxb = self._stream_bufs, self._stream_vox
+        hs, ds = self._h2d_stream, self._d2h_stream
+        compute = torch.cuda.current_stream()
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [None, None]
+        slices = self.edge_slices()
+
+        def h2d(i):
+            b = i % 2
+            with torch.cuda.stream(hs):
+                hs.wait_stream(compute)          # buffer b's previous snapshot is done with it
+                for e0, e1 in slices:
+                    for c in range(nrhs):
+                        bufs[b][c, e0:e1].copy_(inputs[i][c, e0:e1], non_blocking=inputs[i].is_pinned())
+                ev_in[b].record(hs)
+
+        reports = []
+        h2d(0)
+        for i in range(len(inputs)):
+            b = i % 2
+            if i + 1 < len(inputs):
+                h2d(i + 1)
+            compute.wait_event(ev_in[b])
+            if ev_out[b] is not None:
+                compute.wait_event(ev_out[b])    # result i-2 has left voxb[b]
+            _, rep, _ = self.snapshot(bufs[b], vox_out=voxb[b])
+            reports.append(rep)
+            with torch.cuda.stream(ds):
+                ds.wait_stream(compute)
+                outs[i].copy_(voxb[b][:, v0:v1], non_blocking=True)
+                ev_out[b] = torch.cuda.Event()
+                ev_out[b].record(ds)
+        ds.synchronize()
+        hs.synchronize()
+        return outs, reports
 
     def host_bytes(self, nrhs: int):
         """(H2D, D2H) bytes per snapshot_host call on this rank."""

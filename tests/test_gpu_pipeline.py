@@ -104,3 +104,23 @@ def test_snapshot_host_matches_device(case):
     assert np.array_equal(vox_h, vox_d)
     h2d, _ = sess.host_bytes(a.shape[0])
     assert h2d <= a.size * 8
+
+
+def test_snapshots_host_stream_matches_single_snapshots():
+    """The pipelined host stream (copy-in of i+1 and copy-out of i-1 overlap
+    the solve of i) returns, per snapshot, exactly the device snapshot's
+    voxel field (different inputs, odd count, double-buffer reuse)."""
+    import torch
+    from paper_2010_12879_b200 import Session, SolveConfig, workloads
+    w = workloads.c1(20)
+    sess = Session(w.model, w.frequency_hz, SolveConfig(rel_tol=1e-10))
+    ins = [torch.from_numpy(np.ascontiguousarray(w.a * s)).pin_memory() for s in (1.0, -0.5, 2.0, 0.25, 3.0)]
+    ref = []
+    for a in ins:
+        vox, rep, _ = sess.snapshot(a.cuda())
+        ref.append((vox.cpu().numpy().copy(), rep.iterations))
+    outs, reps = sess.snapshots_host(ins)
+    assert len(outs) == len(ins) == len(reps)
+    for (v, its), o, r in zip(ref, outs, reps):
+        assert r.iterations == its
+        assert np.array_equal(o.numpy(), v)
