@@ -65,6 +65,7 @@ struct Amg {
     DevBuf<double> fg_basis, fg_prec;  // FGMRES basis (allocated on demand)
     int64_t fg_m = 0;
     int fg_R = 1;             // rhs count the FGMRES basis was sized for
+    std::vector<int32_t> l1_perm;  // solve-layout level-1 index -> reference index (empty = identity)
     int vc_partials = 0;      // r.z partials written by the last V-cycle (0 = none)
     Dist *dist = nullptr;     // set by amg_distribute (owned)
     cudaStream_t side = nullptr;            // PCG x-update overlap stream
@@ -96,6 +97,7 @@ void amg_to_level0(Amg &h, const double *planar, double *inter, int nrhs, cudaSt
 void amg_from_level0(Amg &h, const double *inter, double *planar, int nrhs, cudaStream_t s);
 
 int csr_group(int64_t nnz, int64_t rows);  // lanes per row of the CSR kernels
+void level1_unpermute(Amg &h, cudaStream_t s);  // reference level-1 numbering (amg_setup.cu)
 void amg_distribute(Amg &h, Comm *comm, int64_t replicate_below, int64_t *range, cudaStream_t s);
 void dist_range_exchange(Amg &h, double *v, int nrhs, cudaStream_t s);
 void dist_info(const Amg &h, int64_t *out);  // pb, pe, voxel-row begin, end

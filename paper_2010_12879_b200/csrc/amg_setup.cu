@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <chrono>
+#include <algorithm>
 #include <cstdlib>
 
 #include "amg.cuh"
@@ -786,6 +787,156 @@ int64_t Amg::device_bytes() const {
 
 void alloc_krylov(Amg &h, int64_t nvec0, int max_nrhs);
 
+// ---- experiment: Morton renumbering of level 1 (SPFD_MORTON=1) -----------
+// Level-1 unknowns (aggregates) renumbered along a Morton curve of their
+// root nodes; every level-1 structure the single-GPU V-cycle uses is
+// permuted consistently, keeping each row's entry order, so the V-cycle
+// computes the same sums in the same order (same bits).
+template <class T>
+static std::vector<T> d2h(const DevBuf<T> &b, size_t n) {
+    std::vector<T> v(n);
+    if (n) SPFD_CUDA(cudaMemcpy(v.data(), b.get(), n * sizeof(T), cudaMemcpyDeviceToHost));
+    return v;
+}
+template <class T>
+static void h2d(DevBuf<T> &b, const std::vector<T> &v) {
+    if (b.n < v.size()) b.alloc(v.size());
+    if (!v.empty()) SPFD_CUDA(cudaMemcpy(b.get(), v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+static uint64_t morton3(uint32_t x, uint32_t y, uint32_t z) {
+    auto spread = [](uint64_t v) {
+        v &= 0x1fffff;
+        v = (v | v << 32) & 0x1f00000000ffffull;
+        v = (v | v << 16) & 0x1f0000ff0000ffull;
+        v = (v | v << 8) & 0x100f00f00f00f00full;
+        v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+        v = (v | v << 2) & 0x1249249249249249ull;
+        return v;
+    };
+    return spread(x) | spread(y) << 1 | spread(z) << 2;
+}
+static void permute_csr_rows_cols(Csr &m, const std::vector<int32_t> *perm_rows, const std::vector<int32_t> *inv_cols) {
+    auto ptr = d2h(m.ptr, m.rows + 1);
+    auto col = d2h(m.col, m.nnz);
+    auto val = d2h(m.val, m.nnz);
+    std::vector<int64_t> np(m.rows + 1, 0);
+    std::vector<int32_t> nc(m.nnz);
+    std::vector<double> nv(m.nnz);
+    for (int64_t r = 0; r < m.rows; ++r) {
+        const int64_t o = perm_rows ? (*perm_rows)[r] : r;
+        np[r + 1] = np[r] + (ptr[o + 1] - ptr[o]);
+        for (int64_t q = ptr[o], t = np[r]; q < ptr[o + 1]; ++q, ++t) {
+            nc[t] = inv_cols ? (*inv_cols)[col[q]] : col[q];
+            nv[t] = val[q];
+        }
+    }
+    h2d(m.ptr, np);
+    h2d(m.col, nc);
+    h2d(m.val, nv);
+}
+// Apply a renumbering of the level-1 unknowns (P: new index -> current
+// index) to every structure the single-GPU V-cycle reads; h.l1_perm keeps
+// new -> reference index (empty = reference numbering).
+void level1_permute(Amg &h, const std::vector<int32_t> &P, cudaStream_t s) {
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    Level &L0 = h.lv[0], &L1 = h.lv[1];
+    const int64_t n1 = L1.n;
+    std::vector<int32_t> inv(n1);
+    for (int64_t g = 0; g < n1; ++g) inv[P[g]] = (int32_t)g;
+    permute_csr_rows_cols(L1.A, &P, &inv);
+    if (L1.AP.rows) permute_csr_rows_cols(L1.AP, &P, nullptr);
+    permute_csr_rows_cols(L1.P, &P, nullptr);
+    permute_csr_rows_cols(L1.R, nullptr, &inv);
+    for (DevBuf<double> *b : {&L1.odinv, &L1.dinv}) {
+        auto v = d2h(*b, b->n);
+        std::vector<double> nv(v);
+        for (int64_t g = 0; g < n1; ++g) nv[g] = v[P[g]];
+        h2d(*b, nv);
+    }
+    auto ap = d2h(L0.agg_pos, L0.agg_pos.n);
+    for (int64_t p = 0; p < L0.nvec; ++p)
+        if (ap[p] > 0) ap[p] = inv[ap[p] - 1] + 1;
+    h2d(L0.agg_pos, ap);
+    auto mptr = d2h(L0.mem_ptr, n1 + 1);
+    auto mpos = d2h(L0.mem_pos, (size_t)mptr[n1]);
+    std::vector<int64_t> nptr(n1 + 1, 0);
+    std::vector<int32_t> npos(mpos.size());
+    for (int64_t g = 0; g < n1; ++g) {
+        const int64_t o = P[g];
+        nptr[g + 1] = nptr[g] + (mptr[o + 1] - mptr[o]);
+        std::copy(mpos.begin() + mptr[o], mpos.begin() + mptr[o + 1], npos.begin() + nptr[g]);
+    }
+    h2d(L0.mem_ptr, nptr);
+    h2d(L0.mem_pos, npos);
+    std::vector<int32_t> comp(n1);
+    for (int64_t g = 0; g < n1; ++g) comp[g] = h.l1_perm.empty() ? P[g] : h.l1_perm[P[g]];
+    bool ident = true;
+    for (int64_t g = 0; g < n1 && ident; ++g) ident = comp[g] == g;
+    if (ident) h.l1_perm.clear();
+    else h.l1_perm = std::move(comp);
+}
+
+// back to the reference numbering (before distributing the hierarchy)
+void level1_unpermute(Amg &h, cudaStream_t s) {
+    if (h.l1_perm.empty()) return;
+    const int64_t n1 = h.lv[1].n;
+    std::vector<int32_t> Q(n1);
+    for (int64_t g = 0; g < n1; ++g) Q[h.l1_perm[g]] = (int32_t)g;  // reference index -> current index
+    level1_permute(h, Q, s);
+}
+
+// Morton order of the level-1 aggregates' root nodes
+static void morton_level1(Amg &h, cudaStream_t s) {
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    Level &L0 = h.lv[0], &L1 = h.lv[1];
+    const Operator &op = *h.op;
+    const int64_t n1 = L1.n;
+    auto mptr = d2h(L0.mem_ptr, n1 + 1);
+    auto mpos = d2h(L0.mem_pos, (size_t)mptr[n1]);
+    auto rows = d2h(op.rows, op.n_rows + 1);
+    std::vector<int> rowof(op.L);
+    for (int64_t r = 0; r < op.n_rows; ++r)
+        for (int p = rows[r].x; p < rows[r].x + (rows[r].z - rows[r].y); ++p) rowof[p] = (int)r;
+    std::vector<uint64_t> key(n1);
+    for (int64_t g = 0; g < n1; ++g) {
+        const int p = mpos[mptr[g]];  // root: the aggregate's first member
+        const int r = rowof[p];
+        const int i = rows[r].y + (p - rows[r].x), j = r % (int)op.NY, k = r / (int)op.NY;
+        key[g] = morton3(i, j, k);
+    }
+    std::vector<int32_t> P(n1);
+    for (int64_t g = 0; g < n1; ++g) P[g] = (int32_t)g;
+    std::stable_sort(P.begin(), P.end(), [&](int a, int b) { return key[a] < key[b]; });
+    level1_permute(h, P, s);
+}
+
+// level-1 CSR in the reference numbering into caller buffers (exports)
+static void export_level1(const Amg &h, const Csr &m, bool rows_perm, bool cols_perm, int64_t *ptr, int32_t *col,
+                          double *val) {
+    const auto &perm = h.l1_perm;  // current -> reference
+    std::vector<int32_t> inv(perm.size());
+    for (size_t g = 0; g < perm.size(); ++g) inv[perm[g]] = (int32_t)g;
+    auto hp = d2h(m.ptr, m.rows + 1);
+    auto hc = d2h(m.col, m.nnz);
+    auto hv = d2h(m.val, m.nnz);
+    std::vector<int64_t> np(m.rows + 1, 0);
+    std::vector<int32_t> nc(m.nnz);
+    std::vector<double> nv(m.nnz);
+    for (int64_t o = 0; o < m.rows; ++o) {
+        const int64_t r = rows_perm ? inv[o] : o;
+        np[o + 1] = np[o] + (hp[r + 1] - hp[r]);
+        for (int64_t q = hp[r], t = np[o]; q < hp[r + 1]; ++q, ++t) {
+            nc[t] = cols_perm ? perm[hc[q]] : hc[q];
+            nv[t] = hv[q];
+        }
+    }
+    SPFD_CUDA(cudaMemcpy(ptr, np.data(), np.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (m.nnz) {
+        SPFD_CUDA(cudaMemcpy(col, nc.data(), nc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        SPFD_CUDA(cudaMemcpy(val, nv.data(), nv.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+}
+
 static void finish_level(Level &L, const Csr &A, double omega, cudaStream_t s) {
     const int T = 256;
     L.dinv.alloc(L.nvec);
@@ -911,6 +1062,11 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
             // single-level structured hierarchy: keep the DOF CSR
         }
     }
+    // solve layout: level 1 in Morton order of the aggregate roots (gathers of
+    // neighbouring aggregates share cache lines); exports and the distributed
+    // path see the reference numbering (export_level1, level1_unpermute)
+    if (!(getenv("SPFD_MORTON") && std::string(getenv("SPFD_MORTON")) == "0") && h->structured && nl > 2)
+        morton_level1(*h, s);
     alloc_krylov(*h, h->lv[0].nvec, R);
     SPFD_CUDA(cudaEventRecord(e1, s));
     SPFD_CUDA(cudaEventSynchronize(e1));
@@ -989,6 +1145,11 @@ void amg_level_csr(Amg &h, int level, int which, int64_t *ptr, int32_t *col, dou
         m = (level == 0 && h.structured) ? &L.R_dof : &L.R;
     }
     SPFD_CHECK(m != nullptr && m->rows > 0, SPFD_EINVAL, "no such matrix on this level");
+    if (level == 1 && !h.l1_perm.empty()) {  // solve layout is renumbered: export the reference order
+        SPFD_CUDA(cudaStreamSynchronize(s));
+        export_level1(h, *m, which != 2, which != 1, ptr, col, val);
+        return;
+    }
     SPFD_CUDA(cudaMemcpyAsync(ptr, m->ptr.get(), (m->rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
     if (m->nnz) {
         SPFD_CUDA(cudaMemcpyAsync(col, m->col.get(), m->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));

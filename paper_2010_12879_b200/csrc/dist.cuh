@@ -431,6 +431,7 @@ int launch_fine_ov(Dist &D, const Operator &op, const SpanArgs &sa, double *xin,
 
 void amg_distribute_impl(Amg &h, Comm *comm, int64_t replicate_below, int64_t *range, cudaStream_t s) {
     SPFD_CHECK(h.structured, SPFD_EINVAL, "distribution needs an operator (structured) hierarchy");
+    level1_unpermute(h, s);  // the slab decomposition works in the reference numbering
     SPFD_CHECK(h.pre <= 1 && h.post == 1, SPFD_EINVAL, "distributed V-cycle supports pre_sweeps <= 1, post_sweeps == 1");
     SPFD_CHECK(fine_kernel_kind() == 2, SPFD_EINVAL, "distributed solve needs the flat span kernel");
     const int T = 256;

@@ -190,3 +190,34 @@ def test_fgmres_block_single_rhs_matches_mgs(case, monkeypatch):
     assert rb.converged and rm.converged
     assert abs(rb.iterations - rm.iterations) <= 1
     assert np.linalg.norm(xb - xm) <= 1e-9 * np.linalg.norm(xm)
+
+
+def test_level1_morton_renumbering_is_bitwise_neutral(monkeypatch, rng):
+    """The solve layout renumbers level 1 along a Morton curve (rows and
+    columns permuted, each row's entry order kept): V-cycle and PCG give the
+    same bits as the reference numbering (SPFD_MORTON=0), and the exported
+    level-1 matrices are the reference's."""
+    import paper_2010_12879_b200 as p
+    from paper_2010_12879_b200 import workloads
+    w = workloads.c1(40)
+    grid = p.StaggeredGrid.from_model(w.model)
+    system = p.assemble_poisson(w.model, grid, w.a[0], w.frequency_hz)
+    cfg = p.SolveConfig(rel_tol=1e-10)
+    r = rng.standard_normal((2, system.matrix.shape[0]))
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SPFD_MORTON", flag)
+        h = p.amg_setup(system.matrix, cfg)
+        assert h.n_levels >= 3
+        z = p.v_cycle(h, r)
+        x, rep = p.solve(system.matrix, system.rhs, h, cfg)
+        lv = h.levels[1]
+        out.append((z, x, rep.iterations, lv.matrix.toarray() if lv.matrix.shape[0] < 4000 else lv.matrix,
+                    lv.prolongation, lv.restriction))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1]) and out[0][2] == out[1][2]
+    for k in (4, 5):
+        a, b = out[0][k], out[1][k]
+        assert (a != b).nnz == 0
+    a, b = out[0][3], out[1][3]
+    assert np.array_equal(a, b) if isinstance(a, np.ndarray) else (a != b).nnz == 0
