@@ -787,23 +787,18 @@ int64_t Amg::device_bytes() const {
 
 void alloc_krylov(Amg &h, int64_t nvec0, int max_nrhs);
 
-// ---- experiment: Morton renumbering of level 1 (SPFD_MORTON=1) -----------
+// ---- level-1 renumbering (solve layout) ------------------------------------
 // Level-1 unknowns (aggregates) renumbered along a Morton curve of their
 // root nodes; every level-1 structure the single-GPU V-cycle uses is
-// permuted consistently, keeping each row's entry order, so the V-cycle
-// computes the same sums in the same order (same bits).
+// permuted consistently on the device, keeping each row's entry order, so
+// the V-cycle computes the same sums in the same order (same bits).
 template <class T>
 static std::vector<T> d2h(const DevBuf<T> &b, size_t n) {
     std::vector<T> v(n);
     if (n) SPFD_CUDA(cudaMemcpy(v.data(), b.get(), n * sizeof(T), cudaMemcpyDeviceToHost));
     return v;
 }
-template <class T>
-static void h2d(DevBuf<T> &b, const std::vector<T> &v) {
-    if (b.n < v.size()) b.alloc(v.size());
-    if (!v.empty()) SPFD_CUDA(cudaMemcpy(b.get(), v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-}
-static uint64_t morton3(uint32_t x, uint32_t y, uint32_t z) {
+__host__ __device__ inline uint64_t morton3(uint32_t x, uint32_t y, uint32_t z) {
     auto spread = [](uint64_t v) {
         v &= 0x1fffff;
         v = (v | v << 32) & 0x1f00000000ffffull;
@@ -815,63 +810,127 @@ static uint64_t morton3(uint32_t x, uint32_t y, uint32_t z) {
     };
     return spread(x) | spread(y) << 1 | spread(z) << 2;
 }
-static void permute_csr_rows_cols(Csr &m, const std::vector<int32_t> *perm_rows, const std::vector<int32_t> *inv_cols) {
-    auto ptr = d2h(m.ptr, m.rows + 1);
-    auto col = d2h(m.col, m.nnz);
-    auto val = d2h(m.val, m.nnz);
-    std::vector<int64_t> np(m.rows + 1, 0);
-    std::vector<int32_t> nc(m.nnz);
-    std::vector<double> nv(m.nnz);
-    for (int64_t r = 0; r < m.rows; ++r) {
-        const int64_t o = perm_rows ? (*perm_rows)[r] : r;
-        np[r + 1] = np[r] + (ptr[o + 1] - ptr[o]);
-        for (int64_t q = ptr[o], t = np[r]; q < ptr[o + 1]; ++q, ++t) {
-            nc[t] = inv_cols ? (*inv_cols)[col[q]] : col[q];
-            nv[t] = val[q];
+__global__ void k_perm_len(const int64_t *ptr, const int32_t *P, int64_t n, int64_t *len) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o = P ? P[r] : r;
+        len[r] = ptr[o + 1] - ptr[o];
+    }
+}
+// new row r = old row P[r] (entry order kept), columns relabelled by cmap
+__global__ void k_perm_rows(const int64_t *ptr, const int32_t *col, const double *val, const int32_t *P,
+                            const int32_t *cmap, const int64_t *nptr, int64_t n, int32_t *ncol, double *nval) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = warp; r < n; r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t o = P ? P[r] : r;
+        const int64_t b = ptr[o], e = ptr[o + 1], t0 = nptr[r];
+        for (int64_t q = b + lane; q < e; q += 32) {
+            const int32_t c = col[q];
+            ncol[t0 + (q - b)] = cmap ? cmap[c] : c;
+            if (val) nval[t0 + (q - b)] = val[q];
         }
     }
-    h2d(m.ptr, np);
-    h2d(m.col, nc);
-    h2d(m.val, nv);
 }
+__global__ void k_gather_d(const double *x, const int32_t *P, int64_t n, double *y) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        y[r] = x[P[r]];
+}
+__global__ void k_inv_perm(const int32_t *P, int64_t n, int32_t *inv) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        inv[P[r]] = (int32_t)r;
+}
+__global__ void k_relabel_aggpos(int32_t *ap, int64_t n, const int32_t *inv) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+        if (ap[p] > 0) ap[p] = inv[ap[p] - 1] + 1;
+}
+__global__ void k_root_keys(const int64_t *mptr, const int32_t *mpos, int64_t n1, const int4 *rows, int64_t n_rows,
+                            int NY, uint64_t *key, int32_t *idx) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n1; g += (int64_t)gridDim.x * blockDim.x) {
+        const int p = mpos[mptr[g]];  // root: the aggregate's first member
+        int lo = 0, hi = (int)n_rows - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (rows[mid].x <= p) lo = mid; else hi = mid - 1;
+        }
+        const int4 q = rows[lo];
+        key[g] = morton3((uint32_t)(q.y + (p - q.x)), (uint32_t)(lo % NY), (uint32_t)(lo / NY));
+        idx[g] = (int32_t)g;
+    }
+}
+
+// permute rows (P: new -> old, device) and relabel columns (cmap, device) of a CSR in place
+static void perm_csr(Csr &m, const int32_t *P, const int32_t *cmap, cudaStream_t s) {
+    const int T = 256;
+    DevBuf<int64_t> len, nptr;
+    len.alloc(m.rows + 1);
+    nptr.alloc(m.rows + 1);
+    SPFD_CUDA(cudaMemsetAsync(len.get() + m.rows, 0, sizeof(int64_t), s));
+    k_perm_len<<<grid_for(m.rows, T), T, 0, s>>>(m.ptr.get(), P, m.rows, len.get());
+    SPFD_LAUNCH_CHECK();
+    scan_excl(len.get(), nptr.get(), m.rows + 1, s);
+    DevBuf<int32_t> ncol;
+    DevBuf<double> nval;
+    ncol.alloc(m.nnz);
+    nval.alloc(m.nnz);
+    k_perm_rows<<<grid_for(m.rows * 32, T), T, 0, s>>>(m.ptr.get(), m.col.get(), m.val.get(), P, cmap, nptr.get(),
+                                                       m.rows, ncol.get(), nval.get());
+    SPFD_LAUNCH_CHECK();
+    m.ptr = std::move(nptr);
+    m.col = std::move(ncol);
+    m.val = std::move(nval);
+}
+
 // Apply a renumbering of the level-1 unknowns (P: new index -> current
-// index) to every structure the single-GPU V-cycle reads; h.l1_perm keeps
-// new -> reference index (empty = reference numbering).
-void level1_permute(Amg &h, const std::vector<int32_t> &P, cudaStream_t s) {
-    SPFD_CUDA(cudaStreamSynchronize(s));
+// index, device array) to every structure the single-GPU V-cycle reads;
+// h.l1_perm keeps new -> reference index (empty = reference numbering).
+void level1_permute(Amg &h, const int32_t *P, cudaStream_t s) {
+    const int T = 256;
     Level &L0 = h.lv[0], &L1 = h.lv[1];
     const int64_t n1 = L1.n;
-    std::vector<int32_t> inv(n1);
-    for (int64_t g = 0; g < n1; ++g) inv[P[g]] = (int32_t)g;
-    permute_csr_rows_cols(L1.A, &P, &inv);
-    if (L1.AP.rows) permute_csr_rows_cols(L1.AP, &P, nullptr);
-    permute_csr_rows_cols(L1.P, &P, nullptr);
-    permute_csr_rows_cols(L1.R, nullptr, &inv);
+    DevBuf<int32_t> inv;
+    inv.alloc(n1);
+    k_inv_perm<<<grid_for(n1, T), T, 0, s>>>(P, n1, inv.get());
+    SPFD_LAUNCH_CHECK();
+    perm_csr(L1.A, P, inv.get(), s);
+    if (L1.AP.rows) perm_csr(L1.AP, P, nullptr, s);
+    perm_csr(L1.P, P, nullptr, s);
+    perm_csr(L1.R, nullptr, inv.get(), s);
     for (DevBuf<double> *b : {&L1.odinv, &L1.dinv}) {
-        auto v = d2h(*b, b->n);
-        std::vector<double> nv(v);
-        for (int64_t g = 0; g < n1; ++g) nv[g] = v[P[g]];
-        h2d(*b, nv);
+        DevBuf<double> nb;
+        nb.alloc(b->n);
+        SPFD_CUDA(cudaMemcpyAsync(nb.get(), b->get(), b->bytes(), cudaMemcpyDeviceToDevice, s));
+        k_gather_d<<<grid_for(n1, T), T, 0, s>>>(b->get(), P, n1, nb.get());
+        SPFD_LAUNCH_CHECK();
+        *b = std::move(nb);
     }
-    auto ap = d2h(L0.agg_pos, L0.agg_pos.n);
-    for (int64_t p = 0; p < L0.nvec; ++p)
-        if (ap[p] > 0) ap[p] = inv[ap[p] - 1] + 1;
-    h2d(L0.agg_pos, ap);
-    auto mptr = d2h(L0.mem_ptr, n1 + 1);
-    auto mpos = d2h(L0.mem_pos, (size_t)mptr[n1]);
-    std::vector<int64_t> nptr(n1 + 1, 0);
-    std::vector<int32_t> npos(mpos.size());
-    for (int64_t g = 0; g < n1; ++g) {
-        const int64_t o = P[g];
-        nptr[g + 1] = nptr[g] + (mptr[o + 1] - mptr[o]);
-        std::copy(mpos.begin() + mptr[o], mpos.begin() + mptr[o + 1], npos.begin() + nptr[g]);
+    k_relabel_aggpos<<<grid_for(L0.nvec, T), T, 0, s>>>(L0.agg_pos.get(), L0.nvec, inv.get());
+    SPFD_LAUNCH_CHECK();
+    {   // member lists: a CSR without values
+        DevBuf<int64_t> len, nptr;
+        len.alloc(n1 + 1);
+        nptr.alloc(n1 + 1);
+        SPFD_CUDA(cudaMemsetAsync(len.get() + n1, 0, sizeof(int64_t), s));
+        k_perm_len<<<grid_for(n1, T), T, 0, s>>>(L0.mem_ptr.get(), P, n1, len.get());
+        SPFD_LAUNCH_CHECK();
+        scan_excl(len.get(), nptr.get(), n1 + 1, s);
+        DevBuf<int32_t> npos;
+        npos.alloc(L0.mem_pos.n);
+        k_perm_rows<<<grid_for(n1 * 32, T), T, 0, s>>>(L0.mem_ptr.get(), L0.mem_pos.get(), nullptr, P, nullptr,
+                                                       nptr.get(), n1, npos.get(), nullptr);
+        SPFD_LAUNCH_CHECK();
+        L0.mem_ptr = std::move(nptr);
+        L0.mem_pos = std::move(npos);
     }
-    h2d(L0.mem_ptr, nptr);
-    h2d(L0.mem_pos, npos);
+    // compose the bookkeeping on the host (n1 ints)
+    std::vector<int32_t> hp(n1);
+    SPFD_CUDA(cudaMemcpyAsync(hp.data(), P, n1 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
     std::vector<int32_t> comp(n1);
-    for (int64_t g = 0; g < n1; ++g) comp[g] = h.l1_perm.empty() ? P[g] : h.l1_perm[P[g]];
     bool ident = true;
-    for (int64_t g = 0; g < n1 && ident; ++g) ident = comp[g] == g;
+    for (int64_t g = 0; g < n1; ++g) {
+        comp[g] = h.l1_perm.empty() ? hp[g] : h.l1_perm[hp[g]];
+        ident = ident && comp[g] == g;
+    }
     if (ident) h.l1_perm.clear();
     else h.l1_perm = std::move(comp);
 }
@@ -882,32 +941,32 @@ void level1_unpermute(Amg &h, cudaStream_t s) {
     const int64_t n1 = h.lv[1].n;
     std::vector<int32_t> Q(n1);
     for (int64_t g = 0; g < n1; ++g) Q[h.l1_perm[g]] = (int32_t)g;  // reference index -> current index
-    level1_permute(h, Q, s);
+    DevBuf<int32_t> dq;
+    dq.alloc(n1);
+    SPFD_CUDA(cudaMemcpyAsync(dq.get(), Q.data(), n1 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    level1_permute(h, dq.get(), s);
 }
 
-// Morton order of the level-1 aggregates' root nodes
+// Morton order of the level-1 aggregates' root nodes (device keys + CUB sort)
 static void morton_level1(Amg &h, cudaStream_t s) {
-    SPFD_CUDA(cudaStreamSynchronize(s));
+    const int T = 256;
     Level &L0 = h.lv[0], &L1 = h.lv[1];
     const Operator &op = *h.op;
     const int64_t n1 = L1.n;
-    auto mptr = d2h(L0.mem_ptr, n1 + 1);
-    auto mpos = d2h(L0.mem_pos, (size_t)mptr[n1]);
-    auto rows = d2h(op.rows, op.n_rows + 1);
-    std::vector<int> rowof(op.L);
-    for (int64_t r = 0; r < op.n_rows; ++r)
-        for (int p = rows[r].x; p < rows[r].x + (rows[r].z - rows[r].y); ++p) rowof[p] = (int)r;
-    std::vector<uint64_t> key(n1);
-    for (int64_t g = 0; g < n1; ++g) {
-        const int p = mpos[mptr[g]];  // root: the aggregate's first member
-        const int r = rowof[p];
-        const int i = rows[r].y + (p - rows[r].x), j = r % (int)op.NY, k = r / (int)op.NY;
-        key[g] = morton3(i, j, k);
-    }
-    std::vector<int32_t> P(n1);
-    for (int64_t g = 0; g < n1; ++g) P[g] = (int32_t)g;
-    std::stable_sort(P.begin(), P.end(), [&](int a, int b) { return key[a] < key[b]; });
-    level1_permute(h, P, s);
+    DevBuf<uint64_t> key, key2;
+    DevBuf<int32_t> idx, P;
+    key.alloc(n1); key2.alloc(n1); idx.alloc(n1); P.alloc(n1);
+    k_root_keys<<<grid_for(n1, T), T, 0, s>>>(L0.mem_ptr.get(), L0.mem_pos.get(), n1, op.rows.get(), op.n_rows,
+                                              (int)op.NY, key.get(), idx.get());
+    SPFD_LAUNCH_CHECK();
+    size_t bytes = 0;
+    SPFD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.get(), key2.get(), idx.get(), P.get(), (int)n1, 0,
+                                              64, s));
+    DevBuf<uint8_t> tmp;
+    tmp.alloc(bytes);
+    SPFD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, key.get(), key2.get(), idx.get(), P.get(), (int)n1, 0,
+                                              64, s));
+    level1_permute(h, P.get(), s);
 }
 
 // level-1 CSR in the reference numbering into caller buffers (exports)
