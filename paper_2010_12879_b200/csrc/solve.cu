@@ -1969,6 +1969,31 @@ __global__ void __launch_bounds__(256) k_mdot2(int64_t n, const double *Vb, int 
         for (int k = 0; k < 2 * NI * R; ++k) partials[(int64_t)blockIdx.x * 2 * NI * R + k] = acc[k];
 }
 
+// Gram-corrected CGS2 coefficients on the device (one block): store the new
+// Gram column G[:, j] from the dual block dot, then hsum = h1 + (h1 - G h1)
+// for every rhs; raw layout as written by k_mfinal per 4-vector block.
+template <int R, int NI2>
+__global__ void k_gram_step(const double *raw, int j, int m, double *gram, double *hsum) {
+    const int nv = j + 1;
+    for (int t = threadIdx.x; t < nv * R; t += blockDim.x) {
+        const int i = t / R, c = t % R, blk = i / NI2, k = i % NI2;
+        const double gij = raw[(size_t)blk * 2 * NI2 * R + (NI2 + k) * R + c];
+        double *G = gram + (size_t)c * (m + 1) * (m + 1);
+        G[(size_t)i * (m + 1) + j] = gij;
+        G[(size_t)j * (m + 1) + i] = gij;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nv * R; t += blockDim.x) {
+        const int i = t / R, c = t % R;
+        const double *G = gram + (size_t)c * (m + 1) * (m + 1);
+        auto h1 = [&](int q) { return raw[(size_t)(q / NI2) * 2 * NI2 * R + (q % NI2) * R + c]; };
+        double gh = 0.0;
+        for (int k = 0; k < nv; ++k) gh += G[(size_t)i * (m + 1) + k] * h1(k);
+        const double a = h1(i);
+        hsum[(size_t)i * R + c] = a + (a - gh);
+    }
+}
+
 // out[k] = sum over CTAs of partials[.][k], k < nv (one block per value, fixed order)
 __global__ void __launch_bounds__(256) k_mfinal(const double *partials, int nblocks, int stride, double *out) {
     __shared__ double red[32];
@@ -2059,9 +2084,10 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
         rep.rel_residual[c] = 0.0;
     }
     if (all) { rep.converged = 1; return rep; }
-    std::vector<double> H[R], cs[R], sn[R], g[R], Gm[R];
+    std::vector<double> H[R], cs[R], sn[R], g[R];
+    DevBuf<double> gram;  // per-rhs Gram matrix of the current cycle's basis
+    gram.alloc((size_t)R * (m + 1) * (m + 1));
     for (int c = 0; c < R; ++c) {
-        Gm[c].assign((size_t)(m + 1) * (m + 1), 0.0);
         H[c].assign((size_t)(m + 1) * m, 0.0);
         cs[c].assign(m, 0.0); sn[c].assign(m, 0.0); g[c].assign(m + 1, 0.0);
     }
@@ -2089,12 +2115,12 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
             active[c] = !done[c];
             any = any || active[c];
             std::fill(H[c].begin(), H[c].end(), 0.0);
-            std::fill(Gm[c].begin(), Gm[c].end(), 0.0);
             std::fill(g[c].begin(), g[c].end(), 0.0);
             g[c][0] = beta;
             mult[c] = active[c] ? 1.0 / beta : 0.0;
         }
         if (!any) break;
+        SPFD_CUDA(cudaMemsetAsync(gram.get(), 0, gram.bytes(), s));
         SPFD_CUDA(cudaMemcpyAsync(sc + SMUL, mult, R * sizeof(double), cudaMemcpyHostToDevice, s));
         k_scale_r<R><<<G, 256, 0, s>>>(n, sc + SMUL, r, Vb);
         int jc[R];
@@ -2116,32 +2142,14 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
                 k_mfinal<<<2 * NI2 * R, 256, 0, s>>>(h.partials.get(), nparts, 2 * NI2 * R, sc + SH1 + 2 * i0 * R);
                 SPFD_LAUNCH_CHECK();
             }
-            // SH1 + 2*i0*R + [ (0|NI2)*R + k*R + c ] -> h1 and the Gram column per block
-            std::vector<double> raw((size_t)2 * ((j + NI2) / NI2) * NI2 * R);
-            SPFD_CUDA(cudaMemcpyAsync(raw.data(), sc + SH1, raw.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-            SPFD_CUDA(cudaStreamSynchronize(s));
-            std::vector<double> h1((size_t)(j + 1) * R), h2((size_t)(j + 1) * R);
-            for (int i = 0; i <= j; ++i) {
-                const int blk = i / NI2, k = i % NI2;
-                for (int c = 0; c < R; ++c) {
-                    h1[(size_t)i * R + c] = raw[(size_t)blk * 2 * NI2 * R + k * R + c];
-                    Gm[c][(size_t)i * (m + 1) + j] = Gm[c][(size_t)j * (m + 1) + i] =
-                        raw[(size_t)blk * 2 * NI2 * R + (NI2 + k) * R + c];
-                }
-            }
-            std::vector<double> hsum((size_t)(j + 1) * R);
-            for (int c = 0; c < R; ++c)
-                for (int i = 0; i <= j; ++i) {
-                    double gh = 0.0;
-                    for (int k = 0; k <= j; ++k) gh += Gm[c][(size_t)i * (m + 1) + k] * h1[(size_t)k * R + c];
-                    h2[(size_t)i * R + c] = h1[(size_t)i * R + c] - gh;
-                    hsum[(size_t)i * R + c] = h1[(size_t)i * R + c] + h2[(size_t)i * R + c];
-                }
-            SPFD_CUDA(cudaMemcpyAsync(sc + SH2, hsum.data(), hsum.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+            // the re-orthogonalisation coefficients and the Gram column on the device
+            k_gram_step<R, NI2><<<1, 256, 0, s>>>(sc + SH1, j, m, gram.get(), sc + SH2);
             k_maxpy<R><<<G, 256, 0, s>>>(n, Vb, j + 1, sc + SH2, w);
             SPFD_LAUNCH_CHECK();
             dot<R>(h, n, w, w, S_TMP, F_STORE, s);
+            std::vector<double> hcol((size_t)(j + 1) * R);
             double nn[R];
+            SPFD_CUDA(cudaMemcpyAsync(hcol.data(), sc + SH2, hcol.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
             SPFD_CUDA(cudaMemcpyAsync(nn, sc + S_TMP, R * sizeof(double), cudaMemcpyDeviceToHost, s));
             SPFD_CUDA(cudaStreamSynchronize(s));
             ++its;
@@ -2152,7 +2160,7 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
                 const double hn = std::sqrt(nn[c]);
                 if (!std::isfinite(hn)) { rep.status = SPFD_ENONFINITE; rep.iterations = its; return rep; }
                 auto &Hc = H[c];
-                for (int i = 0; i <= j; ++i) Hc[(size_t)i * m + j] = h1[(size_t)i * R + c] + h2[(size_t)i * R + c];
+                for (int i = 0; i <= j; ++i) Hc[(size_t)i * m + j] = hcol[(size_t)i * R + c];
                 for (int i = 0; i < j; ++i) {
                     const double t1 = cs[c][i] * Hc[(size_t)i * m + j] + sn[c][i] * Hc[(size_t)(i + 1) * m + j];
                     const double t2 = -sn[c][i] * Hc[(size_t)i * m + j] + cs[c][i] * Hc[(size_t)(i + 1) * m + j];
