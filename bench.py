@@ -13,7 +13,7 @@ as `setup_s`), as in the reference's run_benchmark (pipeline.py:277-288).
 
 `--impl reference` times the reference algorithm on the host CPU (the
 numpy/scipy oracle port, oracle/; the reference itself is Python and
-cannot travel to the GPU box) on a bounded sample of the same workload.
+cannot travel to the GPU box) on the same C3 workload, the same step.
 """
 
 from __future__ import annotations
@@ -112,68 +112,79 @@ def build_workload(name):
 
 
 # --------------------------------------------------------------------------
-# CPU reference (oracle port) on a bounded sample
+# CPU reference (oracle port) on the real C3 phantom
 # --------------------------------------------------------------------------
 
-def cpu_sample_model():
-    """z-slab of the C3 phantom: the full 160x112 cross-section, 100 voxel
-    layers from the middle of the body (~1.14M DOFs)."""
-    import numpy as np
-    from paper_2010_12879_b200 import workloads
-    from paper_2010_12879_b200.voxel_model import VoxelModel
-    full = workloads.duke_like_model(0.002)
-    ids = np.array(full.tissue_ids[:, :, 380:480])
-    return VoxelModel(ids.shape, full.spacing, (0.0, 0.0, 0.0), ids, full.tissue_table), full
-
-
-def cpu_reference(steps, warmup, n_full_dofs=8_913_552, nrhs=2, log=print):
-    """Time the reference algorithm (oracle port: assemble_poisson,
-    amg_setup hoisted, fgmres_solve to 1e-8) on the slab sample; scale per
-    DOF to the full C3 phantom and to both rhs."""
-    import numpy as np
-    import oracle
-    from paper_2010_12879_b200 import workloads
+def _blas_threads():
     try:
         from threadpoolctl import threadpool_info
-        blas_threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     except Exception:
-        blas_threads = os.cpu_count() or 1
-    model, full = cpu_sample_model()
-    kappa = model.voxel_kappa(workloads.FREQ_HZ)
-    a = workloads.uniform_potential(model.dims, model.spacing, (0.0, 0.0, 1e-6))
-    t0 = time.perf_counter()
-    sysd = oracle.assemble(kappa, model.spacing, a)
-    t_asm = time.perf_counter() - t0
-    cfg = oracle.OracleSolveConfig(rel_tol=REL_TOL)
-    t0 = time.perf_counter()
-    h = oracle.amg_setup(sysd["matrix"], cfg)
-    t_setup = time.perf_counter() - t0
-    n_s = sysd["matrix"].shape[0]
-    times, its = [], []
-    for k in range(warmup + steps):
+        return os.cpu_count() or 1
+
+
+class CpuReference:
+    """The reference algorithm on the host CPU (numpy/scipy oracle port of
+    /root/reference/pkg/src/spfd; the reference itself is Python and cannot
+    travel to the GPU box), on the full C3 phantom (8,913,552 DOFs).
+
+    Setup (assemble_poisson + amg_setup, fit_operators.py:367-457,
+    linsolve.py:120-169) is hoisted like run_benchmark (pipeline.py:277-288).
+    One step = the GPU arm's step: RHS of both parts (fit_operators.py:438-
+    441), fgmres_solve to 1e-8 for each (linsolve.py:200-298), E-field chain
+    + voxel average for each (dosimetry.py:27-116)."""
+
+    def __init__(self, config="C3", log=print):
+        import oracle
+        from paper_2010_12879_b200 import workloads
+        self.oracle, self.log = oracle, log
+        self.w = build_workload(config)
+        self.kappa = self.w.model.voxel_kappa(self.w.frequency_hz)
         t0 = time.perf_counter()
-        _, it, rel, conv = oracle.fgmres(sysd["matrix"], sysd["rhs"], h, cfg)
-        dt = time.perf_counter() - t0
-        if k >= warmup:
-            times.append(dt)
-            its.append(it)
-        log(f"[cpu] fgmres sample {k}: {dt:.3f}s, {it} it, rel {rel:.2e}")
-    t = statistics.mean(times)
-    scale = n_full_dofs / n_s * nrhs
-    return {
-        "value": t * scale,
-        "unit": "s",
-        "cores": int(blas_threads),
-        "kind": "port",
-        "sample": (f"oracle FGMRES(30)+SA-AMG to rel.res {REL_TOL:g} on a 160x112x100 z-slab of the C3 phantom "
-                   f"({n_s} DOFs, {statistics.mean(its):.1f} it, {t:.3f}s mean of {len(times)}), scaled x{scale:.2f} "
-                   f"= (C3 DOFs / slab DOFs) x 2 rhs; scipy sparse kernels single-threaded, BLAS {blas_threads} threads; "
-                   f"setup {t_setup:.2f}s and assembly {t_asm:.2f}s not included"),
-        "sample_solve_s": t,
-        "sample_dofs": n_s,
-        "sample_iters": statistics.mean(its),
-        "sample_setup_s": t_setup,
-    }
+        self.sysd = oracle.assemble(self.kappa, self.w.model.spacing, self.w.a[0])
+        self.t_asm = time.perf_counter() - t0
+        self.cfg = oracle.OracleSolveConfig(rel_tol=REL_TOL)
+        t0 = time.perf_counter()
+        self.h = oracle.amg_setup(self.sysd["matrix"], self.cfg)
+        self.t_setup = time.perf_counter() - t0
+        self.n = self.sysd["matrix"].shape[0]
+        log(f"[cpu] {self.w.name}: {self.n} DOFs, assembly {self.t_asm:.1f}s, amg_setup {self.t_setup:.1f}s, "
+            f"levels {self.h['sizes']}")
+        self.steps, self.solves, self.its = [], [], []
+
+    def step(self):
+        o, w, sysd = self.oracle, self.w, self.sysd
+        t0 = time.perf_counter()
+        for c in range(w.a.shape[0]):
+            rhs = o.assemble_rhs(sysd, w.model.dims, w.a[c])
+            ts = time.perf_counter()
+            x, it, rel, conv = o.fgmres(sysd["matrix"], rhs, self.h, self.cfg)
+            self.solves.append(time.perf_counter() - ts)
+            self.its.append(it)
+            v = o.edge_voltages(w.a[c], x, sysd["dof_to_node"], w.model.dims, w.omega)
+            o.voxel_average(o.node_field(v, sysd["w"], w.model.dims, w.model.spacing), self.kappa)
+            self.log(f"[cpu] rhs {c}: fgmres {self.solves[-1]:.2f}s, {it} it, rel {rel:.2e}")
+        self.steps.append(time.perf_counter() - t0)
+        self.log(f"[cpu] step {len(self.steps)}: {self.steps[-1]:.2f}s")
+        return self.steps[-1]
+
+    def summary(self):
+        t = statistics.mean(self.steps)
+        sd = statistics.stdev(self.steps) if len(self.steps) > 1 else None
+        ts = statistics.mean(self.solves)
+        threads = _blas_threads()
+        return {
+            "value": t, "unit": "s", "cores": int(threads), "kind": "port",
+            "sample": (f"{self.w.name}, {self.n:,} DOFs (the full bench workload, not a sample): "
+                       f"{len(self.steps)} step(s) of RHS + fgmres_solve to rel.res {REL_TOL:g} + E-field/voxel "
+                       f"average for both re/im parts, mean {t:.2f}s" + (f" +- {sd:.2f}s (n-1)" if sd else "") +
+                       f"; per-rhs fgmres {ts:.2f}s at {statistics.mean(self.its):.1f} it; setup hoisted "
+                       f"(assembly {self.t_asm:.1f}s, amg_setup {self.t_setup:.1f}s); scipy sparse kernels "
+                       f"single-threaded, BLAS {threads} threads"),
+            "stddev_s": sd, "steps": len(self.steps), "fgmres_per_rhs_s": ts,
+            "iterations": statistics.mean(self.its), "setup_s": self.t_setup, "assembly_s": self.t_asm,
+            "dofs": self.n,
+        }
 
 
 # --------------------------------------------------------------------------
@@ -188,8 +199,10 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=1, help="timed CPU steps of the cpu_baseline leg")
+    ap.add_argument("--ref-steps", type=int, default=2, help="cap on timed steps of --impl reference")
     ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--tol-reps", type=int, default=5, help="reps of the 1e-8/1e-12 solve-time table (0 = skip)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
                     help="host = gloo host-callback transport (testing several ranks on one GPU)")
     ap.add_argument("--replicate-below", type=int, default=100_000,
@@ -206,15 +219,29 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_reference(args.steps, args.warmup, log=log)
+        # each step is a full C3 snapshot pair on the CPU (~80 s): the run is
+        # capped at --ref-steps timed steps so it ends within a few minutes;
+        # no warm-up (nothing is compiled or cached between steps)
+        steps = max(1, min(args.steps, args.ref_steps))
+        ref = CpuReference(args.config, log=log)
+        for _ in range(steps):
+            ref.step()
+        cb = ref.summary()
         line = {
             "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["sample_solve_s"] * 1e3,
+            "steps": steps, "warmup": 0, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": cb["value"] * 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (Duke-like layered elliptic cylinder, uniform B)",
-            "config": {"workload": "C3 Duke-like 2 mm, 8,913,552 DOFs, complex (re/im) rhs", "rel_tol": REL_TOL,
-                       "parallelism": "host CPU"},
+            "data": "synthetic (Duke-like layered elliptic cylinder, uniform B re/im, comb-gauge edge potentials)",
+            "config": {"workload": f"{args.config} {ref.w.name}: {ref.n} DOFs, complex (re/im) rhs",
+                       "rel_tol": REL_TOL, "method": "FGMRES(30) + SA-AMG V(1,1) (the reference's fgmres_solve)",
+                       "parallelism": "host CPU",
+                       "step": "rhs assembly + fgmres solve to 1e-8 (both rhs) + E-field/voxel average",
+                       "steps_note": f"{steps} timed step(s) of the {args.steps} requested: one step is a full C3 "
+                                     f"snapshot pair on the CPU"},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "fgmres_per_rhs_s": cb["fgmres_per_rhs_s"], "iterations": cb["iterations"],
+            "stddev_s": cb["stddev_s"], "setup_s": cb["setup_s"],
             "e2e": {"value": cb["value"], "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line), flush=True)
@@ -332,6 +359,43 @@ def main():
         dist.all_reduce(t)
         h2d, d2h = int(t[0].item()), int(t[1].item())
 
+    # the paper's tolerance (reference default linsolve.py:30): the
+    # same step at rel.res 1e-12, and the reference's own fgmres_solve on one rhs
+    # (the paper-comparable single solve, "< 0.5 s on a V100") at
+    # 1e-8 and 1e-12 -- device time with CUDA events on the solve stream
+    tolerances = None
+    if world == 1 and args.tol_reps > 0:
+        from paper_2010_12879_b200 import fgmres_solve
+
+        def _timed(fn, reps):
+            fn()
+            torch.cuda.synchronize()
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            out = []
+            for _ in range(reps):
+                t0.record(stream)
+                r_ = fn()
+                t1.record(stream)
+                torch.cuda.synchronize()
+                out.append((t0.elapsed_time(t1), r_))
+            return statistics.mean(o[0] for o in out), out[-1][1]
+
+        tolerances = {}
+        for tv in (1e-8, 1e-12):
+            c_ = SolveConfig(rel_tol=tv, max_nrhs=2)
+            ms_s, rep_s = _timed(lambda: sess.snapshot(a_dev, cfg=c_)[1], args.tol_reps)
+            rhs_dev = sess.op.rhs(a_dev)
+            ms_f, rep_f = _timed(lambda: fgmres_solve(None, rhs_dev[0], h, c_)[1], args.tol_reps)
+            ms_fp, rep_fp = _timed(lambda: fgmres_solve(None, rhs_dev, h, c_)[1], args.tol_reps)
+            tolerances[f"{tv:g}"] = {
+                "step_pcg_pair_s": ms_s / 1e3, "step_pcg_iterations": rep_s.iterations,
+                "fgmres_single_rhs_s": ms_f / 1e3, "fgmres_single_rhs_iterations": rep_f.iterations,
+                "fgmres_single_rhs_rel_residual": rep_f.rel_residual,
+                "fgmres_pair_s": ms_fp / 1e3, "fgmres_pair_iterations": rep_fp.iterations,
+                "reps": args.tol_reps}
+            log(f"[bench] rel_tol {tv:g}: step {ms_s:.2f} ms ({rep_s.iterations} it), fgmres single rhs "
+                f"{ms_f:.2f} ms ({rep_f.iterations} it), fgmres pair {ms_fp:.2f} ms")
+
     # roofline of the dominant kernel (fine-level matrix-free SpMV, both rhs)
     import ctypes
     kms, kbytes = ctypes.c_double(), ctypes.c_double()
@@ -392,9 +456,13 @@ def main():
                        "its voxel |E| copied out; transfers overlap the neighbouring snapshots' solves",
                 "single_snapshot_s": e2e_single_ms / 1e3},
         "clocks": clk,
+        "tolerances": tolerances,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference(args.cpu_steps, 1, log=log)
+        ref = CpuReference(args.config, log=log)
+        for _ in range(max(1, args.cpu_steps)):
+            ref.step()
+        cb = ref.summary()
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)

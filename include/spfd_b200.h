@@ -352,9 +352,9 @@ int spfd_bench_kernel(spfd_amg_t amg, int which, int reps, int nrhs, double *h_m
                       void *stream);
 /* Tuning knob (not part of the reference API): select the fine-level
  * stencil kernel used by every later solve / V-cycle in this process.
- * kind = -1 default (environment SPFD_SPAN_KERNEL, else the z-march
- * kernel), 2 flat per-position kernel, 4 z-march register-pipeline kernel.
- * Both give bit-identical results; this exists for A/B parity tests. */
+ * kind = -1 default (environment SPFD_SPAN_KERNEL=flat|seg, else the
+ * row-segment kernel), 2 flat per-position kernel, 8 row-segment kernel.
+ * Both give bit-identical stencil outputs; this exists for A/B parity tests. */
 int spfd_set_fine_kernel(int kind);
 /* Tuning knob: run PCG as one CUDA graph with a device-side WHILE node
  * (mode 1, the default) or as the host-driven loop (mode 0); -1 restores the

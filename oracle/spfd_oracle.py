@@ -23,7 +23,7 @@ from scipy.sparse.csgraph import connected_components
 __all__ = [
     "OracleSolveConfig", "kappa_at", "edge_dims", "edge_offsets", "n_edges", "kappa_lut",
     "voxel_kappa", "edge_conductance", "node_conductive_mask",
-    "component_labels", "assemble", "strength_graph", "plain_aggregation",
+    "component_labels", "assemble", "assemble_rhs", "strength_graph", "plain_aggregation",
     "amg_setup", "v_cycle", "fgmres", "pcg", "edge_voltages", "node_field",
     "voxel_average", "comb_gauge", "uniform_face_fluxes", "node_index", "coil_field",
     "interpolate_to_faces", "divergence_matrix", "divergence_clean", "circulation_residual", "comb_tree_mask",
@@ -242,6 +242,24 @@ def assemble(kappa, spacing, a_edges, pin=True):
     return dict(matrix=mat, rhs=rhs_nodes[dof_to_node], node_to_dof=node_to_dof,
                 dof_to_node=dof_to_node, pinned=pinned, w=w, labels=labels,
                 n_conductive=int(cond.size), n_components=int(pinned.size))
+
+
+def assemble_rhs(sysd, dims, a_edges):
+    """RHS of an already assembled system for another vector potential
+    (fit_operators.py:438-441: the same bincount over active edges, no
+    re-assembly of the matrix)."""
+    w = sysd["w"]
+    a_edges = np.asarray(a_edges, dtype=np.float64)
+    if a_edges.shape != w.shape:
+        raise ValueError("vector potential has the wrong length")
+    tails, heads = _edge_endpoints(dims)
+    on = w > 0.0
+    t, h = tails[on], heads[on]
+    flow = w[on] * a_edges[on]
+    nn = sysd["labels"].size
+    rhs_nodes = np.bincount(t, weights=flow, minlength=nn)
+    rhs_nodes -= np.bincount(h, weights=flow, minlength=nn)
+    return rhs_nodes[sysd["dof_to_node"]]
 
 
 # --------------------------------------------------------------------------

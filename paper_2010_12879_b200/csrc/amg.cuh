@@ -98,6 +98,7 @@ void amg_from_level0(Amg &h, const double *inter, double *planar, int nrhs, cuda
 
 int csr_group(int64_t nnz, int64_t rows);  // lanes per row of the CSR kernels
 void level1_unpermute(Amg &h, cudaStream_t s);  // reference level-1 numbering (amg_setup.cu)
+void amg_drop_graphs(Amg &h);  // destroy captured solve graphs (buffers changed; solve.cu)
 void amg_distribute(Amg &h, Comm *comm, int64_t replicate_below, int64_t *range, cudaStream_t s);
 void dist_range_exchange(Amg &h, double *v, int nrhs, cudaStream_t s);
 void dist_info(const Amg &h, int64_t *out);  // pb, pe, voxel-row begin, end

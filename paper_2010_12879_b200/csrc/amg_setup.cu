@@ -886,6 +886,8 @@ static void perm_csr(Csr &m, const int32_t *P, const int32_t *cmap, cudaStream_t
 void level1_permute(Amg &h, const int32_t *P, cudaStream_t s) {
     const int T = 256;
     Level &L0 = h.lv[0], &L1 = h.lv[1];
+    // the captured PCG graphs hold the buffers replaced below: recapture
+    amg_drop_graphs(h);
     const int64_t n1 = L1.n;
     DevBuf<int32_t> inv;
     inv.alloc(n1);

@@ -333,7 +333,7 @@ int spfd_bench_kernel(spfd_amg_t h, int which, int reps, int nrhs, double *h_ms,
 
 int spfd_set_fine_kernel(int kind) {
     return guarded([&] {
-        SPFD_CHECK(kind == -1 || (kind >= 2 && kind <= 7 && kind != 3), SPFD_EINVAL, "fine kernel kind must be -1, 2, 4, 5, 6 or 7");
+        SPFD_CHECK(kind == -1 || kind == 2 || kind == 8, SPFD_EINVAL, "fine kernel kind must be -1, 2 or 8");
         g_fine_kind_override = kind;
     });
 }

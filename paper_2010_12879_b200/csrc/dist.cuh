@@ -430,10 +430,13 @@ int launch_fine_ov(Dist &D, const Operator &op, const SpanArgs &sa, double *xin,
 }
 
 void amg_distribute_impl(Amg &h, Comm *comm, int64_t replicate_below, int64_t *range, cudaStream_t s) {
+    // validate everything before touching the hierarchy
     SPFD_CHECK(h.structured, SPFD_EINVAL, "distribution needs an operator (structured) hierarchy");
-    level1_unpermute(h, s);  // the slab decomposition works in the reference numbering
     SPFD_CHECK(h.pre <= 1 && h.post == 1, SPFD_EINVAL, "distributed V-cycle supports pre_sweeps <= 1, post_sweeps == 1");
-    SPFD_CHECK(fine_kernel_kind() == 2, SPFD_EINVAL, "distributed solve needs the flat span kernel");
+    SPFD_CHECK(comm != nullptr && comm->size >= 1 && comm->rank >= 0 && comm->rank < comm->size, SPFD_EINVAL,
+               "invalid communicator");
+    SPFD_CHECK(h.op->NZ >= 2 * comm->size, SPFD_EINVAL, "fewer than two node planes per rank");
+    level1_unpermute(h, s);  // the slab decomposition works in the reference numbering
     const int T = 256;
     const Operator &op = *h.op;
     auto *D = new Dist();

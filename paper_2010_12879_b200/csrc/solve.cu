@@ -144,9 +144,36 @@ __device__ __forceinline__ typename V<R>::T xin(const SpanArgs &a, int pp) {
     return W::ld(a.x, pp);
 }
 
-#include "plane.cuh"
-#include "tile.cuh"
-#include "tail.cuh"
+// Output of one fine-level stencil point for MODE (see k_span), in the
+// reference's summation order (shared by every fine kernel: same bits).
+template <int R, int MODE>
+__device__ __forceinline__ typename V<R>::T point_out(const SpanArgs &a, const Nbr &n, int p) {
+    using W = V<R>;
+    using T = typename W::T;
+    T out;
+    if (MODE == 2) {
+        const double *od = a.od, *rr = a.r;
+        T s = apply_row<R>(n, p, [&](int pp) { return W::scale(od[pp], W::ld(rr, pp)); });
+        out = W::sub(W::ld(rr, p), s);
+    } else if (MODE == 4) {
+        const double *ec = a.ec;
+        const int32_t *ag = a.aggp;
+        auto eat = [&](int pp) {
+            int g1 = ag[pp];  // aggregate id + 1, 0 = none
+            return g1 > 0 ? W::ld(ec, g1 - 1) : W::zero();
+        };
+        T s = apply_row<R>(n, p, eat);
+        T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
+        out = W::sub(W::add(b, eat(p)), W::scale(a.od[p], s));
+    } else {
+        const double *xx = a.x;
+        T s = apply_row<R>(n, p, [&](int pp) { return W::ld(xx, pp); });
+        if (MODE == 0) out = s;
+        else if (MODE == 1) out = W::sub(W::ld(a.r, p), s);
+        else out = W::add(W::ld(xx, p), W::scale(a.od[p], W::sub(W::ld(a.r, p), s)));
+    }
+    return out;
+}
 
 // MODE 0: y = A x (+ partial x.y)
 // MODE 1: y = r - A x (+ partial y.y)
@@ -174,28 +201,7 @@ __global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a
         const int4 q = v.rows[row];
         const Nbr n = neighbours(v, p, row, q);
         const bool dof = mbit(v.mask, p);
-        T out;
-        if (MODE == 2) {
-            const double *od = a.od, *rr = a.r;
-            T s = apply_row<R>(n, p, [&](int pp) { return W::scale(od[pp], W::ld(rr, pp)); });
-            out = W::sub(W::ld(rr, p), s);
-        } else if (MODE == 4) {
-            const double *ec = a.ec;
-            const int32_t *ag = a.aggp;
-            auto eat = [&](int pp) {
-                int g1 = ag[pp];  // aggregate id + 1, 0 = none
-                return g1 > 0 ? W::ld(ec, g1 - 1) : W::zero();
-            };
-            T s = apply_row<R>(n, p, eat);
-            T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
-            out = W::sub(W::add(b, eat(p)), W::scale(a.od[p], s));
-        } else {
-            const double *xx = a.x;
-            T s = apply_row<R>(n, p, [&](int pp) { return W::ld(xx, pp); });
-            if (MODE == 0) out = s;
-            else if (MODE == 1) out = W::sub(W::ld(a.r, p), s);
-            else out = W::add(W::ld(xx, p), W::scale(a.od[p], W::sub(W::ld(a.r, p), s)));
-        }
+        T out = point_out<R, MODE>(a, n, p);
         if (!dof) out = W::zero();
         W::st(a.y, p, out);
         if (DOT) {
@@ -215,300 +221,59 @@ __global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a
     }
 }
 
-template <class T>
-__device__ __forceinline__ T shfl_up1(T v);
-template <>
-__device__ __forceinline__ double shfl_up1<double>(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
-template <>
-__device__ __forceinline__ double2 shfl_up1<double2>(double2 v) {
-    return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
-}
-template <class T>
-__device__ __forceinline__ T shfl_dn1(T v);
-template <>
-__device__ __forceinline__ double shfl_dn1<double>(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
-template <>
-__device__ __forceinline__ double2 shfl_dn1<double2>(double2 v) {
-    return make_double2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
-}
+// Segment kernel: one warp per row segment of <= 32 consecutive positions
+// (op.cu k_seg_fill).  The segment record gives every lane its six
+// neighbour positions directly (no row-table search or neighbour-row record
+// gathers), so a lane's loads depend on one uniform record load only; a CTA
+// takes kSegPerCta consecutive segments.  Same per-point arithmetic as
+// k_span (point_out): bit-identical outputs; the DOT partials are per CTA
+// in a fixed order (bitwise reproducible, CTA cut differs from k_span).
+constexpr int kSegWarps = 8;
+constexpr int kSegPerWarp = 4;
+constexpr int kSegPerCta = kSegWarps * kSegPerWarp;
 
-#include "zmarch.cuh"
-#include "zmt.cuh"
+__device__ __forceinline__ bool lane_in(int lanes, int l) { return l >= (lanes & 255) && l < ((lanes >> 8) & 255); }
 
-// Flat per-position kernel with the -x/+x neighbours (input and weight) taken
-// from the adjacent lanes: a warp holds 32 consecutive span positions, so
-// p-1 / p+1 of the same row sit in lane-1 / lane+1 and only the first/last
-// lane of a run gathers them.  Same arithmetic and order as k_span.
-template <int R, int MODE, bool DOT, bool RANGED = false>
-__global__ void __launch_bounds__(kSpanThreads, 5) k_spx(SpanView v, SpanArgs a) {
+template <int R, int MODE, bool DOT>
+__global__ void __launch_bounds__(kSegWarps * 32) k_seg(SpanView v, SpanArgs a, int64_t s0, int64_t s1) {
     using W = V<R>;
     using T = typename W::T;
-    constexpr unsigned FULL = 0xffffffffu;
     __shared__ double red[32 * R];
-    const int lane = threadIdx.x & 31;
-    const int t = RANGED ? a.tile0 + blockIdx.x : blockIdx.x;
-    const int64_t pend = RANGED ? (a.pe < v.L ? a.pe : v.L) : v.L;
-    const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double dot[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) dot[c] = 0.0;
-    int row = r0;
-    for (int u = 0; u < kTile / kSpanThreads; ++u) {
-        const int p = t * kTile + u * kSpanThreads + threadIdx.x;
-        if (__all_sync(FULL, p >= pend)) break;  // warp-uniform
-        const bool act = p < pend && !(RANGED && p < a.pb);
-        int pxm = -1, pxp = -1, pym = -1, pyp = -1, pzm = -1, pzp = -1;
-        double wxp = 0.0, wyp = 0.0, wzp = 0.0;
-        T xc = W::zero();
-        if (act) {
-            row = frow(v.rows, row, r1, p);
-            const int4 q = v.rows[row];
-            const int i = q.y + (p - q.x), j = q.w;
-            pxm = (i > q.y) ? p - 1 : -1;
-            pxp = (i + 1 < q.z) ? p + 1 : -1;
-            pym = (j > 0) ? spos(v.rows, row - 1, i) : -1;
-            pyp = (j + 1 < v.NY) ? spos(v.rows, row + 1, i) : -1;
-            pzm = (row >= v.NY) ? spos(v.rows, row - v.NY, i) : -1;
-            pzp = (row + v.NY < v.n_rows) ? spos(v.rows, row + v.NY, i) : -1;
-            wxp = v.wx[p]; wyp = v.wy[p]; wzp = v.wz[p];
-            xc = xin<R, MODE>(a, p);
-        }
-        const bool left = __shfl_up_sync(FULL, act, 1) && lane > 0;    // lane-1 holds p-1
-        const bool right = __shfl_down_sync(FULL, act, 1) && lane < 31; // lane+1 holds p+1
-        const T xl = shfl_up1(xc), xr = shfl_dn1(xc);
-        const double wl = __shfl_up_sync(FULL, wxp, 1);
-        if (!act) continue;
-        const double wxm = pxm >= 0 ? (left ? wl : v.wx[pxm]) : 0.0;
-        const double wym = pym >= 0 ? v.wy[pym] : 0.0;
-        const double wzm = pzm >= 0 ? v.wz[pzm] : 0.0;
+    const int64_t base = s0 + (int64_t)blockIdx.x * kSegPerCta + warp;
+    for (int u = 0; u < kSegPerWarp; ++u) {
+        const int64_t sg = base + u * kSegWarps;
+        if (sg >= s1) break;
+        const int4 ra = v.segs[2 * sg], rb = v.segs[2 * sg + 1];
+        const int n = rb.y & 255;
+        if (lane >= n) continue;
+        const int p = ra.x + lane;
+        Nbr nb;
+        nb.wxp = v.wx[p]; nb.wyp = v.wy[p]; nb.wzp = v.wz[p];
+        nb.pxm = (lane > 0 || (rb.y & 256)) ? p - 1 : -1;
+        nb.pxp = (lane + 1 < n || (rb.y & 512)) ? p + 1 : -1;
+        nb.pym = lane_in(rb.z & 0xffff, lane) ? p + ra.y : -1;
+        nb.pyp = lane_in(rb.z >> 16, lane) ? p + ra.z : -1;
+        nb.pzm = lane_in(rb.w & 0xffff, lane) ? p + ra.w : -1;
+        nb.pzp = lane_in(rb.w >> 16, lane) ? p + rb.x : -1;
+        nb.wxm = nb.pxm >= 0 ? v.wx[nb.pxm] : 0.0;
+        nb.wym = nb.pym >= 0 ? v.wy[nb.pym] : 0.0;
+        nb.wzm = nb.pzm >= 0 ? v.wz[nb.pzm] : 0.0;
         // reference diagonal order: tail edges x, y, z then head edges x, y, z
-        const double diag = add_rn(add_rn(add_rn(add_rn(add_rn(wxp, wyp), wzp), wxm), wym), wzm);
-        T s = W::zero();
-        if (pzm >= 0) s = W::axpy(-wzm, xin<R, MODE>(a, pzm), s);
-        if (pym >= 0) s = W::axpy(-wym, xin<R, MODE>(a, pym), s);
-        if (pxm >= 0) s = W::axpy(-wxm, left ? xl : xin<R, MODE>(a, pxm), s);
-        s = W::axpy(diag, xc, s);
-        if (pxp >= 0) s = W::axpy(-wxp, right ? xr : xin<R, MODE>(a, pxp), s);
-        if (pyp >= 0) s = W::axpy(-wyp, xin<R, MODE>(a, pyp), s);
-        if (pzp >= 0) s = W::axpy(-wzp, xin<R, MODE>(a, pzp), s);
-        T out;
-        if (MODE == 0) out = s;
-        else if (MODE == 1) out = W::sub(W::ld(a.r, p), s);
-        else if (MODE == 2) out = W::sub(W::ld(a.r, p), s);
-        else if (MODE == 3) out = W::add(xc, W::scale(a.od[p], W::sub(W::ld(a.r, p), s)));
-        else {
-            const T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
-            out = W::sub(W::add(b, xc), W::scale(a.od[p], s));
-        }
-        if (!mbit(v.mask, p)) out = W::zero();
+        nb.diag = add_rn(add_rn(add_rn(add_rn(add_rn(nb.wxp, nb.wyp), nb.wzp), nb.wxm), nb.wym), nb.wzm);
+        const bool dof = mbit(v.mask, p);
+        T out = point_out<R, MODE>(a, nb, p);
+        if (!dof) out = W::zero();
         W::st(a.y, p, out);
         if (DOT) {
 #pragma unroll
             for (int c = 0; c < R; ++c) {
-                if (MODE == 0) dot[c] += W::dot(xc, out, c);
+                if (MODE == 0) dot[c] += W::dot(W::ld(a.x, p), out, c);
                 else if (MODE == 3) dot[c] += W::dot(W::ld(a.r, p), out, c);
                 else dot[c] += W::dot(out, out, c);
-            }
-        }
-    }
-    if (DOT) {
-        block_sum<R>(dot, red);
-        if (threadIdx.x == 0)
-#pragma unroll
-            for (int c = 0; c < R; ++c) a.partials[blockIdx.x * R + c] = dot[c];
-    }
-}
-
-// ---- coded flat kernel ---------------------------------------------------
-// Same per-position mapping and arithmetic as k_span, but the neighbour
-// structure comes from one byte per position (DOF bit + which of the six
-// neighbours exist) and one int4 per row (position deltas to the -y/+y/-z/+z
-// neighbour rows) instead of four neighbour-row records per position: the
-// index traffic through L1 drops from ~80 B to ~17 B per position.
-
-__global__ void k_build_rdelta(const int4 *rows, int64_t n_rows, int NY, int4 *rd) {
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
-        const int4 q = rows[r];
-        const int base = q.x - q.y;
-        auto del = [&](int64_t rn, bool ok) { return ok ? (rows[rn].x - rows[rn].y) - base : 0; };
-        rd[r] = make_int4(del(r - 1, q.w > 0), del(r + 1, q.w + 1 < NY), del(r - NY, r >= NY), del(r + NY, r + NY < n_rows));
-    }
-}
-
-__global__ void k_build_ncode(SpanView v, uint8_t *code) {
-    const int t = blockIdx.x;
-    const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
-    int row = r0;
-    for (int u = 0; u < kTile / kSpanThreads; ++u) {
-        const int p = t * kTile + u * kSpanThreads + threadIdx.x;
-        if (p >= v.L) break;
-        row = frow(v.rows, row, r1, p);
-        const int4 q = v.rows[row];
-        const int i = q.y + (p - q.x), j = q.w;
-        uint8_t c = mbit(v.mask, p) ? 1 : 0;
-        if (i > q.y) c |= 2;
-        if (i + 1 < q.z) c |= 4;
-        if (j > 0 && spos(v.rows, row - 1, i) >= 0) c |= 8;
-        if (j + 1 < v.NY && spos(v.rows, row + 1, i) >= 0) c |= 16;
-        if (row >= v.NY && spos(v.rows, row - v.NY, i) >= 0) c |= 32;
-        if (row + v.NY < v.n_rows && spos(v.rows, row + v.NY, i) >= 0) c |= 64;
-        code[p] = c;
-    }
-}
-
-template <int R, int MODE, bool DOT, bool RANGED = false>
-__global__ void __launch_bounds__(kSpanThreads, 6) k_spc(SpanView v, const uint8_t *__restrict__ code,
-                                                        const int4 *__restrict__ rd, SpanArgs a) {
-    using W = V<R>;
-    using T = typename W::T;
-    __shared__ double red[32 * R];
-    const int t = RANGED ? a.tile0 + blockIdx.x : blockIdx.x;
-    const int64_t pend = RANGED ? (a.pe < v.L ? a.pe : v.L) : v.L;
-    const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
-    double dot[R];
-#pragma unroll
-    for (int c = 0; c < R; ++c) dot[c] = 0.0;
-    int row = r0;
-    for (int u = 0; u < kTile / kSpanThreads; ++u) {
-        const int p = t * kTile + u * kSpanThreads + threadIdx.x;
-        if (p >= pend) break;
-        if (RANGED && p < a.pb) continue;
-        row = frow(v.rows, row, r1, p);
-        const unsigned c = code[p];
-        const int4 d = rd[row];
-        Nbr n;
-        n.pxm = (c & 2) ? p - 1 : -1;
-        n.pxp = (c & 4) ? p + 1 : -1;
-        n.pym = (c & 8) ? p + d.x : -1;
-        n.pyp = (c & 16) ? p + d.y : -1;
-        n.pzm = (c & 32) ? p + d.z : -1;
-        n.pzp = (c & 64) ? p + d.w : -1;
-        n.wxp = v.wx[p]; n.wyp = v.wy[p]; n.wzp = v.wz[p];
-        n.wxm = n.pxm >= 0 ? v.wx[n.pxm] : 0.0;
-        n.wym = n.pym >= 0 ? v.wy[n.pym] : 0.0;
-        n.wzm = n.pzm >= 0 ? v.wz[n.pzm] : 0.0;
-        // reference diagonal order: tail edges x, y, z then head edges x, y, z
-        n.diag = add_rn(add_rn(add_rn(add_rn(add_rn(n.wxp, n.wyp), n.wzp), n.wxm), n.wym), n.wzm);
-        T out;
-        if (MODE == 2) {
-            const double *od = a.od, *rr = a.r;
-            T s = apply_row<R>(n, p, [&](int pp) { return W::scale(od[pp], W::ld(rr, pp)); });
-            out = W::sub(W::ld(rr, p), s);
-        } else if (MODE == 4) {
-            const double *ec = a.ec;
-            const int32_t *ag = a.aggp;
-            auto eat = [&](int pp) {
-                int g1 = ag[pp];  // aggregate id + 1, 0 = none
-                return g1 > 0 ? W::ld(ec, g1 - 1) : W::zero();
-            };
-            T s = apply_row<R>(n, p, eat);
-            T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
-            out = W::sub(W::add(b, eat(p)), W::scale(a.od[p], s));
-        } else {
-            const double *xx = a.x;
-            T s = apply_row<R>(n, p, [&](int pp) { return W::ld(xx, pp); });
-            if (MODE == 0) out = s;
-            else if (MODE == 1) out = W::sub(W::ld(a.r, p), s);
-            else out = W::add(W::ld(xx, p), W::scale(a.od[p], W::sub(W::ld(a.r, p), s)));
-        }
-        if (!(c & 1)) out = W::zero();
-        W::st(a.y, p, out);
-        if (DOT) {
-#pragma unroll
-            for (int cc = 0; cc < R; ++cc) {
-                if (MODE == 0) dot[cc] += W::dot(W::ld(a.x, p), out, cc);
-                else if (MODE == 3) dot[cc] += W::dot(W::ld(a.r, p), out, cc);
-                else dot[cc] += W::dot(out, out, cc);
-            }
-        }
-    }
-    if (DOT) {
-        block_sum<R>(dot, red);
-        if (threadIdx.x == 0)
-#pragma unroll
-            for (int cc = 0; cc < R; ++cc) a.partials[blockIdx.x * R + cc] = dot[cc];
-    }
-}
-
-// Row-chunk kernel: each warp takes work items of 32 consecutive positions
-// of ONE row, so the row record and the four neighbour-row records are
-// warp-uniform (broadcast) loads, every neighbour access is a contiguous
-// (coalesced) run, and the +-x neighbours come from lane shuffles.  Same
-// MODEs and the same reference-order arithmetic as k_span.
-template <int R, int MODE, bool DOT>
-__global__ void __launch_bounds__(256) k_items(SpanView v, SpanArgs a) {
-    using W = V<R>;
-    using T = typename W::T;
-    constexpr unsigned FULL = 0xffffffffu;
-    __shared__ double red[32 * R];
-    const int lane = threadIdx.x & 31;
-    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    double dot[R];
-#pragma unroll
-    for (int c = 0; c < R; ++c) dot[c] = 0.0;
-    for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < v.n_items; it += nwarp) {
-        const int2 item = v.items[it];
-        const int r = item.x;
-        const int4 q = v.rows[r];
-        const int j = q.w;
-        const int4 qym = j > 0 ? v.rows[r - 1] : make_int4(0, 0, 0, 0);
-        const int4 qyp = j + 1 < v.NY ? v.rows[r + 1] : make_int4(0, 0, 0, 0);
-        const int4 qzm = r >= v.NY ? v.rows[r - v.NY] : make_int4(0, 0, 0, 0);
-        const int4 qzp = r + v.NY < v.n_rows ? v.rows[r + v.NY] : make_int4(0, 0, 0, 0);
-        const int i0 = q.y + item.y;
-        const int i = i0 + lane;
-        const bool on = i < q.z;
-        const int ic = on ? i : i0;            // inactive lanes mirror lane 0
-        const int p = q.x + (ic - q.y);
-        const bool hxm = ic > q.y, hxp = ic + 1 < q.z;
-        const double wxp = v.wx[p], wyp = v.wy[p], wzp = v.wz[p];
-        double wxm = __shfl_up_sync(FULL, wxp, 1);
-        if (lane == 0) wxm = hxm ? v.wx[p - 1] : 0.0;
-        if (!hxm) wxm = 0.0;
-        const int pym = (ic >= qym.y && ic < qym.z) ? qym.x + (ic - qym.y) : -1;
-        const int pyp = (ic >= qyp.y && ic < qyp.z) ? qyp.x + (ic - qyp.y) : -1;
-        const int pzm = (ic >= qzm.y && ic < qzm.z) ? qzm.x + (ic - qzm.y) : -1;
-        const int pzp = (ic >= qzp.y && ic < qzp.z) ? qzp.x + (ic - qzp.y) : -1;
-        const double wym = pym >= 0 ? v.wy[pym] : 0.0;
-        const double wzm = pzm >= 0 ? v.wz[pzm] : 0.0;
-        const T xc = xin<R, MODE>(a, p);
-        T xxm = shfl_up1(xc), xxp = shfl_dn1(xc);
-        if (lane == 0) xxm = hxm ? xin<R, MODE>(a, p - 1) : W::zero();
-        if (lane == 31 || !on) xxp = hxp ? xin<R, MODE>(a, p + 1) : W::zero();
-        if (!hxm) xxm = W::zero();
-        if (!hxp) xxp = W::zero();
-        const T xym = pym >= 0 ? xin<R, MODE>(a, pym) : W::zero();
-        const T xyp = pyp >= 0 ? xin<R, MODE>(a, pyp) : W::zero();
-        const T xzm = pzm >= 0 ? xin<R, MODE>(a, pzm) : W::zero();
-        const T xzp = pzp >= 0 ? xin<R, MODE>(a, pzp) : W::zero();
-        // reference diagonal order: tail edges x, y, z then head edges x, y, z
-        const double diag = add_rn(add_rn(add_rn(add_rn(add_rn(wxp, wyp), wzp), wxm), wym), wzm);
-        T s = W::zero();
-        s = W::axpy(-wzm, xzm, s);
-        s = W::axpy(-wym, xym, s);
-        s = W::axpy(-wxm, xxm, s);
-        s = W::axpy(diag, xc, s);
-        s = W::axpy(-wxp, xxp, s);
-        s = W::axpy(-wyp, xyp, s);
-        s = W::axpy(-wzp, xzp, s);
-        T out;
-        if (MODE == 0) out = s;
-        else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(a.r, p), s);
-        else if (MODE == 3) out = W::add(xc, W::scale(a.od[p], W::sub(W::ld(a.r, p), s)));
-        else {
-            const T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
-            out = W::sub(W::add(b, xc), W::scale(a.od[p], s));
-        }
-        if (!mbit(v.mask, p)) out = W::zero();
-        if (on) {
-            W::st(a.y, p, out);
-            if (DOT) {
-#pragma unroll
-                for (int c = 0; c < R; ++c) {
-                    if (MODE == 0) dot[c] += W::dot(xc, out, c);
-                    else if (MODE == 3) dot[c] += W::dot(W::ld(a.r, p), out, c);
-                    else dot[c] += W::dot(out, out, c);
-                }
             }
         }
     }
@@ -1072,7 +837,7 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
     int64_t n = nvec0 * R;
     h.kx.alloc(n); h.kr.alloc(n); h.kz.alloc(n); h.kp.alloc(n); h.kq.alloc(n); h.kb.alloc(n);
     int64_t np = kDotGrid;
-    if (h.structured) np = std::max<int64_t>(np, h.op->n_tiles);
+    if (h.structured) np = std::max<int64_t>(np, std::max<int64_t>(h.op->n_tiles, h.op->n_segs / 32 + 1));
     np = std::max<int64_t>(np, 148 * 16);
     np = std::max<int64_t>(np, (int64_t)kDotGrid * 8);  // batched FGMRES block dots (k_mdot, 8 vectors)
     h.partials.alloc(np * 2 + 64);
@@ -1095,130 +860,25 @@ int g_fine_kind_override = -1;
 
 namespace {
 
-// 0 = row-chunk items, 1 = 2.5-D plane, 2 = flat per-position, 3 = tile,
-// 4 = z-march (register pipeline along z)
+// fine-level stencil kernel: 2 = flat per-position k_span, 8 = row-segment
+// k_seg (default)
 int fine_kernel_kind() {
     if (g_fine_kind_override >= 0) return g_fine_kind_override;
     static int v = -1;
     if (v < 0) {
-        // the 2.5-D plane kernel is experimental (latency-bound at 1-2
-        // CTAs/SM); the flat span kernel is the default
         const char *e = getenv("SPFD_SPAN_KERNEL");
-        v = 2;
-        if (e && std::string(e) == "plane") v = 1;
-        if (e && std::string(e) == "items") v = 0;
-        if (e && std::string(e) == "tile") v = 3;
-        if (e && std::string(e) == "zm") v = 4;
-        if (e && std::string(e) == "spx") v = 5;
+        v = 8;
         if (e && std::string(e) == "flat") v = 2;
-        if (e && std::string(e) == "coded") v = 6;
-        if (e && std::string(e) == "zt") v = 7;
+        if (e && std::string(e) == "seg") v = 8;
     }
     return v;
 }
 
-template <int R, int MODE>
-PlaneGeo plane_geometry(const Operator &op) {
-    size_t per = (size_t)kPlaneSlots * (kPlaneJB + 2) * op.NX * PlaneStage<R, MODE>::bytes + 64;
-    int cps = (int)((227 * 1024) / (per + 1024));
-    if (cps > 8) cps = 8;
-    if (cps < 1) cps = 1;
-    return plane_geo(op, cps);
-}
-
-// Work items of the z-march kernel: for every chunk of kc planes and every
-// node row j, the union [ilo, ihi) of the row's spans over the chunk is cut
-// into 32-wide segments; items are ordered (chunk, segment, j) so that a
-// CTA's warps stream adjacent rows of the same planes (their -y/+y gathers
-// hit L1).  Returns false (flat kernel) when the grid would exceed the dot
-// partials buffer.
-bool zm_build(const Operator &op) {
-    if (op.n_zm_items >= 0) return op.n_zm_items > 0;
-    op.n_zm_items = 0;
-    const int NY = (int)op.NY, NZ = (int)op.NZ;
-    if (op.n_rows <= 0 || NY <= 0 || NZ <= 0) return false;
-    std::vector<int4> rows((size_t)op.n_rows);
-    SPFD_CUDA(cudaMemcpy(rows.data(), op.rows.get(), rows.size() * sizeof(int4), cudaMemcpyDeviceToHost));
-    int64_t s1 = 0;
-    for (const int4 &q : rows) s1 += (q.z - q.y + 31) / 32;
-    int kc = (int)std::min<int64_t>(16, std::max<int64_t>(4, s1 / (148 * 8 * 8)));
-    if (const char *e = getenv("SPFD_ZM_KC")) kc = std::max(1, atoi(e));
-    std::vector<int4> items;
-    std::vector<int> ilo(NY), nseg(NY);
-    for (int k0 = 0; k0 < NZ; k0 += kc) {
-        const int k1 = std::min(NZ, k0 + kc);
-        int smax = 0;
-        const int nb = (NY + kZmRows - 1) / kZmRows;
-        for (int b = 0; b < nb; ++b) {
-            int lo = INT32_MAX, hi = INT32_MIN;
-            for (int j = b * kZmRows; j < std::min(NY, (b + 1) * kZmRows); ++j)
-                for (int k = k0; k < k1; ++k) {
-                    const int4 q = rows[(size_t)k * NY + j];
-                    if (q.y < q.z) { lo = std::min(lo, q.y); hi = std::max(hi, q.z); }
-                }
-            ilo[b] = lo;
-            nseg[b] = lo < hi ? (hi - lo + 31) / 32 : 0;
-            smax = std::max(smax, nseg[b]);
-        }
-        for (int sg = 0; sg < smax; ++sg)
-            for (int b = 0; b < nb; ++b)
-                if (sg < nseg[b]) items.push_back(make_int4(b * kZmRows, ilo[b] + 32 * sg, k0, k1));
-    }
-    const int64_t grid = (int64_t)items.size();
-    if (items.empty() || grid > std::max<int64_t>(op.n_tiles, 148 * 16)) return false;
-    op.zm_items.alloc(items.size());
-    SPFD_CUDA(cudaMemcpy(op.zm_items.get(), items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    op.n_zm_items = (int64_t)items.size();
-    return true;
-}
-
-// Launch one fine-level stencil pass (flat span kernel; the 2.5-D plane
-// kernel with SPFD_SPAN_KERNEL=plane).  Returns the number of CTAs (dot
-// partials written when DOT).
+// Launch one fine-level stencil pass over the owned positions [a.pb, a.pe).
+// Returns the number of CTAs (dot partials written when DOT).
 template <int R, int MODE, bool DOT>
 int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
     SpanView v = span_view(op);
-    const int kind = fine_kernel_kind();
-    if (kind == 3 && a.pb == 0 && a.pe >= op.L) {
-        static int max_dyn = -1;
-        using SM = TileSmem<R, MODE>;
-        if (max_dyn < 0) {
-            int dev = 0, optin = 0;
-            SPFD_CUDA(cudaGetDevice(&dev));
-            SPFD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-            cudaFuncAttributes fa;
-            SPFD_CUDA(cudaFuncGetAttributes(&fa, k_tile<R, MODE, DOT>));
-            max_dyn = optin - (int)fa.sharedSizeBytes;
-            SPFD_CUDA(cudaFuncSetAttribute(k_tile<R, MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
-        }
-        SPFD_CHECK(SM::bytes <= (size_t)max_dyn, SPFD_EINVAL, "tile kernel shared memory exceeds the opt-in limit");
-        int cps = (int)((228 * 1024) / (SM::bytes + 2048));
-        TileGeo g = tile_geo(op, cps < 1 ? 1 : cps);
-        SpanArgs b = a;
-        b.pe = op.L;
-        int grid = g.itiles * g.jtiles * g.ktiles;
-        k_tile<R, MODE, DOT><<<grid, kTileThreads, SM::bytes, s>>>(v, g, b);
-        SPFD_LAUNCH_CHECK();
-        return grid;
-    }
-    if (kind == 4 && a.pb == 0 && a.pe >= op.L && zm_build(op)) {
-        const int g = (int)op.n_zm_items;
-        constexpr size_t smem = zm_smem<R, MODE>();
-        static bool attr = false;
-        if (!attr) {
-            SPFD_CUDA(cudaFuncSetAttribute(k_zm<R, MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
-        k_zm<R, MODE, DOT><<<g, kZmThreads, smem, s>>>(v, op.zm_items.get(), a);
-        SPFD_LAUNCH_CHECK();
-        return g;
-    }
-    if (kind == 0) {
-        int g = grid_for(op.n_items * 32, 256, 148 * 16);
-        k_items<R, MODE, DOT><<<g, 256, 0, s>>>(v, a);
-        SPFD_LAUNCH_CHECK();
-        return g;
-    }
     if (a.pb > 0 || a.pe < op.L) {  // owned z-slab range
         const int64_t pe = a.pe < op.L ? a.pe : op.L;
         const int t0 = (int)(a.pb / kTile), t1 = (int)((pe + kTile - 1) / kTile);
@@ -1229,75 +889,16 @@ int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
         SPFD_LAUNCH_CHECK();
         return g;
     }
-    if constexpr (R == 2) {
-        if (kind == 7 && a.pb == 0 && a.pe >= op.L && zm_build(op)) {
-            const int g = (int)op.n_zm_items;
-            constexpr size_t smem = zt_smem<MODE>();
-            static bool attr = false;
-            if (!attr) {
-                SPFD_CUDA(cudaFuncSetAttribute(k_zt<MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                attr = true;
-            }
-            k_zt<MODE, DOT><<<g, kZtThreads, smem, s>>>(v, op.zm_items.get(), a);
-            SPFD_LAUNCH_CHECK();
-            return g;
-        }
-    }
-    if (kind == 6) {
-        if (!op.coded) {  // lazily: neighbour codes and row deltas (one pass each)
-            op.ncode.alloc(op.L);
-            op.rdelta.alloc(op.n_rows);
-            k_build_rdelta<<<grid_for(op.n_rows, 256), 256, 0, s>>>(op.rows.get(), op.n_rows, (int)op.NY,
-                                                                    op.rdelta.get());
-            SPFD_LAUNCH_CHECK();
-            if (op.n_tiles > 0) k_build_ncode<<<(int)op.n_tiles, kSpanThreads, 0, s>>>(v, op.ncode.get());
-            SPFD_LAUNCH_CHECK();
-            op.coded = true;
-        }
-        if (a.pb > 0 || a.pe < op.L) {
-            const int64_t pe = a.pe < op.L ? a.pe : op.L;
-            const int t0 = (int)(a.pb / kTile), t1 = (int)((pe + kTile - 1) / kTile);
-            SpanArgs b = a;
-            b.tile0 = t0;
-            const int g = t1 - t0;
-            if (g > 0) k_spc<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, op.ncode.get(), op.rdelta.get(), b);
-            SPFD_LAUNCH_CHECK();
-            return g;
-        }
-        const int g = (int)op.n_tiles;
-        if (g > 0) k_spc<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, op.ncode.get(), op.rdelta.get(), a);
+    if (fine_kernel_kind() == 8) {
+        const int g = (int)((op.n_segs + kSegPerCta - 1) / kSegPerCta);
+        if (g > 0) k_seg<R, MODE, DOT><<<g, kSegWarps * 32, 0, s>>>(v, a, 0, op.n_segs);
         SPFD_LAUNCH_CHECK();
         return g;
     }
-    if (kind == 5) {
-        int g = (int)op.n_tiles;
-        if (g > 0) k_spx<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
-        SPFD_LAUNCH_CHECK();
-        return g;
-    }
-    if (kind == 2) {
-        int g = (int)op.n_tiles;
-        if (g > 0) k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
-        SPFD_LAUNCH_CHECK();
-        return g;
-    }
-    static int max_dyn = -1;
-    if (max_dyn < 0) {
-        int dev = 0, optin = 0;
-        SPFD_CUDA(cudaGetDevice(&dev));
-        SPFD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        cudaFuncAttributes fa;
-        SPFD_CUDA(cudaFuncGetAttributes(&fa, k_plane<R, MODE, DOT>));
-        max_dyn = optin - (int)fa.sharedSizeBytes;
-        SPFD_CUDA(cudaFuncSetAttribute(k_plane<R, MODE, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
-    }
-    PlaneGeo g = plane_geometry<R, MODE>(op);
-    size_t smem = plane_smem<R, MODE>(g);
-    SPFD_CHECK(smem <= (size_t)max_dyn, SPFD_EINVAL, "x-extent too large for the plane kernel");
-    int grid = g.jblocks * g.kblocks;
-    k_plane<R, MODE, DOT><<<grid, kPlaneThreads, smem, s>>>(v, g, a);
+    int g = (int)op.n_tiles;
+    if (g > 0) k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
     SPFD_LAUNCH_CHECK();
-    return grid;
+    return g;
 }
 
 // returns number of partial blocks written when DOT
@@ -1343,56 +944,6 @@ void level_apply(Amg &h, int l, int mode, const double *x, const double *r, doub
 
 template <int R>
 void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s);
-
-// first level handled by the cooperative tail kernel (0 = none)
-int tail_level(const Amg &h) {
-    static int enabled = -1;
-    if (enabled < 0) {
-        const char *e = getenv("SPFD_TAIL");
-        // measured slower than the per-level kernels on C3 (grid barriers
-        // cost more than the launches they replace): opt-in
-        enabled = (e && std::string(e) == "1") ? 1 : 0;
-    }
-    const int nl = (int)h.lv.size();
-    if (!enabled || h.pre > 1 || h.post != 1 || nl < 3) return 0;
-    for (int l = 1; l < nl - 1; ++l)
-        if (h.lv[l].n <= 150000 && nl - 1 - l <= kTailMax) return l;
-    return 0;
-}
-
-template <int R>
-void run_tail(Amg &h, int l0, const double *r, double *z, cudaStream_t s) {
-    const int nl = (int)h.lv.size();
-    TailArgs t{};
-    t.nlev = nl - 1 - l0;
-    for (int i = 0; i < t.nlev; ++i) {
-        Level &L = h.lv[l0 + i];
-        TailLevel &T = t.lv[i];
-        T.A = view(L.A); T.P = view(L.P); T.R = view(L.R);
-        T.od = L.odinv.get();
-        T.r = i == 0 ? const_cast<double *>(r) : L.vr.get();
-        T.x = i == 0 ? z : L.vx.get();
-        T.d = L.vd.get();
-        T.gA = std::min(L.a_group, 32); T.gP = std::min(L.p_group, 32); T.gR = std::min(L.r_group, 32);
-    }
-    Level &C = h.lv[nl - 1];
-    t.cinv = h.cinv.get();
-    t.nc = h.nc;
-    t.rc = C.vr.get();
-    t.zc = C.vx.get();
-    static int blocks = 0;
-    if (blocks == 0) {
-        int dev = 0, sms = 0, per = 0;
-        SPFD_CUDA(cudaGetDevice(&dev));
-        SPFD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        SPFD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tail<R>, 256, 0));
-        blocks = sms * (per < 4 ? per : 4);
-        if (blocks < 1) blocks = 1;
-    }
-    void *args[] = {&t};
-    SPFD_CUDA(cudaLaunchCooperativeKernel((const void *)k_tail<R>, blocks, 256, args, 0, s));
-    SPFD_LAUNCH_CHECK();
-}
 
 // Fine level of a structured hierarchy, transfers matrix-free through the
 // aggregates (P = (I - omega D^-1 A) T, R = P^T):
@@ -1472,10 +1023,6 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
     }
     if (l == 0 && h.structured) {
         h.vc_partials = vcycle_fine_mf<R>(h, r, z, s);
-        return;
-    }
-    if (l > 0 && l == tail_level(h)) {
-        run_tail<R>(h, l, r, z, s);
         return;
     }
     double *d = L.vd.get(), *t = L.vt.get();
@@ -1695,6 +1242,19 @@ void pcg_body(Amg &h, cudaGraphConditionalHandle hnd, cudaStream_t s) {
     k_check<<<1, 1, 0, s>>>(sc, R, h.pcg_trace.get(), hnd);
     SPFD_LAUNCH_CHECK();
 }
+
+}  // namespace
+
+void amg_drop_graphs(Amg &h) {
+    for (int R = 0; R < 3; ++R) {
+        if (h.pcg_exec[R]) cudaGraphExecDestroy(h.pcg_exec[R]);
+        h.pcg_exec[R] = nullptr;
+        h.pcg_body_launches[R] = 0;
+        h.pcg_kind[R] = -1;
+    }
+}
+
+namespace {
 
 // Returns false (host-loop PCG) when the body cannot be captured; the reason
 // goes to stderr with SPFD_DEBUG=1.

@@ -88,10 +88,11 @@ class Session:
     def voxel_indices(self):
         return self.op.export(_lib.EXPORT_VOXEL_INDICES)
 
-    def snapshot(self, a, keep_psi: bool = False, stream=None, vox_out=None):
+    def snapshot(self, a, keep_psi: bool = False, stream=None, vox_out=None, cfg: SolveConfig | None = None):
         """One snapshot from device-resident edge potentials `a`
         ((nrhs, n_edges) CUDA float64).  Returns (voxel |E| (nrhs, n_vox)
-        CUDA tensor, SolveReport, psi or None)."""
+        CUDA tensor, SolveReport, psi or None).  `cfg` overrides the
+        session's solver settings (tolerance, method) for this call."""
         if not (isinstance(a, torch.Tensor) and a.is_cuda and a.dtype == torch.float64):
             raise ValueError("snapshot() takes a CUDA float64 tensor; use snapshot_host() for numpy input")
         if a.dim() == 1:
@@ -109,16 +110,17 @@ class Session:
                 raise ValueError("vox_out must be a CUDA float64 tensor shaped like the voxel field buffer")
             vbuf = vox_out
         rep = _lib.Report()
+        c = self._c if cfg is None else _lib.make_config(cfg)
         _lib.check(_lib.load().spfd_snapshot(self.op.handle, self.hierarchy.handle, _lib.ptr(a), self.omega,
                                              _lib.ptr(self._psi) if keep_psi else ctypes.c_void_p(0),
-                                             _lib.ptr(vbuf), nrhs, ctypes.byref(self._c), ctypes.byref(rep),
+                                             _lib.ptr(vbuf), nrhs, ctypes.byref(c), ctypes.byref(rep),
                                              _lib.stream_ptr(stream)))
         rels = tuple(float(rep.rel_residual[k]) for k in range(nrhs))
         report = SolveReport(iterations=int(rep.iterations), rel_residual=max(rels), converged=bool(rep.converged),
                              setup_seconds=self.hierarchy.setup_seconds, solve_seconds=float(rep.solve_seconds),
                              level_sizes=list(self.hierarchy.level_sizes),
                              peak_matrix_memory_bytes=self.hierarchy.matrix_memory_bytes(), rel_residuals=rels,
-                             method=self.cfg.method)
+                             method=(cfg or self.cfg).method)
         if not report.converged:
             raise PipelineError("solve", f"solver did not converge: residual {report.rel_residual:.3e} "
                                          f"after {report.iterations} iterations")

@@ -1,6 +1,5 @@
-"""GPU A/B of the fine-level stencil kernels (flat per-position k_span, its
-lane-shuffle variant k_spx, the neighbour-coded k_spc, the z-march
-cp.async plane-ring kernel k_zm and its bulk-copy (TMA) variant k_zt).
+"""GPU A/B of the fine-level stencil kernels (flat per-position k_span and
+the row-segment kernel k_seg).
 
 Every stencil mode must be bit-identical between the two kernels, so a
 V-cycle (pre-smooth+defect, restriction input, matrix-free prolongation,
@@ -19,8 +18,8 @@ from conftest import golden_cases, golden_model, load_golden
 
 pytestmark = pytest.mark.gpu
 
-FLAT, ZMARCH, SPX, CODED, ZTMA = 2, 4, 5, 6, 7
-KINDS = (FLAT, ZMARCH, SPX, CODED, ZTMA)
+FLAT, SEG = 2, 8
+KINDS = (FLAT, SEG)
 
 
 def _set_kernel(kind):

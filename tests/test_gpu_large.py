@@ -43,6 +43,11 @@ def test_snapshot_matches_oracle(name):
         assert rel <= 1e-8                                      # independent residual
         cfg = oracle.OracleSolveConfig(rel_tol=1e-8)
         h = oracle.amg_setup(a, cfg)
+        if c == 0:   # the device hierarchy is the reference's, level by level
+            hd = sess.hierarchy
+            assert hd.level_sizes == h["sizes"]
+            for lvl in range(len(h["sizes"]) - 1):
+                assert np.array_equal(hd.levels[lvl].aggregates, h["levels"][lvl]["agg"]), lvl
         x, its, rel_o, conv = oracle.fgmres(a, sysd["rhs"], h, cfg)
         assert conv
         v = oracle.edge_voltages(w.a[c], x, sysd["dof_to_node"], w.model.dims, w.omega)

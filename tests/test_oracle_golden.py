@@ -35,6 +35,8 @@ def test_conductance_and_assembly_bit_exact(case):
     assert np.array_equal(sysd["pinned"], d["pinned"])
     assert np.array_equal(sysd["labels"], d["labels"])
     assert sysd["n_components"] == int(d["n_components"])
+    # the RHS-only helper (second rhs of a pair without re-assembly) is the same bincount
+    assert np.array_equal(oracle.assemble_rhs(sysd, kappa.shape, d["a"]), d["rhs"])
 
 
 @pytest.mark.parametrize("case", MODEL_CASES)
