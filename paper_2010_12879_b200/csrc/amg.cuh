@@ -78,6 +78,14 @@ struct Amg {
     int pcg_kind[3] = {-1, -1, -1};         // fine-kernel kind captured in each graph
     DevBuf<double> pcg_trace;               // [cap_iters * 2] per-iteration residual estimates
     int64_t pcg_trace_cap = 0;
+    // FGMRES restart cycle as one graph per rhs count (fgmres_graph.cuh)
+    cudaStream_t cap2 = nullptr;            // second capture stream (conditional step bodies)
+    cudaGraphExec_t fg_exec[3] = {nullptr, nullptr, nullptr};
+    int fg_exec_m[3] = {0, 0, 0};
+    bool fg_failed[3] = {false, false, false};
+    DevBuf<double> fg_state, fg_y, fg_gram, fg_trace;
+    DevBuf<int> fg_jc;
+    int64_t fg_trace_cap = 0;
     Amg() = default;
     Amg(const Amg &) = delete;
     Amg &operator=(const Amg &) = delete;

@@ -67,6 +67,7 @@ int spfd_op_create(const int64_t *h_dims, const double *h_spacing, const uint16_
         SPFD_CHECK(out != nullptr && h_dims != nullptr && h_spacing != nullptr, SPFD_EINVAL, "null argument");
         Operator *op = op_create(h_dims, h_spacing, ids, lut, lut_len, pin, S(stream));
         *out = new spfd_op_s{op};
+        pool_trim();
     });
 }
 
@@ -179,6 +180,7 @@ int spfd_amg_setup_op(spfd_op_t h, const spfd_config *cfg, void *stream, spfd_am
         SPFD_CHECK(h->op->n_dofs >= 1, SPFD_EEMPTY, "empty Poisson system");
         Amg *a = amg_setup_op(h->op, *cfg, S(stream));
         *out = new spfd_amg_s{a, h->op};
+        pool_trim();
     });
 }
 
@@ -189,6 +191,7 @@ int spfd_amg_setup_csr(int64_t n, int64_t nnz, const int64_t *indptr, const int3
         check_cfg(cfg);
         Amg *a = amg_setup_csr(n, nnz, indptr, indices, data, *cfg, S(stream));
         *out = new spfd_amg_s{a, nullptr};
+        pool_trim();
     });
 }
 
@@ -321,6 +324,7 @@ int spfd_amg_distribute(spfd_amg_t h, spfd_comm_t c, int64_t replicate_below, in
         SPFD_CHECK(h && c && h_range, SPFD_EINVAL, "null argument");
         SPFD_CHECK(h->amg->dist == nullptr, SPFD_EINVAL, "hierarchy already distributed");
         amg_distribute(*h->amg, c->comm, replicate_below, h_range, S(stream));
+        pool_trim();
     });
 }
 
@@ -333,7 +337,7 @@ int spfd_bench_kernel(spfd_amg_t h, int which, int reps, int nrhs, double *h_ms,
 
 int spfd_set_fine_kernel(int kind) {
     return guarded([&] {
-        SPFD_CHECK(kind == -1 || kind == 2 || kind == 8, SPFD_EINVAL, "fine kernel kind must be -1, 2 or 8");
+        SPFD_CHECK(kind == -1 || kind == 2, SPFD_EINVAL, "fine kernel kind must be -1 or 2");
         g_fine_kind_override = kind;
     });
 }

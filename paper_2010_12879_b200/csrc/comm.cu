@@ -34,9 +34,10 @@ struct NcclApi {
 NcclApi &nccl() {
     static NcclApi api;
     if (api.h) return api;
+    // SPFD_NCCL_LIB (the Python side sets it to the nvidia-nccl wheel's library
+    // when it is not set, distributed.py), else the loader's search path
     const char *env = getenv("SPFD_NCCL_LIB");
-    const char *cands[] = {env, "libnccl.so.2",
-                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    const char *cands[] = {env, "libnccl.so.2"};
     for (const char *c : cands) {
         if (!c) continue;
         api.h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);

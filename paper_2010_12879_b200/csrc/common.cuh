@@ -45,6 +45,39 @@ void count_launch();
 // ------------------------------------------------------- device buffers --
 // RAII device allocation (stream-ordered).  Handles own their buffers; the
 // Python side owns every input/output tensor.
+// The library's private stream-ordered memory pool on the current device
+// (created on first use; null if the driver has no pool support).
+inline cudaMemPool_t lib_pool() {
+    static cudaMemPool_t pools[64] = {};
+    static bool made[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (!made[dev]) {
+        made[dev] = true;
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+            cudaGetLastError();
+            pools[dev] = nullptr;
+        } else {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+    return pools[dev];
+}
+
+// Return the pool's unused reservations (setup temporaries) to the device.
+inline void pool_trim() {
+    if (cudaMemPool_t pool = lib_pool()) {
+        cudaDeviceSynchronize();
+        cudaMemPoolTrimTo(pool, 0);
+    }
+}
+
 template <class T>
 struct DevBuf {
     T *p = nullptr;
@@ -58,21 +91,25 @@ struct DevBuf {
         return *this;
     }
     ~DevBuf() { release(); }
-    // Device memory comes from the device's default stream-ordered pool with
-    // an unlimited release threshold: setup allocates and frees many large
-    // temporaries (SpGEMM expansions, sorts), and recycling pool memory avoids
-    // re-mapping pages every time (plain cudaMalloc/cudaFree made the C3
-    // setup vary between 2 and 12 s).  Frees first synchronise the device,
-    // like cudaFree, so no stream can still be using the buffer.
+    // Device memory comes from the library's own stream-ordered pool (one per
+    // device, unlimited release threshold): setup allocates and frees many
+    // large temporaries (SpGEMM expansions, sorts), and recycling pool memory
+    // avoids re-mapping pages every time (plain cudaMalloc/cudaFree made the C3
+    // setup vary between 2 and 12 s).  The pool is private, so the default
+    // pool other libraries (PyTorch's cudaMallocAsync backend) use keeps its
+    // own policy, and pool_trim() hands the setup temporaries back at the end
+    // of every setup entry point.  Frees first synchronise the device, like
+    // cudaFree, so no stream can still be using the buffer.
     void alloc(size_t count) {
         release();
         if (count == 0) count = 1;
-        pool_init();
-        cudaError_t e = cudaMallocAsync(&p, count * sizeof(T), 0);
+        cudaMemPool_t pool = lib_pool();
+        cudaError_t e = pool ? cudaMallocFromPoolAsync((void **)&p, count * sizeof(T), pool, 0)
+                             : cudaMallocAsync((void **)&p, count * sizeof(T), 0);
         if (e == cudaSuccess) e = cudaStreamSynchronize(0);
         if (e != cudaSuccess) {
             p = nullptr;
-            throw Error(SPFD_ENOMEM, std::string("cudaMallocAsync failed: ") + cudaGetErrorString(e));
+            throw Error(SPFD_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
         }
         n = count;
     }
@@ -83,17 +120,6 @@ struct DevBuf {
         }
         p = nullptr;
         n = 0;
-    }
-    static void pool_init() {
-        static bool done = false;
-        if (done) return;
-        done = true;
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
     }
     size_t bytes() const { return n * sizeof(T); }
     T *get() const { return p; }

@@ -544,6 +544,7 @@ static void ensure_clean_amg(Field &F, cudaStream_t s) {
     c.max_nrhs = 1;
     F.clean_amg = amg_setup_csr(nc, nnz, ptr.get(), col.get(), val.get(), c, s);
     F.clean_setup_seconds = F.clean_amg->setup_seconds;
+    pool_trim();
 }
 
 void field_clean(Field &F, const double *in, double *out, double tol, spfd_clean_info *info, cudaStream_t s) {

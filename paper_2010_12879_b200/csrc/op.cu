@@ -206,59 +206,6 @@ __global__ void k_tile_rows(const int4 *rows, int64_t n_rows, int64_t n_tiles, i
     }
 }
 
-// Row segments: every row is cut into chunks of 32 consecutive positions,
-// one warp work item each.  A segment record holds everything a warp needs
-// to find the six neighbours of its lanes without the row table:
-//   a = {p0, dym, dyp, dzm}   first position; position deltas to the -y, +y,
-//                             -z neighbour rows (neighbour = own position + d)
-//   b = {dzp, n | xm0 << 8 | xpl << 9, lanes(-y) | lanes(+y) << 16,
-//        lanes(-z) | lanes(+z) << 16}
-// n = lanes in use; xm0 / xpl: lane 0 has a -x / lane n-1 has a +x
-// neighbour; lanes(.) = [first, end) lane range (bytes) holding that
-// neighbour (empty = 0, 0).
-__global__ void k_seg_count(const int4 *rows, int64_t n_rows, int *cnt) {
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        int len = rows[r].z - rows[r].y;
-        cnt[r] = (len + 31) / 32;
-    }
-}
-
-__device__ __forceinline__ int seg_delta(int4 q, int4 qn, int i0, int n, int *lanes) {
-    int a = qn.y - i0, b = qn.z - i0;
-    a = a < 0 ? 0 : (a > n ? n : a);
-    b = b < 0 ? 0 : (b > n ? n : b);
-    if (a >= b) { a = 0; b = 0; }
-    *lanes = a | (b << 8);
-    return (qn.x - qn.y) - (q.x - q.y);
-}
-
-__global__ void k_seg_fill(const int4 *rows, int64_t n_rows, int NY, const int *off, int4 *segs) {
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        const int4 q = rows[r];
-        const int j = q.w;
-        const int4 none = make_int4(0, 0, 0, 0);
-        const int4 qym = j > 0 ? rows[r - 1] : none;
-        const int4 qyp = j + 1 < NY ? rows[r + 1] : none;
-        const int4 qzm = r >= NY ? rows[r - NY] : none;
-        const int4 qzp = r + NY < n_rows ? rows[r + NY] : none;
-        int o = off[r];
-        for (int s = 0; s < q.z - q.y; s += 32, ++o) {
-            const int i0 = q.y + s;
-            const int n = min(32, q.z - i0);
-            int lym, lyp, lzm, lzp;
-            const int dym = seg_delta(q, qym, i0, n, &lym);
-            const int dyp = seg_delta(q, qyp, i0, n, &lyp);
-            const int dzm = seg_delta(q, qzm, i0, n, &lzm);
-            const int dzp = seg_delta(q, qzp, i0, n, &lzp);
-            const int flags = n | ((i0 > q.y) << 8) | ((i0 + n < q.z) << 9);
-            segs[2 * o] = make_int4(q.x + s, dym, dyp, dzm);
-            segs[2 * o + 1] = make_int4(dzp, flags, lym | (lyp << 16), lzm | (lzp << 16));
-        }
-    }
-}
-
 // Sum of the <= 4 voxel conductivities around an edge in the reference's
 // (da, db) order, then *0.25, then *geom (fit_operators.py:289-324).
 __device__ __forceinline__ double kap(const uint16_t *ids, const double *lut, Geo g, int i, int j,
@@ -529,20 +476,6 @@ Operator *op_create(const int64_t *dims, const double *spacing, const uint16_t *
         op->rows.alloc(op->n_rows + 1);
         k_rows_pack<<<grid_for(op->n_rows + 1, T), T, 0, s>>>(lo.get(), hi.get(), off.get(), op->n_rows,
                                                              op->L, (int)op->NY, op->rows.get());
-        {
-            DevBuf<int> icnt, ioff;
-            icnt.alloc(op->n_rows + 1);
-            ioff.alloc(op->n_rows + 1);
-            SPFD_CUDA(cudaMemsetAsync(icnt.get() + op->n_rows, 0, sizeof(int), s));
-            k_seg_count<<<grid_for(op->n_rows, T), T, 0, s>>>(op->rows.get(), op->n_rows, icnt.get());
-            SPFD_LAUNCH_CHECK();
-            exclusive_scan(icnt.get(), ioff.get(), op->n_rows + 1, s);
-            op->n_segs = read_scalar(ioff.get() + op->n_rows, s);
-            op->segs.alloc(2 * op->n_segs + 2);
-            k_seg_fill<<<grid_for(op->n_rows, T), T, 0, s>>>(op->rows.get(), op->n_rows, (int)op->NY, ioff.get(),
-                                                            op->segs.get());
-            SPFD_LAUNCH_CHECK();
-        }
         op->n_tiles = (op->L + kTile - 1) / kTile;
         op->tile_row.alloc(op->n_tiles + 1);
         k_tile_rows<<<grid_for(op->n_tiles + 1, T), T, 0, s>>>(op->rows.get(), op->n_rows, op->n_tiles,

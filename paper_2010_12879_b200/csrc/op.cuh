@@ -28,8 +28,6 @@ struct Operator {
 
     DevBuf<int4> rows;               // [n_rows+1] {off, lo, hi, j|k<<?>}  (sentinel at end)
     DevBuf<int32_t> tile_row;        // [n_tiles+1] first row of each tile
-    DevBuf<int4> segs;               // [2*n_segs] row segments: 32-position warp work items (seg.cuh)
-    int64_t n_segs = 0;
     DevBuf<double> wx, wy, wz;       // [L] edge conductance of the +axis edge at each position
     DevBuf<double> diag;             // [L] reference-order diagonal (0 for non-DOF)
     DevBuf<double> dinv;             // [L] 1/diag (0 for non-DOF)
@@ -42,7 +40,7 @@ struct Operator {
     DevBuf<int32_t> nnz_row;         // [N+1] CSR row pointer cache (int32 counts, built lazily)
     DevBuf<double> ws_a, ws_b;       // span workspaces [L*2]
     int64_t device_bytes() const {
-        return rows.bytes() + tile_row.bytes() + segs.bytes() + wx.bytes() + wy.bytes() + wz.bytes() +
+        return rows.bytes() + tile_row.bytes() + wx.bytes() + wy.bytes() + wz.bytes() +
                diag.bytes() + dinv.bytes() + dofmask.bytes() + pos_to_dof.bytes() +
                dof_to_pos.bytes() + pinned.bytes() + vox_cond.bytes() + vrow_off.bytes() +
                nnz_row.bytes() + ws_a.bytes() + ws_b.bytes();
@@ -53,8 +51,6 @@ struct Operator {
 struct SpanView {
     const int4 *rows;
     const int32_t *tile_row;
-    const int4 *segs;        // row segments (2 int4 each, see k_seg_fill)
-    int64_t n_segs;
     const double *wx, *wy, *wz;
     const uint32_t *mask;
     int64_t L;
@@ -63,7 +59,7 @@ struct SpanView {
 };
 
 inline SpanView span_view(const Operator &op) {
-    return SpanView{op.rows.get(), op.tile_row.get(), op.segs.get(), op.n_segs, op.wx.get(), op.wy.get(), op.wz.get(),
+    return SpanView{op.rows.get(), op.tile_row.get(), op.wx.get(), op.wy.get(), op.wz.get(),
                     op.dofmask.get(), op.L, (int)op.NY, (int)op.n_rows};
 }
 

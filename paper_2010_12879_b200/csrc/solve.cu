@@ -221,70 +221,6 @@ __global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a
     }
 }
 
-// Segment kernel: one warp per row segment of <= 32 consecutive positions
-// (op.cu k_seg_fill).  The segment record gives every lane its six
-// neighbour positions directly (no row-table search or neighbour-row record
-// gathers), so a lane's loads depend on one uniform record load only; a CTA
-// takes kSegPerCta consecutive segments.  Same per-point arithmetic as
-// k_span (point_out): bit-identical outputs; the DOT partials are per CTA
-// in a fixed order (bitwise reproducible, CTA cut differs from k_span).
-constexpr int kSegWarps = 8;
-constexpr int kSegPerWarp = 4;
-constexpr int kSegPerCta = kSegWarps * kSegPerWarp;
-
-__device__ __forceinline__ bool lane_in(int lanes, int l) { return l >= (lanes & 255) && l < ((lanes >> 8) & 255); }
-
-template <int R, int MODE, bool DOT>
-__global__ void __launch_bounds__(kSegWarps * 32) k_seg(SpanView v, SpanArgs a, int64_t s0, int64_t s1) {
-    using W = V<R>;
-    using T = typename W::T;
-    __shared__ double red[32 * R];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double dot[R];
-#pragma unroll
-    for (int c = 0; c < R; ++c) dot[c] = 0.0;
-    const int64_t base = s0 + (int64_t)blockIdx.x * kSegPerCta + warp;
-    for (int u = 0; u < kSegPerWarp; ++u) {
-        const int64_t sg = base + u * kSegWarps;
-        if (sg >= s1) break;
-        const int4 ra = v.segs[2 * sg], rb = v.segs[2 * sg + 1];
-        const int n = rb.y & 255;
-        if (lane >= n) continue;
-        const int p = ra.x + lane;
-        Nbr nb;
-        nb.wxp = v.wx[p]; nb.wyp = v.wy[p]; nb.wzp = v.wz[p];
-        nb.pxm = (lane > 0 || (rb.y & 256)) ? p - 1 : -1;
-        nb.pxp = (lane + 1 < n || (rb.y & 512)) ? p + 1 : -1;
-        nb.pym = lane_in(rb.z & 0xffff, lane) ? p + ra.y : -1;
-        nb.pyp = lane_in(rb.z >> 16, lane) ? p + ra.z : -1;
-        nb.pzm = lane_in(rb.w & 0xffff, lane) ? p + ra.w : -1;
-        nb.pzp = lane_in(rb.w >> 16, lane) ? p + rb.x : -1;
-        nb.wxm = nb.pxm >= 0 ? v.wx[nb.pxm] : 0.0;
-        nb.wym = nb.pym >= 0 ? v.wy[nb.pym] : 0.0;
-        nb.wzm = nb.pzm >= 0 ? v.wz[nb.pzm] : 0.0;
-        // reference diagonal order: tail edges x, y, z then head edges x, y, z
-        nb.diag = add_rn(add_rn(add_rn(add_rn(add_rn(nb.wxp, nb.wyp), nb.wzp), nb.wxm), nb.wym), nb.wzm);
-        const bool dof = mbit(v.mask, p);
-        T out = point_out<R, MODE>(a, nb, p);
-        if (!dof) out = W::zero();
-        W::st(a.y, p, out);
-        if (DOT) {
-#pragma unroll
-            for (int c = 0; c < R; ++c) {
-                if (MODE == 0) dot[c] += W::dot(W::ld(a.x, p), out, c);
-                else if (MODE == 3) dot[c] += W::dot(W::ld(a.r, p), out, c);
-                else dot[c] += W::dot(out, out, c);
-            }
-        }
-    }
-    if (DOT) {
-        block_sum<R>(dot, red);
-        if (threadIdx.x == 0)
-#pragma unroll
-            for (int c = 0; c < R; ++c) a.partials[blockIdx.x * R + c] = dot[c];
-    }
-}
-
 // Restriction r_c = T^T u: sequential sum over each aggregate's member
 // positions (ascending) -- deterministic, no atomics.  Optionally also
 // writes x0_c = od_c * r_c, the next level's implicit first Jacobi sweep.
@@ -837,7 +773,7 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
     int64_t n = nvec0 * R;
     h.kx.alloc(n); h.kr.alloc(n); h.kz.alloc(n); h.kp.alloc(n); h.kq.alloc(n); h.kb.alloc(n);
     int64_t np = kDotGrid;
-    if (h.structured) np = std::max<int64_t>(np, std::max<int64_t>(h.op->n_tiles, h.op->n_segs / 32 + 1));
+    if (h.structured) np = std::max<int64_t>(np, h.op->n_tiles);
     np = std::max<int64_t>(np, 148 * 16);
     np = std::max<int64_t>(np, (int64_t)kDotGrid * 8);  // batched FGMRES block dots (k_mdot, 8 vectors)
     h.partials.alloc(np * 2 + 64);
@@ -860,18 +796,11 @@ int g_fine_kind_override = -1;
 
 namespace {
 
-// fine-level stencil kernel: 2 = flat per-position k_span, 8 = row-segment
-// k_seg (default)
+// fine-level stencil kernel: 2 = flat per-position k_span (the only one
+// kept; round-1/2 variants measured slower are documented in DESIGN.md)
 int fine_kernel_kind() {
     if (g_fine_kind_override >= 0) return g_fine_kind_override;
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SPFD_SPAN_KERNEL");
-        v = 8;
-        if (e && std::string(e) == "flat") v = 2;
-        if (e && std::string(e) == "seg") v = 8;
-    }
-    return v;
+    return 2;
 }
 
 // Launch one fine-level stencil pass over the owned positions [a.pb, a.pe).
@@ -886,12 +815,6 @@ int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
         b.tile0 = t0;
         int g = t1 - t0;
         if (g > 0) k_span<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, b);
-        SPFD_LAUNCH_CHECK();
-        return g;
-    }
-    if (fine_kernel_kind() == 8) {
-        const int g = (int)((op.n_segs + kSegPerCta - 1) / kSegPerCta);
-        if (g > 0) k_seg<R, MODE, DOT><<<g, kSegWarps * 32, 0, s>>>(v, a, 0, op.n_segs);
         SPFD_LAUNCH_CHECK();
         return g;
     }
@@ -1251,6 +1174,9 @@ void amg_drop_graphs(Amg &h) {
         h.pcg_exec[R] = nullptr;
         h.pcg_body_launches[R] = 0;
         h.pcg_kind[R] = -1;
+        if (h.fg_exec[R]) cudaGraphExecDestroy(h.fg_exec[R]);
+        h.fg_exec[R] = nullptr;
+        h.fg_exec_m[R] = 0;
     }
 }
 
@@ -1427,7 +1353,10 @@ Amg::~Amg() {
     delete dist;
     for (auto &e : pcg_exec)
         if (e) cudaGraphExecDestroy(e);
+    for (auto &e : fg_exec)
+        if (e) cudaGraphExecDestroy(e);
     if (cap) cudaStreamDestroy(cap);
+    if (cap2) cudaStreamDestroy(cap2);
     if (side) cudaStreamDestroy(side);
     if (ev_alpha) cudaEventDestroy(ev_alpha);
     if (ev_x) cudaEventDestroy(ev_x);
@@ -1610,6 +1539,8 @@ __global__ void k_combine_r(int64_t n, int m, const int *jc, const double *y, co
     }
 }
 
+#include "fgmres_graph.cuh"
+
 template <int R>
 spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &cfg, double *h_trace,
                          cudaStream_t s) {
@@ -1645,16 +1576,14 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
     }
     if (all) { rep.converged = 1; return rep; }
     std::vector<double> H[R], cs[R], sn[R], g[R];
-    DevBuf<double> gram;  // per-rhs Gram matrix of the current cycle's basis
-    gram.alloc((size_t)R * (m + 1) * (m + 1));
+    fg_small_alloc(h);  // per-rhs Gram matrix, y and jc live in the hierarchy (no per-solve allocation)
+    DevBuf<double> &gram = h.fg_gram;
     for (int c = 0; c < R; ++c) {
         H[c].assign((size_t)(m + 1) * m, 0.0);
         cs[c].assign(m, 0.0); sn[c].assign(m, 0.0); g[c].assign(m + 1, 0.0);
     }
-    DevBuf<double> ydev;
-    ydev.alloc((int64_t)R * m);
-    DevBuf<int> jcdev;
-    jcdev.alloc(R);
+    DevBuf<double> &ydev = h.fg_y;
+    DevBuf<int> &jcdev = h.fg_jc;
     const int nparts = kDotGrid;
     int its = 0;
     int its_c[R];  // iterations each rhs took part in (fgmres1's count per rhs)
@@ -1680,7 +1609,7 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
             mult[c] = active[c] ? 1.0 / beta : 0.0;
         }
         if (!any) break;
-        SPFD_CUDA(cudaMemsetAsync(gram.get(), 0, gram.bytes(), s));
+        SPFD_CUDA(cudaMemsetAsync(gram.get(), 0, (size_t)R * (m + 1) * (m + 1) * sizeof(double), s));
         SPFD_CUDA(cudaMemcpyAsync(sc + SMUL, mult, R * sizeof(double), cudaMemcpyHostToDevice, s));
         k_scale_r<R><<<G, 256, 0, s>>>(n, sc + SMUL, r, Vb);
         int jc[R];
@@ -1963,10 +1892,15 @@ spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spf
         // exceeds its scalar workspace; else the reference's MGS per rhs
         const bool block = !(getenv("SPFD_FGMRES_BATCH") && std::string(getenv("SPFD_FGMRES_BATCH")) == "0") &&
                            cfg.restart <= 31;
-        if (nrhs == 1 && block) {
+        const bool graph = block && fgmres_graph_enabled();
+        if (nrhs == 1 && graph) {
+            rep = fgmres_graph<1>(h, b, x, cfg, h_trace, s);
+        } else if (nrhs == 1 && block) {
             rep = fgmres_batch<1>(h, b, x, cfg, h_trace, s);
         } else if (nrhs == 1) {
             rep = fgmres1(h, b, x, cfg, h_trace, s);
+        } else if (graph) {
+            rep = fgmres_graph<2>(h, b, x, cfg, h_trace, s);
         } else if (block) {
             rep = fgmres_batch<2>(h, b, x, cfg, h_trace, s);
         } else {

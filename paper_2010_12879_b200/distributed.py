@@ -18,6 +18,7 @@ GPU in tests.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -55,6 +56,22 @@ class HostTransport:
         return torch.cat(out)
 
 
+def _nccl_library_hint():
+    """Point the library's NCCL loader (dlopen, csrc/comm.cu) at the
+    nvidia-nccl wheel PyTorch uses, unless SPFD_NCCL_LIB is already set."""
+    if os.environ.get("SPFD_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl
+        for base in list(getattr(nvidia.nccl, "__path__", [])):
+            cand = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["SPFD_NCCL_LIB"] = cand
+                return
+    except ImportError:
+        pass
+
+
 class Communicator:
     """Owns a spfd_comm_t handle."""
 
@@ -68,6 +85,7 @@ class Communicator:
     def nccl(cls, group=None):
         """NCCL transport; rank 0 creates the unique id, torch.distributed
         broadcasts it."""
+        _nccl_library_hint()
         lib = _lib.load()
         rank, size = dist.get_rank(group), dist.get_world_size(group)
         uid = torch.zeros(128, dtype=torch.uint8)
