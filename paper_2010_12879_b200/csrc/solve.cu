@@ -181,13 +181,43 @@ __device__ __forceinline__ typename V<R>::T point_out(const SpanArgs &a, const N
 // MODE 3: y = x + od (r - A x) (+ partial r.y)   (Jacobi sweep)
 // MODE 4: y = base + e - od (A e), e = T ec      (matrix-free prolongation
 //         with P = (I - omega D^-1 A) T; base = od r when null)
-template <int R, int MODE, bool DOT, bool RANGED = false>
+// Bulk L2 prefetch (TMA engine, no registers) of the byte range
+// [p0, p1) * esz of a streamed array; 16-byte granules.
+__device__ __forceinline__ void l2_prefetch(const void *base, int64_t p0, int64_t p1, int esz) {
+    if (!base || p1 <= p0) return;
+    uintptr_t b = reinterpret_cast<uintptr_t>(base) + (uintptr_t)(p0 * esz);
+    uintptr_t e = reinterpret_cast<uintptr_t>(base) + (uintptr_t)(p1 * esz);
+    b = (b + 15) & ~(uintptr_t)15;
+    e &= ~(uintptr_t)15;
+    if (e <= b) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b), "r"((unsigned)(e - b)) : "memory");
+}
+
+// One thread of the CTA queues the tile's streamed (center-position) arrays
+// into L2, so the per-position dependent load chains below hit L2 instead
+// of waiting on DRAM (PF = true).
+template <int R, int MODE>
+__device__ __forceinline__ void tile_prefetch(const SpanView &v, const SpanArgs &a, int64_t p0, int64_t p1) {
+    l2_prefetch(v.wx, p0, p1, 8);
+    l2_prefetch(v.wy, p0, p1, 8);
+    l2_prefetch(v.wz, p0, p1, 8);
+    if (MODE == 0 || MODE == 1 || MODE == 3) l2_prefetch(a.x, p0, p1, 8 * R);
+    if (MODE != 0) l2_prefetch(a.r, p0, p1, 8 * R);
+    if (MODE >= 2) l2_prefetch(a.od, p0, p1, 8);
+    if (MODE == 4) { l2_prefetch(a.aggp, p0, p1, 4); l2_prefetch(a.base, p0, p1, 8 * R); }
+}
+
+template <int R, int MODE, bool DOT, bool RANGED = false, bool PF = false>
 __global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a) {
     using W = V<R>;
     using T = typename W::T;
     __shared__ double red[32 * R];
     const int t = RANGED ? a.tile0 + blockIdx.x : blockIdx.x;
     const int64_t pend = RANGED ? (a.pe < v.L ? a.pe : v.L) : v.L;
+    if (PF && threadIdx.x == 0) {
+        const int64_t q0 = (int64_t)t * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
+        tile_prefetch<R, MODE>(v, a, q0, q1);
+    }
     const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
     double dot[R];
 #pragma unroll
@@ -252,11 +282,21 @@ __global__ void k_agg_sum(const int64_t *mptr, const int32_t *mpos, int64_t n_ag
 // MODE 0: y = M x (aux: also od_aux * y);  1: y = r - M x;  2: y = r - M(odinv r);
 // MODE 3: y = x + odinv (r - M x);  4: y = odinv r + M e (prolongation, x=e)
 // MODE 5: y = base + M e (prolongation on a materialised smoother iterate)
+// L2 bulk prefetch of the column/value ranges of rows [row, row + n) (the
+// warp's next rows in the grid-stride loop).
+__device__ __forceinline__ void csr_prefetch(const CsrView &m, int64_t row, int n) {
+    if (row >= m.rows) return;
+    const int64_t e = row + n < m.rows ? row + n : m.rows;
+    const int64_t q0 = m.ptr[row], q1 = m.ptr[e];
+    l2_prefetch(m.col, q0, q1, 4);
+    l2_prefetch(m.val, q0, q1, 8);
+}
+
 template <int G, int R, int MODE, bool DOT>
 __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__restrict__ r,
                       const double *__restrict__ od, const double *__restrict__ base, double *__restrict__ y,
                       double *__restrict__ partials, const double *__restrict__ od_aux, double *__restrict__ aux,
-                      const int32_t *__restrict__ rowmap) {
+                      const int32_t *__restrict__ rowmap, int pf) {
     using W = V<R>;
     using T = typename W::T;
     __shared__ double red[32 * R];
@@ -269,6 +309,7 @@ __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__r
     for (int c = 0; c < R; ++c) dot[c] = 0.0;
     // warp-uniform trip count so the full-mask shuffles below are safe
     for (int64_t rbase = warp * GPW; rbase < m.rows; rbase += nwarp * GPW) {
+        if (pf && (threadIdx.x & 31) == 0) csr_prefetch(m, rbase + nwarp * GPW, GPW);
         const int64_t row = rbase + (threadIdx.x & 31) / G;
         const bool valid = row < m.rows;
         T acc = W::zero();
@@ -345,7 +386,7 @@ constexpr int kCsrThreads = 256;
 template <int G, int R>
 __global__ void __launch_bounds__(kCsrThreads) k_csr_pp(CsrView P, CsrView M, const double *__restrict__ e,
                                                        const double *__restrict__ r, const double *__restrict__ od,
-                                                       const double *__restrict__ d, double *__restrict__ z) {
+                                                       const double *__restrict__ d, double *__restrict__ z, int pf) {
     using W = V<R>;
     using T = typename W::T;
     const int lane = threadIdx.x % G;
@@ -353,6 +394,10 @@ __global__ void __launch_bounds__(kCsrThreads) k_csr_pp(CsrView P, CsrView M, co
     const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
     constexpr int GPW = 32 / G;
     for (int64_t rbase = warp * GPW; rbase < P.rows; rbase += nwarp * GPW) {
+        if (pf && (threadIdx.x & 31) == 0) {
+            csr_prefetch(P, rbase + nwarp * GPW, GPW);
+            csr_prefetch(M, rbase + nwarp * GPW, GPW);
+        }
         const int64_t row = rbase + (threadIdx.x & 31) / G;
         const bool valid = row < P.rows;
         T ap = W::zero(), am = W::zero();
@@ -494,6 +539,16 @@ __global__ void __launch_bounds__(kCsrThreads) k_csr_wide(CsrView m, const doubl
     }
 }
 
+// SPFD_CSR_PF=1: L2 bulk prefetch of the next rows in the CSR kernels (A/B)
+inline int csr_prefetch_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_CSR_PF");
+        v = (e && std::string(e) == "1") ? 1 : 0;
+    }
+    return v;
+}
+
 inline int csr_grid(int64_t rows, int G) {
     int64_t groups = G >= kCsrThreads ? 1 : (int64_t)kCsrThreads / G;
     int64_t g = (rows + groups - 1) / groups;
@@ -510,7 +565,8 @@ void launch_csr_g(const Csr &m, const double *x, const double *r, const double *
         k_csr_wide<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials, od_aux, aux,
                                                                  rowmap);
     else
-        k_csr<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials, od_aux, aux, rowmap);
+        k_csr<G, R, MODE, DOT><<<grid, kCsrThreads, 0, s>>>(view(m), x, r, od, base, y, partials, od_aux, aux, rowmap,
+                                                            csr_prefetch_enabled());
 }
 
 template <int R, int MODE, bool DOT>
@@ -796,11 +852,19 @@ int g_fine_kind_override = -1;
 
 namespace {
 
-// fine-level stencil kernel: 2 = flat per-position k_span (the only one
-// kept; round-1/2 variants measured slower are documented in DESIGN.md)
+// fine-level stencil kernel: 2 = flat per-position k_span, 3 = the same with
+// the tile's streamed arrays bulk-prefetched into L2 (round-1/2 variants
+// measured slower are documented in DESIGN.md)
 int fine_kernel_kind() {
     if (g_fine_kind_override >= 0) return g_fine_kind_override;
-    return 2;
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_SPAN_KERNEL");
+        v = 2;
+        if (e && std::string(e) == "flat") v = 2;
+        if (e && std::string(e) == "pf") v = 3;
+    }
+    return v;
 }
 
 // Launch one fine-level stencil pass over the owned positions [a.pb, a.pe).
@@ -814,12 +878,18 @@ int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
         SpanArgs b = a;
         b.tile0 = t0;
         int g = t1 - t0;
-        if (g > 0) k_span<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, b);
+        if (g > 0) {
+            if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, true, true><<<g, kSpanThreads, 0, s>>>(v, b);
+            else k_span<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, b);
+        }
         SPFD_LAUNCH_CHECK();
         return g;
     }
     int g = (int)op.n_tiles;
-    if (g > 0) k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
+    if (g > 0) {
+        if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, false, true><<<g, kSpanThreads, 0, s>>>(v, a);
+        else k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
+    }
     SPFD_LAUNCH_CHECK();
     return g;
 }
@@ -974,10 +1044,10 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
         // fused prolongation + post-smooth from the pre-smoothing defect d
         const int grid = csr_grid(L.P.rows, std::min(L.ap_group, 32));
         switch (std::min(L.ap_group, 32)) {
-            case 4: k_csr_pp<4, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z); break;
-            case 8: k_csr_pp<8, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z); break;
-            case 16: k_csr_pp<16, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z); break;
-            default: k_csr_pp<32, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z); break;
+            case 4: k_csr_pp<4, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z, csr_prefetch_enabled()); break;
+            case 8: k_csr_pp<8, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z, csr_prefetch_enabled()); break;
+            case 16: k_csr_pp<16, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z, csr_prefetch_enabled()); break;
+            default: k_csr_pp<32, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z, csr_prefetch_enabled()); break;
         }
         SPFD_LAUNCH_CHECK();
         return;
