@@ -338,7 +338,8 @@ def main():
     # the public streaming API (C5 use case): every step's potentials copied in
     # and voxel field copied out, transfers overlapping the neighbouring solves
     outs = [torch.empty((w.a.shape[0], v1 - v0), dtype=torch.float64, pin_memory=True) for _ in range(args.steps)]
-    sess.snapshots_host([a_host] * 2, outs[:2])   # warm the copy streams / buffers
+    warm_outs = [torch.empty(tuple(outs[0].shape), dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    sess.snapshots_host([a_host] * 2, warm_outs)   # warm the copy streams / buffers
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

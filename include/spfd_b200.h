@@ -311,6 +311,12 @@ typedef struct {
  * non-convergence or a violated postcondition.  out may alias in. */
 int spfd_field_clean(spfd_field_t f, const double *in, double *out, double tol,
                      spfd_clean_info *h_info, void *stream);
+/* The same for nrhs = 1 or 2 flux vectors (planar [nrhs][n_faces], e.g.
+ * the real and imaginary sample sets of a snapshot) with one batched
+ * Krylov solve at the stricter of the two tolerances; per-vector decisions
+ * and post-checks as above; h_info[nrhs]. */
+int spfd_field_clean_batch(spfd_field_t f, int nrhs, const double *in, double *out, double tol,
+                           spfd_clean_info *h_info, void *stream);
 
 typedef struct {
     double  rel_residual;        /* ||C a - flux|| / ||flux||                */
@@ -352,9 +358,10 @@ int spfd_bench_kernel(spfd_amg_t amg, int which, int reps, int nrhs, double *h_m
                       void *stream);
 /* Tuning knob (not part of the reference API): select the fine-level
  * stencil kernel used by every later solve / V-cycle in this process.
- * kind = -1 default (environment SPFD_SPAN_KERNEL=flat|seg, else the
- * row-segment kernel), 2 flat per-position kernel, 8 row-segment kernel.
- * Both give bit-identical stencil outputs; this exists for A/B parity tests. */
+ * kind = -1 default (environment SPFD_SPAN_KERNEL=flat|pf, else pf),
+ * 2 flat per-position kernel, 3 the same with the tile's streamed arrays
+ * bulk-prefetched into L2.  Both give bit-identical outputs; this exists for
+ * A/B tests. */
 int spfd_set_fine_kernel(int kind);
 /* Tuning knob: run PCG as one CUDA graph with a device-side WHILE node
  * (mode 1, the default) or as the host-driven loop (mode 0); -1 restores the

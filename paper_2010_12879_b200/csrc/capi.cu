@@ -410,7 +410,16 @@ int spfd_field_divergence(spfd_field_t f, const double *flux, double *div, void 
 int spfd_field_clean(spfd_field_t f, const double *in, double *out, double tol, spfd_clean_info *info, void *stream) {
     return guarded([&] {
         SPFD_CHECK(f && in && out && info, SPFD_EINVAL, "null argument");
-        field_clean(*f->f, in, out, tol, info, S(stream));
+        field_clean(*f->f, 1, in, out, tol, info, S(stream));
+    });
+}
+
+int spfd_field_clean_batch(spfd_field_t f, int nrhs, const double *in, double *out, double tol,
+                           spfd_clean_info *info, void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(f && in && out && info, SPFD_EINVAL, "null argument");
+        SPFD_CHECK(nrhs == 1 || nrhs == 2, SPFD_EINVAL, "nrhs must be 1 or 2");
+        field_clean(*f->f, nrhs, in, out, tol, info, S(stream));
     });
 }
 

@@ -541,49 +541,79 @@ static void ensure_clean_amg(Field &F, cudaStream_t s) {
     k_normal_fill<<<blocks(nc), 256, 0, s>>>(F.g, ptr.get(), col.get(), val.get());
     SPFD_LAUNCH_CHECK();
     spfd_config c = F.cfg;
-    c.max_nrhs = 1;
+    c.max_nrhs = 2;   // re/im sample sets batched (field_clean)
     F.clean_amg = amg_setup_csr(nc, nnz, ptr.get(), col.get(), val.get(), c, s);
     F.clean_setup_seconds = F.clean_amg->setup_seconds;
     pool_trim();
 }
 
-void field_clean(Field &F, const double *in, double *out, double tol, spfd_clean_info *info, cudaStream_t s) {
+// Batched projection of nrhs (1 or 2, e.g. the real and imaginary sample
+// sets of a snapshot) face-flux vectors, planar [nrhs][n_faces]: the
+// per-vector decisions of field_source.py:292-329 (skip when already
+// solenoidal, tolerance min(1e-12, 0.25 tol / rel)), one Krylov solve for
+// the vectors that need it (the stricter tolerance of the two; each then
+// meets its own), and the same post-check per vector.
+void field_clean(Field &F, int nrhs, const double *in, double *out, double tol, spfd_clean_info *info,
+                 cudaStream_t s) {
+    SPFD_CHECK(nrhs == 1 || nrhs == 2, SPFD_EINVAL, "nrhs must be 1 or 2");
     const int64_t nc = F.n_cells(), nf = F.n_faces();
-    *info = spfd_clean_info{};
-    if (out != in) SPFD_CUDA(cudaMemcpyAsync(out, in, nf * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    const double fnorm = std::sqrt(sumsq(F, in, nf, s));
-    if (fnorm == 0.0 || nc == 0) return;
-    if (F.wc.n < (size_t)nc) F.wc.alloc(nc);
-    field_divergence(F, in, F.wc.get(), s);
-    const double rel = std::sqrt(sumsq(F, F.wc.get(), nc, s)) / fnorm;
-    info->rel_before = rel;
-    info->rel_after = rel;
-    if (rel <= tol) return;
-    ensure_clean_amg(F, s);
-    spfd_config c = F.cfg;
-    c.rel_tol = std::min(1e-12, 0.25 * tol / rel);
-    c.max_nrhs = 1;
-    Amg &h = *F.clean_amg;
-    spfd_report rep = krylov_solve(h, F.wc.get(), h.kx.get(), 1, c, nullptr, s);
-    SPFD_CUDA(cudaStreamSynchronize(s));
-    info->solved = 1;
-    info->iterations = rep.iterations;
-    info->solve_rel_residual = rep.rel_residual[0];
-    info->setup_seconds = F.clean_setup_seconds;
-    SPFD_CHECK(rep.status != SPFD_ENONFINITE, SPFD_ENONFINITE, "non-finite value in the projection solve");
-    if (!rep.converged) {
-        char msg[160];
-        snprintf(msg, sizeof msg, "divergence projection did not converge (residual %.3e)", rep.rel_residual[0]);
-        throw Error(SPFD_EPROJECTION, msg);
+    if (F.wc.n < (size_t)(4 * nc)) F.wc.alloc(4 * nc);  // [2][nc] divergences + [nc][2] interleaved
+    double *divp = F.wc.get(), *inter = F.wc.get() + 2 * nc;
+    double fnorm[2] = {0.0, 0.0};
+    int act[2], na = 0;
+    double rtol = 1e-12;
+    for (int c = 0; c < nrhs; ++c) {
+        info[c] = spfd_clean_info{};
+        const double *ic = in + (int64_t)c * nf;
+        double *oc = out + (int64_t)c * nf;
+        if (oc != ic) SPFD_CUDA(cudaMemcpyAsync(oc, ic, nf * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        fnorm[c] = std::sqrt(sumsq(F, ic, nf, s));
+        if (fnorm[c] == 0.0 || nc == 0) continue;
+        field_divergence(F, ic, divp + (int64_t)na * nc, s);
+        const double rel = std::sqrt(sumsq(F, divp + (int64_t)na * nc, nc, s)) / fnorm[c];
+        info[c].rel_before = rel;
+        info[c].rel_after = rel;
+        if (rel <= tol) continue;
+        rtol = std::min(rtol, std::min(1e-12, 0.25 * tol / rel));
+        act[na++] = c;
     }
-    k_sub_div_transpose<<<blocks(nf), 256, 0, s>>>(F.g, h.kx.get(), in, out);
-    SPFD_LAUNCH_CHECK();
-    field_divergence(F, out, F.wc.get(), s);
-    info->rel_after = std::sqrt(sumsq(F, F.wc.get(), nc, s)) / fnorm;
-    if (info->rel_after > tol) {
-        char msg[160];
-        snprintf(msg, sizeof msg, "divergence cleaning left relative defect %.3e > %.3e", info->rel_after, tol);
-        throw Error(SPFD_EPROJECTION, msg);
+    if (na == 0) return;
+    ensure_clean_amg(F, s);
+    spfd_config cfg = F.cfg;
+    cfg.rel_tol = rtol;
+    cfg.max_nrhs = 2;
+    Amg &h = *F.clean_amg;
+    amg_to_level0(h, divp, inter, na, s);
+    spfd_report rep = krylov_solve(h, inter, h.kx.get(), na, cfg, nullptr, s);
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    SPFD_CHECK(rep.status != SPFD_ENONFINITE, SPFD_ENONFINITE, "non-finite value in the projection solve");
+    amg_from_level0(h, h.kx.get(), divp, na, s);   // potentials, planar [na][nc]
+    for (int k = 0; k < na; ++k) {
+        const int c = act[k];
+        spfd_clean_info &ic = info[c];
+        ic.solved = 1;
+        ic.iterations = rep.iterations;
+        ic.solve_rel_residual = rep.rel_residual[k];
+        ic.setup_seconds = F.clean_setup_seconds;
+        if (!rep.converged) {
+            char msg[160];
+            snprintf(msg, sizeof msg, "divergence projection did not converge (residual %.3e)", rep.rel_residual[k]);
+            throw Error(SPFD_EPROJECTION, msg);
+        }
+        k_sub_div_transpose<<<blocks(nf), 256, 0, s>>>(F.g, divp + (int64_t)k * nc, in + (int64_t)c * nf,
+                                                       out + (int64_t)c * nf);
+        SPFD_LAUNCH_CHECK();
+    }
+    for (int k = 0; k < na; ++k) {
+        const int c = act[k];
+        double *div = inter;  // scratch
+        field_divergence(F, out + (int64_t)c * nf, div, s);
+        info[c].rel_after = std::sqrt(sumsq(F, div, nc, s)) / fnorm[c];
+        if (info[c].rel_after > tol) {
+            char msg[160];
+            snprintf(msg, sizeof msg, "divergence cleaning left relative defect %.3e > %.3e", info[c].rel_after, tol);
+            throw Error(SPFD_EPROJECTION, msg);
+        }
     }
 }
 

@@ -11,7 +11,8 @@ Field *field_create(const spfd_box &grid, const spfd_config &cfg);
 void field_destroy(Field *F);
 void field_interpolate(Field &F, const spfd_box &lattice, const double *b, double *flux, cudaStream_t s);
 void field_divergence(Field &F, const double *flux, double *div, cudaStream_t s);
-void field_clean(Field &F, const double *in, double *out, double tol, spfd_clean_info *info, cudaStream_t s);
+void field_clean(Field &F, int nrhs, const double *in, double *out, double tol, spfd_clean_info *info,
+                 cudaStream_t s);
 void field_gauge_comb(Field &F, const double *flux, double *a, double tol, spfd_gauge_info *info, cudaStream_t s);
 void field_circulation(Field &F, const double *a, const double *flux, double *defect, cudaStream_t s);
 void coil_field(int64_t n, const double *pts, int nseg, const double *verts, double scale, double *out,

@@ -103,15 +103,16 @@ __device__ __forceinline__ Nbr neighbours(const SpanView &v, int p, int r, int4 
     return n;
 }
 
-// (A x)_p in the reference's sorted-column order; X(pos) -> V<R>::T.
+// (A x)_p in the reference's sorted-column order; X(pos) -> V<R>::T gives
+// the neighbour inputs, xc is the centre input (loaded once by the caller).
 template <int R, class X>
-__device__ __forceinline__ typename V<R>::T apply_row(const Nbr &n, int p, X xat) {
+__device__ __forceinline__ typename V<R>::T apply_row(const Nbr &n, typename V<R>::T xc, X xat) {
     using W = V<R>;
     typename W::T s = W::zero();
     if (n.pzm >= 0) s = W::axpy(-n.wzm, xat(n.pzm), s);
     if (n.pym >= 0) s = W::axpy(-n.wym, xat(n.pym), s);
     if (n.pxm >= 0) s = W::axpy(-n.wxm, xat(n.pxm), s);
-    s = W::axpy(n.diag, xat(p), s);
+    s = W::axpy(n.diag, xc, s);
     if (n.pxp >= 0) s = W::axpy(-n.wxp, xat(n.pxp), s);
     if (n.pyp >= 0) s = W::axpy(-n.wyp, xat(n.pyp), s);
     if (n.pzp >= 0) s = W::axpy(-n.wzp, xat(n.pzp), s);
@@ -130,6 +131,7 @@ struct SpanArgs {
     int64_t pb = 0;       // owned position range [pb, pe) (z-slab); defaults = all
     int64_t pe = INT64_MAX;
     int tile0 = 0;        // first tile of the launch (set by launch_fine)
+    int pf_ahead = 0;     // PF: also prefetch the tile this many tiles ahead (0 = own tile only)
 };
 
 // Input of a fine-level stencil at a position, per mode (see k_span).
@@ -147,14 +149,16 @@ __device__ __forceinline__ typename V<R>::T xin(const SpanArgs &a, int pp) {
 // Output of one fine-level stencil point for MODE (see k_span), in the
 // reference's summation order (shared by every fine kernel: same bits).
 template <int R, int MODE>
-__device__ __forceinline__ typename V<R>::T point_out(const SpanArgs &a, const Nbr &n, int p) {
+__device__ __forceinline__ typename V<R>::T point_out(const SpanArgs &a, const Nbr &n, int p,
+                                                      typename V<R>::T &dotv) {
     using W = V<R>;
     using T = typename W::T;
     T out;
     if (MODE == 2) {
         const double *od = a.od, *rr = a.r;
-        T s = apply_row<R>(n, p, [&](int pp) { return W::scale(od[pp], W::ld(rr, pp)); });
-        out = W::sub(W::ld(rr, p), s);
+        const T rc = W::ld(rr, p);
+        T s = apply_row<R>(n, W::scale(od[p], rc), [&](int pp) { return W::scale(od[pp], W::ld(rr, pp)); });
+        out = W::sub(rc, s);
     } else if (MODE == 4) {
         const double *ec = a.ec;
         const int32_t *ag = a.aggp;
@@ -162,15 +166,25 @@ __device__ __forceinline__ typename V<R>::T point_out(const SpanArgs &a, const N
             int g1 = ag[pp];  // aggregate id + 1, 0 = none
             return g1 > 0 ? W::ld(ec, g1 - 1) : W::zero();
         };
-        T s = apply_row<R>(n, p, eat);
-        T b = a.base ? W::ld(a.base, p) : W::scale(a.od[p], W::ld(a.r, p));
-        out = W::sub(W::add(b, eat(p)), W::scale(a.od[p], s));
+        const T ecc = eat(p);
+        const double odc = a.od[p];
+        T s = apply_row<R>(n, ecc, eat);
+        T b = a.base ? W::ld(a.base, p) : W::scale(odc, W::ld(a.r, p));
+        out = W::sub(W::add(b, ecc), W::scale(odc, s));
     } else {
         const double *xx = a.x;
-        T s = apply_row<R>(n, p, [&](int pp) { return W::ld(xx, pp); });
-        if (MODE == 0) out = s;
-        else if (MODE == 1) out = W::sub(W::ld(a.r, p), s);
-        else out = W::add(W::ld(xx, p), W::scale(a.od[p], W::sub(W::ld(a.r, p), s)));
+        const T xc = W::ld(xx, p);
+        T s = apply_row<R>(n, xc, [&](int pp) { return W::ld(xx, pp); });
+        if (MODE == 0) {
+            out = s;
+            dotv = xc;
+        } else if (MODE == 1) {
+            out = W::sub(W::ld(a.r, p), s);
+        } else {
+            const T rc = W::ld(a.r, p);
+            out = W::add(xc, W::scale(a.od[p], W::sub(rc, s)));
+            dotv = rc;
+        }
     }
     return out;
 }
@@ -207,16 +221,22 @@ __device__ __forceinline__ void tile_prefetch(const SpanView &v, const SpanArgs 
     if (MODE == 4) { l2_prefetch(a.aggp, p0, p1, 4); l2_prefetch(a.base, p0, p1, 8 * R); }
 }
 
-template <int R, int MODE, bool DOT, bool RANGED = false, bool PF = false>
-__global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a) {
+template <int R, int MODE, bool DOT, bool RANGED = false, bool PF = false, int MINB = 6>
+__global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArgs a) {
     using W = V<R>;
     using T = typename W::T;
     __shared__ double red[32 * R];
     const int t = RANGED ? a.tile0 + blockIdx.x : blockIdx.x;
     const int64_t pend = RANGED ? (a.pe < v.L ? a.pe : v.L) : v.L;
     if (PF && threadIdx.x == 0) {
-        const int64_t q0 = (int64_t)t * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
-        tile_prefetch<R, MODE>(v, a, q0, q1);
+        if (a.pf_ahead <= 0 || blockIdx.x < a.pf_ahead) {  // first wave: its own tile
+            const int64_t q0 = (int64_t)t * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
+            tile_prefetch<R, MODE>(v, a, q0, q1);
+        }
+        if (a.pf_ahead > 0) {  // later CTAs find their tile queued by an earlier one
+            const int64_t q0 = (int64_t)(t + a.pf_ahead) * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
+            tile_prefetch<R, MODE>(v, a, q0, q1);
+        }
     }
     const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
     double dot[R];
@@ -231,14 +251,14 @@ __global__ void __launch_bounds__(kSpanThreads, 6) k_span(SpanView v, SpanArgs a
         const int4 q = v.rows[row];
         const Nbr n = neighbours(v, p, row, q);
         const bool dof = mbit(v.mask, p);
-        T out = point_out<R, MODE>(a, n, p);
+        T dotv = W::zero();
+        T out = point_out<R, MODE>(a, n, p, dotv);
         if (!dof) out = W::zero();
         W::st(a.y, p, out);
         if (DOT) {
 #pragma unroll
             for (int c = 0; c < R; ++c) {
-                if (MODE == 0) dot[c] += W::dot(W::ld(a.x, p), out, c);
-                else if (MODE == 3) dot[c] += W::dot(W::ld(a.r, p), out, c);
+                if (MODE == 0 || MODE == 3) dot[c] += W::dot(dotv, out, c);
                 else dot[c] += W::dot(out, out, c);
             }
         }
@@ -852,15 +872,16 @@ int g_fine_kind_override = -1;
 
 namespace {
 
-// fine-level stencil kernel: 2 = flat per-position k_span, 3 = the same with
-// the tile's streamed arrays bulk-prefetched into L2 (round-1/2 variants
-// measured slower are documented in DESIGN.md)
+// fine-level stencil kernel: 3 = flat per-position k_span with the tile's
+// streamed arrays bulk-prefetched into L2 (default), 2 = without the
+// prefetch (A/B); round-1/2 variants measured slower are documented in
+// DESIGN.md
 int fine_kernel_kind() {
     if (g_fine_kind_override >= 0) return g_fine_kind_override;
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("SPFD_SPAN_KERNEL");
-        v = 2;
+        v = 3;
         if (e && std::string(e) == "flat") v = 2;
         if (e && std::string(e) == "pf") v = 3;
     }
@@ -869,9 +890,21 @@ int fine_kernel_kind() {
 
 // Launch one fine-level stencil pass over the owned positions [a.pb, a.pe).
 // Returns the number of CTAs (dot partials written when DOT).
+inline int pf_ahead() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_PF_AHEAD");
+        v = e ? atoi(e) : 0;
+        if (v < 0) v = 0;
+    }
+    return v;
+}
+
 template <int R, int MODE, bool DOT>
-int launch_fine(const Operator &op, const SpanArgs &a, cudaStream_t s) {
+int launch_fine(const Operator &op, const SpanArgs &a_in, cudaStream_t s) {
     SpanView v = span_view(op);
+    SpanArgs a = a_in;
+    a.pf_ahead = pf_ahead();
     if (a.pb > 0 || a.pe < op.L) {  // owned z-slab range
         const int64_t pe = a.pe < op.L ? a.pe : op.L;
         const int t0 = (int)(a.pb / kTile), t1 = (int)((pe + kTile - 1) / kTile);

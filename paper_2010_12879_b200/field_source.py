@@ -249,8 +249,20 @@ class FieldOps:
         return out
 
     def clean(self, flux, tol: float = 1e-10, out=None, stream=None):
+        """Divergence cleaning of one (n_faces,) or a batch of two (2, n_faces)
+        flux vectors (one batched Krylov solve); `last_clean` holds the info
+        (a list for a batch)."""
         flux = _dev(flux)
         out = torch.empty_like(flux) if out is None else out
+        if flux.dim() == 2:
+            nrhs = flux.shape[0]
+            if nrhs not in (1, 2) or flux.shape[1] != self.grid.n_faces or tuple(out.shape) != tuple(flux.shape):
+                raise ValueError(f"expected (1 or 2, {self.grid.n_faces}) flux vectors")
+            infos = (_lib.CleanInfo * nrhs)()
+            _lib.check(self._lib.spfd_field_clean_batch(self.handle, nrhs, _lib.ptr(flux), _lib.ptr(out), float(tol),
+                                                        infos, _lib.stream_ptr(stream)))
+            self.last_clean = list(infos)
+            return out
         info = _lib.CleanInfo()
         _lib.check(self._lib.spfd_field_clean(self.handle, _lib.ptr(flux), _lib.ptr(out), float(tol),
                                               ctypes.byref(info), _lib.stream_ptr(stream)))

@@ -90,6 +90,27 @@ def test_cleaning_matches_reference(g, grid):
     assert np.array_equal(c2, g["clean"]) and field_ops(grid).last_clean.solved == 0
 
 
+def test_cleaning_batched_pair(g, grid):
+    """re/im flux pair in one batched projection solve: each meets the
+    reference result and its postcondition; an already-solenoidal member of
+    the pair is passed through unchanged (no solve for it)."""
+    import torch
+    from paper_2010_12879_b200.field_source import divergence, field_ops
+    ops = field_ops(grid)
+    fn = np.linalg.norm(g["flux"])
+    pair = torch.from_numpy(np.stack([g["flux"], 0.5 * g["flux"][::-1].copy()])).cuda()
+    out = ops.clean(pair, 1e-10).cpu().numpy()
+    infos = ops.last_clean
+    assert len(infos) == 2 and all(i.solved == 1 and i.rel_after <= 1e-10 for i in infos)
+    assert np.linalg.norm(out[0] - g["clean"]) <= 1e-9 * fn
+    for c in range(2):
+        assert np.linalg.norm(divergence(out[c], grid)) <= 1e-10 * np.linalg.norm(pair[c].cpu().numpy())
+    mixed = torch.from_numpy(np.stack([g["clean"], g["flux"]])).cuda()
+    out = ops.clean(mixed, 1e-10).cpu().numpy()
+    assert ops.last_clean[0].solved == 0 and ops.last_clean[1].solved == 1
+    assert np.array_equal(out[0], g["clean"]) and np.linalg.norm(out[1] - g["clean"]) <= 1e-9 * fn
+
+
 def test_cleaning_hierarchy_aggregates(g):
     from paper_2010_12879_b200.linsolve import SolveConfig, amg_setup
     dims = tuple(int(v) for v in g["grid_dims"])

@@ -1,8 +1,7 @@
-"""GPU: repeatability of the fine-level stencil kernel and of the solvers
-(the same call twice gives the same bits), plus the graph /
-host-loop and block / MGS solver A/B tests.  The fine-kernel selection knob
-(spfd_set_fine_kernel) keeps one kernel since the round-2 cleanup; the
-loops below run it twice.
+"""GPU A/B of the fine-level stencil kernel with and without the tile's L2
+bulk prefetch (every stencil mode bit-identical, so V-cycles give the same
+bits; Krylov solves agree to tolerance), plus the graph / host-loop and
+block / MGS solver A/B tests.
 
 Every stencil mode must be bit-identical between the two kernels, so a
 V-cycle (pre-smooth+defect, restriction input, matrix-free prolongation,
@@ -21,8 +20,8 @@ from conftest import golden_cases, golden_model, load_golden
 
 pytestmark = pytest.mark.gpu
 
-FLAT = 2
-KINDS = (FLAT, FLAT)
+FLAT, PF = 2, 3
+KINDS = (PF, FLAT)
 
 
 def _set_kernel(kind):

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+tools/ab.sh ab6 flat pf pf5
+timeout 600 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py tests/test_gpu_field.py -q -x > gpurun_out/t6_pytest.log 2>&1; tail -3 gpurun_out/t6_pytest.log
+timeout 900 python tools/bench_streaming.py > gpurun_out/t6_c5.json 2> gpurun_out/t6_c5.err; python -c "
+import json; d=json.loads(open('gpurun_out/t6_c5.json').read().strip().splitlines()[-1]); print(d['per_snapshot_ms_mean'], d['stage_ms_mean'], d['clean_iterations_mean'])"; tail -3 gpurun_out/t6_c5.err

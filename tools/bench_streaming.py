@@ -7,7 +7,8 @@ with the hierarchy reused (`_hierarchy`, pipeline.py:136,162):
 
     sampled B on a lattice (host, pinned)  --H2D-->
     interpolate_to_faces (field_source.py:254-272)
-    divergence_clean on S S^T (field_source.py:292-329, AMG reused)
+    divergence_clean on S S^T (field_source.py:292-329, AMG reused; the re
+    and im sets in one batched solve)
     gauge_vector_potential, comb tree (gauging.py:137-172)
     assemble RHS + AMG-PCG to 1e-8 + E-field / voxel average (one spfd_snapshot)
     --D2H--> voxel |E|
@@ -75,8 +76,8 @@ def run_measured(count, rel_tol, clean_tol, gauge_tol):
     outs = [torch.empty((2, n_vox), dtype=torch.float64, pin_memory=True) for _ in range(count)]
     b_dev = torch.empty(samples[0].shape, dtype=torch.float64, device="cuda")
     a = torch.empty((2, grid.n_edges), dtype=torch.float64, device="cuda")
-    fl = [torch.empty(grid.n_faces, dtype=torch.float64, device="cuda") for _ in range(2)]
-    fc = [torch.empty(grid.n_faces, dtype=torch.float64, device="cuda") for _ in range(2)]
+    fl = torch.empty((2, grid.n_faces), dtype=torch.float64, device="cuda")
+    fc = torch.empty((2, grid.n_faces), dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
     names = ("h2d", "interpolate", "clean", "gauge", "rhs+solve+efield", "d2h")
 
@@ -90,10 +91,8 @@ def run_measured(count, rel_tol, clean_tol, gauge_tol):
             ops.interpolate(lattice, b_dev[c], out=fl[c])
         if ev:
             ev[2].record(stream)
-        infos = []
-        for c in range(2):
-            ops.clean(fl[c], clean_tol, out=fc[c])
-            infos.append(ops.last_clean)
+        ops.clean(fl, clean_tol, out=fc)          # re and im in one batched projection solve
+        infos = ops.last_clean
         if ev:
             ev[3].record(stream)
         for c in range(2):
