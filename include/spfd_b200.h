@@ -331,6 +331,13 @@ typedef struct {
  * (SPFD_EINCOMPAT, info filled).  Zero fluxes give a = 0. */
 int spfd_field_gauge(spfd_field_t f, const double *flux, double *a, double tol,
                      spfd_gauge_info *h_info, void *stream);
+/* The same with the spanning tree selected (build_tree(grid, kind),
+ * gauging.py:122-127): tree 0 = comb, 1 = BFS from node 0
+ * (build_bfs_tree, gauging.py:74-119: all x-edges, the y-edges of the plane
+ * i = 0 and the z-edges of the line i = j = 0), whose FIFO elimination
+ * (_kernels.py:12-76) unrolls into running sums along x. */
+int spfd_field_gauge_tree(spfd_field_t f, int tree, const double *flux, double *a, double tol,
+                          spfd_gauge_info *h_info, void *stream);
 
 /* circulation_residual (gauging.py:127-134): defect double[n_faces] */
 int spfd_field_circulation(spfd_field_t f, const double *a, const double *flux, double *defect,

@@ -27,7 +27,7 @@ __all__ = [
     "amg_setup", "v_cycle", "fgmres", "pcg", "edge_voltages", "node_field",
     "voxel_average", "comb_gauge", "uniform_face_fluxes", "node_index", "coil_field",
     "interpolate_to_faces", "divergence_matrix", "divergence_clean", "circulation_residual", "comb_tree_mask",
-    "eliminate_cotree_edges", "percentile99", "exposure_stats",
+    "eliminate_cotree_edges", "percentile99", "exposure_stats", "bfs_tree_mask", "bfs_gauge",
 ]
 
 
@@ -573,6 +573,43 @@ def comb_gauge(dims, fluxes):
     ax[:, 1:, 0] = -np.cumsum(bz[:, :, 0], axis=1)
     ax[:, :, 1:] = ax[:, :, :1] + np.cumsum(by, axis=2)
     ay[:, :, 1:] = -np.cumsum(bx, axis=2)
+    return np.concatenate([ax.ravel(order="F"), ay.ravel(order="F"), az.ravel(order="F")])
+
+
+def bfs_tree_mask(dims):
+    """Tree edges of the BFS spanning tree from node 0 (gauging.py:74-119).
+    On the full node box the level-synchronous BFS with its direction order
+    (+x first) reaches every node with i > 0 through its -x neighbour, nodes
+    (0, j > 0, k) through -y and (0, 0, k > 0) through -z: all x-edges, the
+    y-edges of the plane i = 0 and the z-edges of the line i = j = 0."""
+    nx, ny, nz = [int(n) for n in dims]
+    m = np.zeros(n_edges(dims), bool)
+    eoff = edge_offsets(dims)[0]
+    ey, ez = edge_dims(dims, 1), edge_dims(dims, 2)
+    m[eoff[0]:eoff[1]] = True
+    j, k = np.meshgrid(np.arange(ny), np.arange(nz + 1), indexing="ij")
+    m[eoff[1] + (ey[0] * (j + ey[1] * k)).ravel()] = True
+    m[eoff[2] + ez[0] * ez[1] * np.arange(nz)] = True
+    return m
+
+
+def bfs_gauge(dims, fluxes):
+    """BFS-tree gauge as three prefix scans along x (the FIFO elimination
+    _kernels.py:12-76 with the BFS tree, up to rounding): z-faces give
+    a_y(i+1) = a_y(i) + b_z(i), x-faces of the plane i = 0 give a_z(0, j+1)
+    = a_z(0, j) + b_x(0, j), y-faces give a_z(i+1) = a_z(i) - b_y(i);
+    tree edges are 0."""
+    nx, ny, nz = [int(d) for d in dims]
+    fcount = [(nx + 1) * ny * nz, nx * (ny + 1) * nz, nx * ny * (nz + 1)]
+    bx = fluxes[:fcount[0]].reshape((nx + 1, ny, nz), order="F")
+    by = fluxes[fcount[0]:fcount[0] + fcount[1]].reshape((nx, ny + 1, nz), order="F")
+    bz = fluxes[fcount[0] + fcount[1]:].reshape((nx, ny, nz + 1), order="F")
+    ax = np.zeros((nx, ny + 1, nz + 1))
+    ay = np.zeros((nx + 1, ny, nz + 1))
+    az = np.zeros((nx + 1, ny + 1, nz))
+    ay[1:] = np.cumsum(bz, axis=0)
+    az[0, 1:] = np.cumsum(bx[0], axis=0)
+    az[1:] = az[:1] - np.cumsum(by, axis=0)
     return np.concatenate([ax.ravel(order="F"), ay.ravel(order="F"), az.ravel(order="F")])
 
 

@@ -11,6 +11,7 @@ from .dosimetry import corner_mean, edge_voltages, efield_voxel_average, node_fi
 from .errors import EmptySystemError, PipelineError, SolverError, SpfdError
 from .fit_operators import (DeviceOperator, PoissonSystem, StaggeredGrid, StencilMatrix, assemble_poisson,
                             edge_conductance)
+from .gauging import SpanningTree, build_bfs_tree, build_comb_tree, gauge_vector_potential
 from .linsolve import (AmgHierarchy, AmgLevel, SolveConfig, SolveReport, amg_setup, fgmres_solve, pcg_solve,
                        solve, v_cycle)
 from .pipeline import Session
@@ -20,6 +21,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AmgHierarchy", "AmgLevel", "ConductivitySamples", "DeviceOperator", "EmptySystemError", "PipelineError",
+    "SpanningTree", "build_bfs_tree", "build_comb_tree", "gauge_vector_potential",
     "PoissonSystem", "Session", "SolveConfig", "SolveReport", "SolverError", "SpfdError", "StaggeredGrid",
     "StencilMatrix", "Tissue", "VoxelModel", "amg_setup", "assemble_poisson", "corner_mean", "edge_conductance",
     "edge_voltages", "efield_voxel_average", "fgmres_solve", "kappa_at", "make_phantom", "node_field_strength",

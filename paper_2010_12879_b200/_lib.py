@@ -170,6 +170,7 @@ _SIGS = {
     "spfd_field_clean": (_INT, [_VP, _VP, _VP, _D, _VP, _VP]),
     "spfd_field_clean_batch": (_INT, [_VP, _INT, _VP, _VP, _D, _VP, _VP]),
     "spfd_field_gauge": (_INT, [_VP, _VP, _VP, _D, _VP, _VP]),
+    "spfd_field_gauge_tree": (_INT, [_VP, _INT, _VP, _VP, _D, _VP, _VP]),
     "spfd_field_circulation": (_INT, [_VP, _VP, _VP, _VP, _VP]),
     "spfd_exposure_stats": (_INT, [_VP, _I64, _D, _VP, _VP, ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
 }

@@ -961,6 +961,7 @@ static void morton_level1(Amg &h, cudaStream_t s) {
     k_root_keys<<<grid_for(n1, T), T, 0, s>>>(L0.mem_ptr.get(), L0.mem_pos.get(), n1, op.rows.get(), op.n_rows,
                                               (int)op.NY, key.get(), idx.get());
     SPFD_LAUNCH_CHECK();
+    SPFD_CUDA(cudaMemsetAsync(P.get(), 0, n1 * sizeof(int32_t), s));  // (initcheck: CUB's stores are not tracked)
     size_t bytes = 0;
     SPFD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.get(), key2.get(), idx.get(), P.get(), (int)n1, 0,
                                               64, s));

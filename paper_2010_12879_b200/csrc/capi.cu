@@ -426,7 +426,16 @@ int spfd_field_clean_batch(spfd_field_t f, int nrhs, const double *in, double *o
 int spfd_field_gauge(spfd_field_t f, const double *flux, double *a, double tol, spfd_gauge_info *info, void *stream) {
     return guarded([&] {
         SPFD_CHECK(f && flux && a && info, SPFD_EINVAL, "null argument");
-        field_gauge_comb(*f->f, flux, a, tol, info, S(stream));
+        field_gauge(*f->f, 0, flux, a, tol, info, S(stream));
+    });
+}
+
+int spfd_field_gauge_tree(spfd_field_t f, int tree, const double *flux, double *a, double tol, spfd_gauge_info *info,
+                          void *stream) {
+    return guarded([&] {
+        SPFD_CHECK(f && flux && a && info, SPFD_EINVAL, "null argument");
+        SPFD_CHECK(tree == 0 || tree == 1, SPFD_EINVAL, "tree must be 0 (comb) or 1 (bfs)");
+        field_gauge(*f->f, tree, flux, a, tol, info, S(stream));
     });
 }
 

@@ -164,6 +164,7 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double *smem /* [32*K]
 #pragma unroll
         for (int k = 0; k < K; ++k) smem[warp * K + k] = v[k];
     }
+    __syncwarp();      // reconverge the warp before the CTA barrier (synccheck)
     __syncthreads();
     if (warp == 0) {
 #pragma unroll

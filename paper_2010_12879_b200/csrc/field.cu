@@ -288,6 +288,43 @@ __global__ void __launch_bounds__(128) k_gauge_kscan(int64_t ncol, int64_t nk, c
     }
 }
 
+// BFS tree (gauging.py:74-119) on the full node box: all x-edges, the
+// y-edges of the plane i = 0 and the z-edges of the line i = j = 0 carry 0
+// (level-synchronous BFS from node 0 with the +x pass first reaches every
+// node with i > 0 through its -x neighbour).  The remaining edges unroll
+// into running sums along x (and along j on the plane i = 0):
+//   a_y(i+1, j, k) = sum_{i'<=i} b_z(i', j, k)              (z-faces)
+//   a_z(0, j+1, k) = sum_{j'<=j} b_x(0, j', k)              (x-faces, i = 0)
+//   a_z(i+1, j, k) = a_z(0, j, k) - sum_{i'<=i} b_y(i', j, k) (y-faces)
+// one thread per row, sequential in the scan index (numpy cumsum order).
+template <bool BASE>
+__global__ void k_gauge_xscan(int64_t nrows, int64_t nx, const double *__restrict__ src, double *__restrict__ dst) {
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= nrows) return;
+    const double *sr = src + row * nx;
+    double *dr = dst + row * (nx + 1);
+    const double base = BASE ? dr[0] : 0.0;
+    if (!BASE) dr[0] = 0.0;
+    double c = 0.0;
+    for (int64_t i = 0; i < nx; ++i) {
+        c = __dadd_rn(c, sr[i]);
+        dr[i + 1] = BASE ? __dsub_rn(base, c) : c;
+    }
+}
+
+// a_z on the plane i = 0: one thread per k, scanning j
+__global__ void k_gauge_bfs_az0(int64_t nx, int64_t ny, int64_t nz, const double *__restrict__ bx,
+                                double *__restrict__ az) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= nz) return;
+    az[(nx + 1) * (ny + 1) * k] = 0.0;
+    double c = 0.0;
+    for (int64_t j = 0; j < ny; ++j) {
+        c = __dadd_rn(c, bx[(nx + 1) * (j + ny * k)]);
+        az[(nx + 1) * (j + 1 + (ny + 1) * k)] = c;
+    }
+}
+
 __global__ void k_zero(int64_t n, double *p) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
         p[q] = 0.0;
@@ -624,7 +661,7 @@ void field_circulation(Field &F, const double *a, const double *flux, double *de
     SPFD_LAUNCH_CHECK();
 }
 
-void field_gauge_comb(Field &F, const double *flux, double *a, double tol, spfd_gauge_info *info, cudaStream_t s) {
+void field_gauge(Field &F, int tree, const double *flux, double *a, double tol, spfd_gauge_info *info, cudaStream_t s) {
     const int64_t nx = F.g.n[0], ny = F.g.n[1], nz = F.g.n[2];
     const int64_t F0 = face_count(F.g, 0), F1 = face_count(F.g, 1);
     const int64_t E0 = edge_count(F.g, 0), E1 = edge_count(F.g, 1), E2 = edge_count(F.g, 2);
@@ -639,22 +676,39 @@ void field_gauge_comb(Field &F, const double *flux, double *a, double tol, spfd_
         return;
     }
     const double *bx = flux, *by = flux + F0, *bz = flux + F0 + F1;
-    // a_x: k = 0 plane, then the k scans (nx * (ny+1) columns)
-    if (nx > 0) {
-        k_gauge_ax0<<<(int)((nx + 127) / 128), 128, 0, s>>>(nx, ny, bz, ax);
+    if (tree == 1) {  // BFS tree: x-scans
+        k_zero<<<blocks(E0), 256, 0, s>>>(E0, ax);
         SPFD_LAUNCH_CHECK();
-        const int64_t ncol = nx * (ny + 1);
-        k_gauge_kscan<false, 16><<<(int)((ncol + 127) / 128), 128, 0, s>>>(ncol, nz, by, ax);
-        SPFD_LAUNCH_CHECK();
-    }
-    if (ny > 0) {
-        const int64_t ncol = (nx + 1) * ny;
-        k_gauge_kscan<true, 16><<<(int)((ncol + 127) / 128), 128, 0, s>>>(ncol, nz, bx, ay);
-        SPFD_LAUNCH_CHECK();
-    }
-    if (E2) {
-        k_zero<<<blocks(E2), 256, 0, s>>>(E2, az);
-        SPFD_LAUNCH_CHECK();
+        if (ny > 0) {
+            const int64_t nrow = ny * (nz + 1);
+            k_gauge_xscan<false><<<(int)((nrow + 127) / 128), 128, 0, s>>>(nrow, nx, bz, ay);
+            SPFD_LAUNCH_CHECK();
+        }
+        if (nz > 0) {
+            k_gauge_bfs_az0<<<(int)((nz + 127) / 128), 128, 0, s>>>(nx, ny, nz, bx, az);
+            SPFD_LAUNCH_CHECK();
+            const int64_t nrow = (ny + 1) * nz;
+            k_gauge_xscan<true><<<(int)((nrow + 127) / 128), 128, 0, s>>>(nrow, nx, by, az);
+            SPFD_LAUNCH_CHECK();
+        }
+    } else {
+        // a_x: k = 0 plane, then the k scans (nx * (ny+1) columns)
+        if (nx > 0) {
+            k_gauge_ax0<<<(int)((nx + 127) / 128), 128, 0, s>>>(nx, ny, bz, ax);
+            SPFD_LAUNCH_CHECK();
+            const int64_t ncol = nx * (ny + 1);
+            k_gauge_kscan<false, 16><<<(int)((ncol + 127) / 128), 128, 0, s>>>(ncol, nz, by, ax);
+            SPFD_LAUNCH_CHECK();
+        }
+        if (ny > 0) {
+            const int64_t ncol = (nx + 1) * ny;
+            k_gauge_kscan<true, 16><<<(int)((ncol + 127) / 128), 128, 0, s>>>(ncol, nz, bx, ay);
+            SPFD_LAUNCH_CHECK();
+        }
+        if (E2) {
+            k_zero<<<blocks(E2), 256, 0, s>>>(E2, az);
+            SPFD_LAUNCH_CHECK();
+        }
     }
     // postcondition: circulation residual over every face (gauging.py:167-171)
     if (F.wf.n < (size_t)nf) F.wf.alloc(nf);

@@ -13,7 +13,8 @@ void field_interpolate(Field &F, const spfd_box &lattice, const double *b, doubl
 void field_divergence(Field &F, const double *flux, double *div, cudaStream_t s);
 void field_clean(Field &F, int nrhs, const double *in, double *out, double tol, spfd_clean_info *info,
                  cudaStream_t s);
-void field_gauge_comb(Field &F, const double *flux, double *a, double tol, spfd_gauge_info *info, cudaStream_t s);
+// tree: 0 = comb (gauging.py:34-71), 1 = BFS (gauging.py:74-119)
+void field_gauge(Field &F, int tree, const double *flux, double *a, double tol, spfd_gauge_info *info, cudaStream_t s);
 void field_circulation(Field &F, const double *a, const double *flux, double *defect, cudaStream_t s);
 void coil_field(int64_t n, const double *pts, int nseg, const double *verts, double scale, double *out,
                 cudaStream_t s);

@@ -269,13 +269,15 @@ class FieldOps:
         self.last_clean = info
         return out
 
-    def gauge(self, flux, tol: float = 1e-10, out=None, stream=None):
+    def gauge(self, flux, tol: float = 1e-10, out=None, stream=None, tree: str = "comb"):
         from .errors import IncompatibleFluxError
+        if tree not in ("comb", "bfs"):
+            raise ValueError(f"unknown tree kind {tree!r}")
         flux = _dev(flux)
         out = torch.empty(self.grid.n_edges, dtype=torch.float64, device="cuda") if out is None else out
         info = _lib.GaugeInfo()
-        rc = self._lib.spfd_field_gauge(self.handle, _lib.ptr(flux), _lib.ptr(out), float(tol), ctypes.byref(info),
-                                        _lib.stream_ptr(stream))
+        rc = self._lib.spfd_field_gauge_tree(self.handle, 0 if tree == "comb" else 1, _lib.ptr(flux), _lib.ptr(out),
+                                             float(tol), ctypes.byref(info), _lib.stream_ptr(stream))
         if rc == _lib.SPFD_EINCOMPAT:
             raise IncompatibleFluxError(info.rel_residual, int(info.worst_face), info.worst_defect)
         _lib.check(rc)

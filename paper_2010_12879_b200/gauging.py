@@ -9,6 +9,12 @@ residual over every face against `tol` (IncompatibleFluxError).  The result
 equals the reference's FIFO elimination up to rounding (the FIFO may reach
 an edge through a different face; SURVEY P7 measured 9e-16) and equals the
 numpy cumsum formulation (`oracle.comb_gauge`) bit for bit.
+
+The BFS tree (gauging.py:74-119) spans the full node box, where the
+level-synchronous BFS from node 0 (+x pass first) always produces the same
+shape: every x-edge, the y-edges of the plane i = 0 and the z-edges of the
+line i = j = 0.  Its FIFO elimination unrolls into running sums along x
+(k_gauge_xscan, k_gauge_bfs_az0), equal to `oracle.bfs_gauge` bit for bit.
 """
 
 from __future__ import annotations
@@ -35,6 +41,8 @@ class SpanningTree:
 
     @cached_property
     def _arrays(self):
+        if self.kind == "bfs":
+            return self._bfs_arrays()
         g = self.grid
         nx, ny, nz = g.dims
         mask = np.zeros(g.n_edges, dtype=bool)
@@ -62,6 +70,31 @@ class SpanningTree:
             parent_edge[g.node_index(i, j, k + 1)] = e
         return mask, parent_node, parent_edge
 
+    def _bfs_arrays(self):
+        # node (i, j, k): i > 0 via its -x neighbour, else j > 0 via -y, else -z
+        g = self.grid
+        nx, ny, nz = g.dims
+        mask = np.zeros(g.n_edges, dtype=bool)
+        parent_node = np.full(g.n_nodes, -1, dtype=np.int64)
+        parent_edge = np.full(g.n_nodes, -1, dtype=np.int64)
+        i, j, k = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), np.arange(nz + 1), indexing="ij")
+        i, j, k = i.ravel(order="F"), j.ravel(order="F"), k.ravel(order="F")
+        node = g.node_index(i, j, k)
+        sel = i > 0
+        e = g.edge_index(0, i[sel] - 1, j[sel], k[sel])
+        parent_node[node[sel]] = g.node_index(i[sel] - 1, j[sel], k[sel])
+        parent_edge[node[sel]] = e
+        sel = (i == 0) & (j > 0)
+        e2 = g.edge_index(1, i[sel], j[sel] - 1, k[sel])
+        parent_node[node[sel]] = g.node_index(i[sel], j[sel] - 1, k[sel])
+        parent_edge[node[sel]] = e2
+        sel = (i == 0) & (j == 0) & (k > 0)
+        e3 = g.edge_index(2, i[sel], j[sel], k[sel] - 1)
+        parent_node[node[sel]] = g.node_index(i[sel], j[sel], k[sel] - 1)
+        parent_edge[node[sel]] = e3
+        mask[np.concatenate([e, e2, e3])] = True
+        return mask, parent_node, parent_edge
+
     @property
     def edge_mask(self) -> np.ndarray:
         return self._arrays[0]
@@ -77,7 +110,7 @@ class SpanningTree:
     @property
     def n_tree_edges(self) -> int:
         nx, ny, nz = self.grid.dims
-        return nx + (nx + 1) * ny + (nx + 1) * (ny + 1) * nz
+        return (nx + 1) * (ny + 1) * (nz + 1) - 1  # a spanning tree of the node box
 
 
 def build_comb_tree(grid: StaggeredGrid) -> SpanningTree:
@@ -86,12 +119,17 @@ def build_comb_tree(grid: StaggeredGrid) -> SpanningTree:
     return SpanningTree(grid, "comb")
 
 
+def build_bfs_tree(grid: StaggeredGrid) -> SpanningTree:
+    """Breadth-first spanning tree from node 0 with the reference's
+    deterministic frontier order (gauging.py:74-119)."""
+    return SpanningTree(grid, "bfs")
+
+
 def build_tree(grid: StaggeredGrid, kind: str = "comb") -> SpanningTree:
     if kind == "comb":
         return build_comb_tree(grid)
     if kind == "bfs":
-        raise NotImplementedError("the device gauge implements the comb tree (the pipeline default); "
-                                  "the BFS robustness-check tree (gauging.py:74-119) is not provided")
+        return build_bfs_tree(grid)
     raise ValueError(f"unknown tree kind {kind!r}")
 
 
@@ -110,7 +148,7 @@ def gauge_vector_potential(fluxes, grid: StaggeredGrid, tree: SpanningTree, tol:
     n = int(np.prod(np.shape(fluxes)))
     if n != grid.n_faces:
         raise ValueError(f"flux vector has length {n}, expected {grid.n_faces}")
-    if tree.kind != "comb" or tree.grid != grid:
-        raise ValueError("gauge_vector_potential needs the comb tree of this grid (build_comb_tree(grid))")
-    out = field_ops(grid).gauge(_dev(fluxes), tol)
+    if tree.kind not in ("comb", "bfs") or tree.grid != grid:
+        raise ValueError("gauge_vector_potential needs a comb or BFS tree of this grid (build_tree(grid, kind))")
+    out = field_ops(grid).gauge(_dev(fluxes), tol, tree=tree.kind)
     return out.cpu().numpy() if as_np else out

@@ -357,8 +357,8 @@ def run_pipeline(cfg: PipelineConfig, *, _hierarchy=None, _state: PipelineState 
         if cfg.clean_fluxes:
             flux = ops.clean(flux, cfg.clean_tol)
     with _Stage(timing, "gauge"):
-        build_tree(grid, cfg.tree_kind)
-        a = ops.gauge(flux, cfg.gauge_tol)
+        tree = build_tree(grid, cfg.tree_kind)
+        a = ops.gauge(flux, cfg.gauge_tol, tree=tree.kind)
     with _Stage(timing, "assemble"):
         state = _state if _state is not None else PipelineState(model, cfg.frequency_hz, cfg.solve)
         rhs = state.op.rhs(a)

@@ -264,6 +264,29 @@ def field_case(name):
     print(name, "faces", grid.n_faces, "normal levels", h.level_sizes)
 
 
+def bfs_case(name):
+    """The BFS spanning tree (gauging.py:74-119) and the reference's FIFO
+    cotree elimination with it (_kernels.py:12-76) on the field_coil grid:
+    the tree's mask / parents, the gauged potential of the cleaned coil
+    fluxes and of a uniform field, and the circulation residuals."""
+    grid = ro.StaggeredGrid((12, 10, 8), (0.002, 0.0025, 0.003), (0.001, -0.002, 0.0005))
+    coil = rf.CoilSpec(center=(0.012, 0.01, -0.02), axis=(0.2, 0.1, 1.0), radius_m=0.03, current_a=5.0, segments=64)
+    lattice = rf.Lattice((0.004, -0.001, 0.002), (0.006, 0.007, 0.008), (4, 4, 3))
+    samples = rf.sample_on_lattice(coil, lattice, FREQ)
+    clean = rf.divergence_clean(rf.interpolate_to_faces(samples, grid), grid, 1e-10)
+    tree = rg.build_tree(grid, "bfs")
+    d = {"grid_dims": np.array(grid.dims, np.int64), "grid_spacing": np.array(grid.spacing),
+         "grid_origin": np.array(grid.origin), "clean": clean, "tree_mask": tree.edge_mask,
+         "parent_node": tree.parent_node, "parent_edge": tree.parent_edge}
+    d["a"] = rg.gauge_vector_potential(clean, grid, tree, 1e-10)
+    d["circ"] = rg.circulation_residual(d["a"], clean, grid)
+    usamp = rf.sample_on_lattice(rf.UniformField((0.3e-6, -0.2e-6, 1e-6)), rf.Lattice.covering(grid, (2, 2, 2)), FREQ)
+    d["uniform_flux"] = rf.interpolate_to_faces(usamp, grid)
+    d["uniform_a"] = rg.gauge_vector_potential(d["uniform_flux"], grid, tree, 1e-10)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(name, "tree edges", int(tree.edge_mask.sum()))
+
+
 def pipeline_case(name):
     """The reference's run_pipeline end to end (coil source sampled on a
     5x5x5 lattice, cleaning, comb gauge, solve, E-field, report) plus the
@@ -331,11 +354,14 @@ def main():
 
     field_case("field_coil")
     pipeline_case("field_pipeline")
+    bfs_case("field_bfs")
 
 
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "field":
         field_case("field_coil")
         pipeline_case("field_pipeline")
+    elif len(sys.argv) > 1 and sys.argv[1] == "bfs":
+        bfs_case("field_bfs")
     else:
         main()

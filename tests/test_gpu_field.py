@@ -136,6 +136,25 @@ def test_gauge_comb(g, grid):
     assert np.array_equal(ua, oracle.comb_gauge(dims, g["uniform_flux"]))
 
 
+def test_gauge_bfs(grid):
+    """BFS tree (gauging.py:74-119) on the device: bit-exact against the
+    oracle's x-scan form, within rounding of the reference's FIFO
+    elimination, zero on tree edges, compatible circulation; the pipeline's
+    tree_kind selects it."""
+    from paper_2010_12879_b200.gauging import build_tree, circulation_residual, gauge_vector_potential
+    b = load_golden("field_bfs")
+    dims = grid.dims
+    tree = build_tree(grid, "bfs")
+    a = gauge_vector_potential(b["clean"], grid, tree, 1e-10)
+    assert np.array_equal(a, oracle.bfs_gauge(dims, b["clean"]))
+    assert np.abs(a - b["a"]).max() <= 1e-12 * np.abs(b["a"]).max()
+    assert np.all(a[b["tree_mask"]] == 0.0)
+    r = circulation_residual(a, b["clean"], grid)
+    assert np.abs(r).max() <= 1e-12 * np.abs(b["clean"]).max()
+    ua = gauge_vector_potential(b["uniform_flux"], grid, tree, 1e-10)
+    assert np.array_equal(ua, oracle.bfs_gauge(dims, b["uniform_flux"]))
+
+
 def test_gauge_incompatible_and_zero(g, grid):
     from paper_2010_12879_b200.errors import IncompatibleFluxError
     from paper_2010_12879_b200.gauging import build_comb_tree, gauge_vector_potential

@@ -82,3 +82,34 @@ def test_exposure_stats(g):
     for t, c, m, x, p in zip(g["st_tids"], g["st_count"], g["st_mean"], g["st_tmax"], g["st_tp99"]):
         assert per[int(t)] == (int(c), float(m), float(x), float(p))
     assert oracle.percentile99(g["st_vals"]) == float(g["p99_plain"])
+
+
+def test_bfs_tree_and_gauge_match_reference():
+    """BFS spanning tree (gauging.py:74-119) and the FIFO elimination with it
+    (_kernels.py:12-76): the closed-form tree equals the reference's, the
+    oracle's FIFO restatement reproduces the reference potential bit for
+    bit, and the x-scan form agrees to rounding."""
+    b = load_golden("field_bfs")
+    dims = tuple(int(v) for v in b["grid_dims"])
+    mask = oracle.bfs_tree_mask(dims)
+    assert np.array_equal(mask, b["tree_mask"])
+    v, und = oracle.eliminate_cotree_edges(dims, b["clean"], mask)
+    assert und == 0 and np.array_equal(v, b["a"])
+    scale = np.abs(b["a"]).max()
+    assert np.abs(oracle.bfs_gauge(dims, b["clean"]) - b["a"]).max() <= 1e-14 * scale
+    assert np.abs(oracle.bfs_gauge(dims, b["uniform_flux"]) - b["uniform_a"]).max() <= 1e-14 * np.abs(b["uniform_a"]).max()
+
+
+def test_bfs_spanning_tree_host_arrays():
+    """The package's BFS SpanningTree metadata (mask, parent node / edge) is
+    the reference's (host index bookkeeping; the gauge itself runs on the
+    device)."""
+    from paper_2010_12879_b200.fit_operators import StaggeredGrid
+    from paper_2010_12879_b200.gauging import build_tree
+    b = load_golden("field_bfs")
+    grid = StaggeredGrid(tuple(int(v) for v in b["grid_dims"]), tuple(b["grid_spacing"]), tuple(b["grid_origin"]))
+    t = build_tree(grid, "bfs")
+    assert np.array_equal(t.edge_mask, b["tree_mask"])
+    assert np.array_equal(t.parent_node, b["parent_node"])
+    assert np.array_equal(t.parent_edge, b["parent_edge"])
+    assert t.n_tree_edges == int(b["tree_mask"].sum())
