@@ -404,28 +404,68 @@ def main():
             log(f"[bench] rel_tol {tv:g}: step {ms_s:.2f} ms ({rep_s.iterations} it), fgmres single rhs "
                 f"{ms_f:.2f} ms ({rep_f.iterations} it), fgmres pair {ms_fp:.2f} ms")
 
-    # roofline of the dominant kernel (fine-level matrix-free SpMV, both rhs)
+    # per-kernel rooflines (each kernel timed alone, back to back on the solve
+    # stream with CUDA events) and the kernel with the largest share of the step
     import ctypes
-    kms, kbytes = ctypes.c_double(), ctypes.c_double()
-    _lib.check(lib.spfd_bench_kernel(h.handle, 0, args.kernel_reps, 2, ctypes.byref(kms), ctypes.byref(kbytes),
-                                     _lib.stream_ptr()))
     peak, peak_src = _peaks()
-    achieved = kbytes.value / (kms.value * 1e-3) / 1e9
-    extra = {}
-    for which, name in ((1, "fine_presmooth_defect"), (2, "fine_postsmooth"), (3, "vcycle")):
-        m_, b_ = ctypes.c_double(), ctypes.c_double()
-        _lib.check(lib.spfd_bench_kernel(h.handle, which, args.kernel_reps, 2, ctypes.byref(m_), ctypes.byref(b_),
-                                         _lib.stream_ptr()))
-        extra[name] = {"ms": round(m_.value, 4)}
-        if b_.value > 0:
-            extra[name]["gbs"] = round(b_.value / (m_.value * 1e-3) / 1e9, 1)
-    traffic = None
+    it_mean = statistics.mean(its)
+    traffic_db = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{args.config}_fine_spmv_dram_bytes")
+            traffic_db = json.load(f)
+    # (which, key, kernel, launches per PCG iteration)
+    table = [(0, "fine_spmv", "k_span<2,0,1> fine SpMV q = A p (+ p.q)", 1),
+             (1, "fine_presmooth", "k_span<2,2> pre-smooth + defect d = r - A(od r) (also the restriction input)", 2),
+             (4, "fine_prolongation", "k_span<2,4> matrix-free prolongation x1 = od r + e - od A e", 1),
+             (2, "fine_postsmooth", "k_span<2,3,1> post-smooth z = x1 + od (r - A x1) (+ r.z)", 1),
+             (5, "fine_restriction", "k_agg_sum<2> restriction sums r_c = T^T u", 1),
+             (6, "level1_presmooth", "k_csr<4,2,1> level-1 pre-smooth residual", 1),
+             (7, "level1_prolong_post", "k_csr_pp<4,2> level-1 fused prolongation + post-smooth", 1),
+             (8, "pcg_r_update", "k_update_r<2> r -= alpha q (+ r.r)", 1),
+             (9, "pcg_p_update", "k_xpby<2> p = z + beta p", 1),
+             (10, "fine_presmooth_restriction_fused",
+              "k_span_fused<2,2,2> pre-smooth defect d + restriction input u = d - A(od d), one launch", 1),
+             (11, "fine_prolong_postsmooth_fused",
+              "k_span_fused<2,4,3> prolongation x1 + post-smooth z (+ r.z), one launch", 1)]
+    fused = lib.spfd_bench_kernel(h.handle, 10, 1, 2, ctypes.byref(ctypes.c_double()),
+                                  ctypes.byref(ctypes.c_double()), _lib.stream_ptr()) == 0
+    if fused:  # the separate passes are not launched by the solve (kept as standalone rooflines)
+        table = [(w_, k_, d_, 0 if w_ in (1, 2, 4) else n_) for (w_, k_, d_, n_) in table]
+    kernels = {}
+    iter_ms = ms / it_mean if it_mean else ms
+    for which, key, desc, per_it in table:
+        m_, b_ = ctypes.c_double(), ctypes.c_double()
+        if lib.spfd_bench_kernel(h.handle, which, args.kernel_reps, 2, ctypes.byref(m_), ctypes.byref(b_),
+                                 _lib.stream_ptr()) != 0:
+            continue  # kernel not used for this hierarchy (too few levels, fusion off)
+        gbs = b_.value / (m_.value * 1e-3) / 1e9
+        kernels[key] = {"kernel": desc, "ms": round(m_.value, 4), "bytes": b_.value, "gbs": round(gbs, 1),
+                        "frac": round(gbs / peak, 4), "launches_per_iteration": per_it,
+                        "share_of_iteration": round(m_.value * per_it / iter_ms, 4)}
+    m_, b_ = ctypes.c_double(), ctypes.c_double()
+    _lib.check(lib.spfd_bench_kernel(h.handle, 3, args.kernel_reps, 2, ctypes.byref(m_), ctypes.byref(b_),
+                                     _lib.stream_ptr()))
+    kernels["vcycle"] = {"ms": round(m_.value, 4), "bytes": b_.value,
+                         "gbs": round(b_.value / (m_.value * 1e-3) / 1e9, 1)}
+    ib = ctypes.c_double()
+    _lib.check(lib.spfd_iteration_bytes(h.handle, 2, ctypes.byref(ib)))
+    step_bytes = ib.value * it_mean
+    step_gbs = step_bytes / (ms * 1e-3) / 1e9
+    dom_key = max((k for k in kernels if kernels[k].get("launches_per_iteration")),
+                  key=lambda k: kernels[k]["share_of_iteration"])
+    dom = kernels[dom_key]
+    achieved = dom["gbs"]
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic_db.get(f"{args.config}_{dom_key}_dram_bytes"),
+                "kernel": dom["kernel"] + ", both rhs", "bytes_per_launch": dom["bytes"],
+                "ms_per_launch": dom["ms"], "share_of_iteration": dom["share_of_iteration"],
+                "peak_source": peak_src,
+                "step": {"algorithmic_bytes": step_bytes, "gbs": round(step_gbs, 1),
+                         "frac": round(step_gbs / peak, 4),
+                         "note": "whole timed step: PCG iterations' algorithmic bytes (SpMV, V-cycle on every level, "
+                                 "vector updates; RHS assembly and E-field not counted) / device step time"}}
 
-    it_mean = statistics.mean(its)
     n_dofs = sess.n_dofs
     line = {
         "metric": METRIC,
@@ -455,11 +495,8 @@ def main():
         "setup_s_repeat": setup_repeat,
         "levels": h.level_sizes,
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "fine-level matrix-free 7-point SpMV (k_span<2,0,true>), both rhs",
-                     "bytes_per_launch": kbytes.value, "ms_per_launch": round(kms.value, 4), "peak_source": peak_src},
-        "kernels": extra,
+        "roofline": roofline,
+        "kernels": kernels,
         "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "Session.snapshots_host: stream of `steps` snapshots from pinned host memory, each copied in and "
                        "its voxel |E| copied out; transfers overlap the neighbouring snapshots' solves",

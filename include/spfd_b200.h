@@ -356,19 +356,30 @@ int spfd_exposure_stats(const double *values, int64_t n, double scale, const int
 
 /* ---- measurement ---------------------------------------------------------- */
 
-/* Time `reps` back-to-back launches of one level-0 kernel between CUDA
+/* Time `reps` back-to-back launches of one solve kernel between CUDA
  * events on `stream` (after 3 warm-up launches):
  *   which = 0 fine SpMV q = A p (+ p.q partials), 1 fused pre-smooth +
- *   defect, 2 post-smooth sweep, 3 one full V-cycle.
- * h_ms: ms per launch; h_bytes: algorithmic bytes per launch (0 for 3). */
+ *   defect (also the restriction input), 2 post-smooth sweep (+ r.z),
+ *   3 one full V-cycle, 4 fine matrix-free prolongation, 5 restriction
+ *   sums over the aggregates, 6 level-1 pre-smooth residual, 7 level-1
+ *   fused prolongation + post-smooth, 8 PCG r update (+ r.r), 9 PCG p update,
+ *   10 fused pre-smooth + restriction input, 11 fused prolongation +
+ *   post-smooth (10, 11: only while the fused fine kernel is selected).
+ * h_ms: ms per launch; h_bytes: algorithmic bytes per launch (3: the whole
+ * V-cycle).  Kernels 4-7 need the corresponding levels (else EINVAL). */
 int spfd_bench_kernel(spfd_amg_t amg, int which, int reps, int nrhs, double *h_ms, double *h_bytes,
                       void *stream);
+/* Algorithmic HBM bytes of one PCG iteration with `nrhs` batched rhs: the
+ * SpMV, the V-cycle (every level) and the three vector updates. */
+int spfd_iteration_bytes(spfd_amg_t amg, int nrhs, double *h_bytes);
 /* Tuning knob (not part of the reference API): select the fine-level
  * stencil kernel used by every later solve / V-cycle in this process.
- * kind = -1 default (environment SPFD_SPAN_KERNEL=flat|pf, else pf),
- * 2 flat per-position kernel, 3 the same with the tile's streamed arrays
- * bulk-prefetched into L2.  Both give bit-identical outputs; this exists for
- * A/B tests. */
+ * kind = -1 default (environment SPFD_SPAN_KERNEL=flat|pf|fused, else
+ * pf), 2 flat per-position kernel, 3 the same with the tile's streamed
+ * arrays bulk-prefetched into L2, 4 = 3 plus the V-cycle's dependent pass
+ * pairs (pre-smooth -> restriction input, prolongation -> post-smooth)
+ * fused into one persistent launch each.  All give bit-identical stencil
+ * outputs; this exists for A/B tests. */
 int spfd_set_fine_kernel(int kind);
 /* Tuning knob: run PCG as one CUDA graph with a device-side WHILE node
  * (mode 1, the default) or as the host-driven loop (mode 0); -1 restores the

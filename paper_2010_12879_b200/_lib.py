@@ -153,6 +153,7 @@ _SIGS = {
     "spfd_solve": (_INT, [_VP, _VP, _VP, _INT, _VP, _VP, _VP, _VP]),
     "spfd_snapshot": (_INT, [_VP, _VP, _VP, _D, _VP, _VP, _INT, _VP, _VP, _VP]),
     "spfd_bench_kernel": (_INT, [_VP, _INT, _INT, _INT, _VP, _VP, _VP]),
+    "spfd_iteration_bytes": (_INT, [_VP, _INT, _VP]),
     "spfd_set_fine_kernel": (_INT, [_INT]),
     "spfd_set_pcg_graph": (_INT, [_INT]),
     "spfd_launch_count": (ctypes.c_int64, []),

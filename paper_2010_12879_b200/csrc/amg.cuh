@@ -76,6 +76,8 @@ struct Amg {
     cudaGraphExec_t pcg_exec[3] = {nullptr, nullptr, nullptr};
     int64_t pcg_body_launches[3] = {0, 0, 0};
     int pcg_kind[3] = {-1, -1, -1};         // fine-kernel kind captured in each graph
+    DevBuf<int> fuse_sync;    // fused fine passes: item counter + per-tile done flags
+    int fuse_dep = 0;         // z-neighbour reach of a tile, in tiles (structured level 0)
     DevBuf<double> pcg_trace;               // [cap_iters * 2] per-iteration residual estimates
     int64_t pcg_trace_cap = 0;
     // FGMRES restart cycle as one graph per rhs count (fgmres_graph.cuh)
@@ -111,6 +113,8 @@ void amg_distribute(Amg &h, Comm *comm, int64_t replicate_below, int64_t *range,
 void dist_range_exchange(Amg &h, double *v, int nrhs, cudaStream_t s);
 void dist_info(const Amg &h, int64_t *out);  // pb, pe, voxel-row begin, end
 double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cudaStream_t s);
+// algorithmic bytes of one PCG iteration (SpMV, V-cycle, vector updates)
+double amg_iteration_bytes(const Amg &h, int nrhs);
 spfd_report krylov_solve(Amg &h, const double *b_inter, double *x_inter, int nrhs, const spfd_config &cfg,
                          double *h_trace, cudaStream_t s);
 

@@ -330,14 +330,21 @@ int spfd_amg_distribute(spfd_amg_t h, spfd_comm_t c, int64_t replicate_below, in
 
 int spfd_bench_kernel(spfd_amg_t h, int which, int reps, int nrhs, double *h_ms, double *h_bytes, void *stream) {
     return guarded([&] {
-        SPFD_CHECK(h && h_ms && h_bytes && which >= 0 && which <= 3, SPFD_EINVAL, "bad argument");
+        SPFD_CHECK(h && h_ms && h_bytes && which >= 0 && which <= 11, SPFD_EINVAL, "bad argument");
         *h_ms = amg_bench_kernel(*h->amg, which, reps, nrhs, h_bytes, S(stream));
+    });
+}
+
+int spfd_iteration_bytes(spfd_amg_t h, int nrhs, double *h_bytes) {
+    return guarded([&] {
+        SPFD_CHECK(h && h_bytes && nrhs >= 1 && nrhs <= 2, SPFD_EINVAL, "bad argument");
+        *h_bytes = amg_iteration_bytes(*h->amg, nrhs);
     });
 }
 
 int spfd_set_fine_kernel(int kind) {
     return guarded([&] {
-        SPFD_CHECK(kind == -1 || kind == 2 || kind == 3, SPFD_EINVAL, "fine kernel kind must be -1, 2 or 3");
+        SPFD_CHECK(kind == -1 || (kind >= 2 && kind <= 4), SPFD_EINVAL, "fine kernel kind must be -1, 2, 3 or 4");
         g_fine_kind_override = kind;
     });
 }

@@ -132,6 +132,7 @@ struct SpanArgs {
     int64_t pe = INT64_MAX;
     int tile0 = 0;        // first tile of the launch (set by launch_fine)
     int pf_ahead = 0;     // PF: also prefetch the tile this many tiles ahead (0 = own tile only)
+    int rev = 0;          // walk the tiles from the high end (L2 reuse of the previous pass's tail)
 };
 
 // Input of a fine-level stencil at a position, per mode (see k_span).
@@ -221,27 +222,14 @@ __device__ __forceinline__ void tile_prefetch(const SpanView &v, const SpanArgs 
     if (MODE == 4) { l2_prefetch(a.aggp, p0, p1, 4); l2_prefetch(a.base, p0, p1, 8 * R); }
 }
 
-template <int R, int MODE, bool DOT, bool RANGED = false, bool PF = false, int MINB = 6>
-__global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArgs a) {
+// One tile of a fine-level stencil pass: positions [t * kTile, +kTile) that
+// lie in [pb, pend); accumulates the thread's dot contribution.
+template <int R, int MODE, bool DOT, bool RANGED>
+__device__ __forceinline__ void span_tile(const SpanView &v, const SpanArgs &a, int t, int64_t pend,
+                                          double (&dot)[R]) {
     using W = V<R>;
     using T = typename W::T;
-    __shared__ double red[32 * R];
-    const int t = RANGED ? a.tile0 + blockIdx.x : blockIdx.x;
-    const int64_t pend = RANGED ? (a.pe < v.L ? a.pe : v.L) : v.L;
-    if (PF && threadIdx.x == 0) {
-        if (a.pf_ahead <= 0 || blockIdx.x < a.pf_ahead) {  // first wave: its own tile
-            const int64_t q0 = (int64_t)t * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
-            tile_prefetch<R, MODE>(v, a, q0, q1);
-        }
-        if (a.pf_ahead > 0) {  // later CTAs find their tile queued by an earlier one
-            const int64_t q0 = (int64_t)(t + a.pf_ahead) * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
-            tile_prefetch<R, MODE>(v, a, q0, q1);
-        }
-    }
     const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
-    double dot[R];
-#pragma unroll
-    for (int c = 0; c < R; ++c) dot[c] = 0.0;
     int row = r0;
     for (int u = 0; u < kTile / kSpanThreads; ++u) {
         const int p = t * kTile + u * kSpanThreads + threadIdx.x;
@@ -263,11 +251,109 @@ __global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArg
             }
         }
     }
+}
+
+template <int R, int MODE, bool DOT, bool RANGED = false, bool PF = false, int MINB = 6>
+__global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArgs a) {
+    __shared__ double red[32 * R];
+    // blk: the tile's index within the launch (CTAs run in blockIdx order;
+    // rev walks the tiles from the high end).  Dot partials are stored by
+    // blk, so the reduction order does not depend on the direction.
+    const int blk = a.rev ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
+    const int t = RANGED ? a.tile0 + blk : blk;
+    const int64_t pend = RANGED ? (a.pe < v.L ? a.pe : v.L) : v.L;
+    if (PF && threadIdx.x == 0) {
+        if (a.pf_ahead <= 0 || blockIdx.x < a.pf_ahead) {  // first wave: its own tile
+            const int64_t q0 = (int64_t)t * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
+            tile_prefetch<R, MODE>(v, a, q0, q1);
+        }
+        if (a.pf_ahead > 0) {  // later CTAs find their tile queued by an earlier one
+            const int ta = a.rev ? t - a.pf_ahead : t + a.pf_ahead;
+            const int64_t q0 = (int64_t)ta * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
+            if (ta >= 0) tile_prefetch<R, MODE>(v, a, q0, q1);
+        }
+    }
+    double dot[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) dot[c] = 0.0;
+    span_tile<R, MODE, DOT, RANGED>(v, a, t, pend, dot);
     if (DOT) {
         block_sum<R>(dot, red);
         if (threadIdx.x == 0)
 #pragma unroll
-            for (int c = 0; c < R; ++c) a.partials[blockIdx.x * R + c] = dot[c];
+            for (int c = 0; c < R; ++c) a.partials[blk * R + c] = dot[c];
+    }
+}
+
+// Two dependent fine-level passes in one persistent launch, the second
+// reading the first's output while it is still in L2:
+//   stage 1: y1 = M1(...)      (a1; e.g. the pre-smoothing defect d)
+//   stage 2: y2 = M2(y1, ...)  (a2; e.g. the restriction input from d)
+// Work items are claimed in a fixed order from a counter: stage-1 tiles
+// run `lag` tiles ahead of stage-2 tiles.  Stage-2 tile t reads stage-1
+// output of tiles [t - dep, t + dep] (one node plane each way, the z
+// neighbours) and waits on their done flags; those tiles were claimed
+// earlier by running CTAs and stage-1 items never wait, so the launch
+// cannot deadlock whatever the residency.  Each tile is computed by the
+// same per-position code as k_span, dot partials stored per tile: the
+// results are bit-identical to the two separate passes.  The second pass's
+// reads of y1, the weights and omega D^-1 hit L2 instead of HBM
+// (C3: 48 of 128 B per position for pre-smooth + restriction input).
+struct FuseCtl {
+    int *sync;  // [0] item counter, [1 + t] stage-1 done flag of tile t (zeroed before each launch)
+    int tiles;  // tiles of the pass
+    int lag;    // stage-1 tile t + lag is claimed before stage-2 tile t
+    int dep;    // stage-2 dependency half-width in tiles (<= lag)
+};
+
+template <int R, int M1, int M2, bool DOT2>
+__global__ void __launch_bounds__(kSpanThreads, 6) k_span_fused(SpanView v, SpanArgs a1, SpanArgs a2, FuseCtl c) {
+    __shared__ double red[32 * R];
+    __shared__ int item_s;
+    const int T = c.tiles, lag = c.lag < T ? c.lag : T;
+    volatile int *flags = c.sync + 1;
+    while (true) {
+        if (threadIdx.x == 0) item_s = atomicAdd(c.sync, 1);
+        __syncthreads();
+        const int k = item_s;
+        __syncthreads();  // item_s is rewritten by the next claim
+        if (k >= 2 * T) break;
+        int stage, t;
+        if (k < lag) { stage = 1; t = k; }
+        else if (k < 2 * T - lag) {
+            const int m = k - lag;
+            stage = (m & 1) ? 2 : 1;
+            t = (m & 1) ? (m >> 1) : lag + (m >> 1);
+        } else { stage = 2; t = k - T; }
+        const int64_t q0 = (int64_t)t * kTile, q1 = q0 + kTile < v.L ? q0 + kTile : v.L;
+        double dot[R];
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) dot[cc] = 0.0;
+        if (stage == 1) {
+            if (threadIdx.x == 0) tile_prefetch<R, M1>(v, a1, q0, q1);
+            span_tile<R, M1, false, false>(v, a1, t, v.L, dot);
+            __syncthreads();  // every store of the tile issued
+            if (threadIdx.x == 0) {
+                __threadfence();
+                flags[t] = 1;
+            }
+        } else {
+            if (threadIdx.x < 32) {  // one warp polls the dependency window
+                const int lo = t - c.dep > 0 ? t - c.dep : 0, hi = t + c.dep < T - 1 ? t + c.dep : T - 1;
+                for (int qq = lo + (int)threadIdx.x; qq <= hi; qq += 32)
+                    while (flags[qq] == 0) __nanosleep(64);
+                __syncwarp();
+                __threadfence();
+            }
+            __syncthreads();
+            span_tile<R, M2, DOT2, false>(v, a2, t, v.L, dot);
+            if (DOT2) {
+                block_sum<R>(dot, red);
+                if (threadIdx.x == 0)
+#pragma unroll
+                    for (int cc = 0; cc < R; ++cc) a2.partials[t * R + cc] = dot[cc];
+            }
+        }
     }
 }
 
@@ -276,9 +362,10 @@ __global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArg
 // writes x0_c = od_c * r_c, the next level's implicit first Jacobi sweep.
 template <int R>
 __global__ void k_agg_sum(const int64_t *mptr, const int32_t *mpos, int64_t n_agg, const double *u, double *rc,
-                          const double *od_c, double *x0_c) {
+                          const double *od_c, double *x0_c, int rev) {
     using W = V<R>;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_agg; g += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_agg; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = rev ? n_agg - 1 - i : i;
         typename W::T s = W::zero();
         const int64_t q1 = mptr[g + 1];
         // 4 members in flight; the sum keeps the ascending member order
@@ -704,13 +791,14 @@ __global__ void k_update_xr(int64_t n, const double *scal, double *x, double *r,
 // split update for overlap: r -= alpha q (+ r.r) on the solve stream while
 // x += alpha p runs on a side stream during the next V-cycle
 template <int R>
-__global__ void k_update_r(int64_t n, const double *scal, double *r, const double *q, double *partials) {
+__global__ void k_update_r(int64_t n, const double *scal, double *r, const double *q, double *partials, int rev) {
     using W = V<R>;
     __shared__ double red[32 * R];
     double na[R], d[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) { na[c] = -scal[S_ALPHA + c]; d[c] = 0.0; }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = rev ? n - 1 - j : j;
         const typename W::T rv = vfma<R>(na, W::ld(q, i), W::ld(r, i));
         W::st(r, i, rv);
 #pragma unroll
@@ -722,24 +810,28 @@ __global__ void k_update_r(int64_t n, const double *scal, double *r, const doubl
         for (int c = 0; c < R; ++c) partials[blockIdx.x * R + c] = d[c];
 }
 template <int R>
-__global__ void k_update_x(int64_t n, const double *scal, double *x, const double *p) {
+__global__ void k_update_x(int64_t n, const double *scal, double *x, const double *p, int rev = 0) {
     using W = V<R>;
     double a[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) a[c] = scal[S_ALPHA + c];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = rev ? n - 1 - j : j;
         W::st(x, i, vfma<R>(a, W::ld(p, i), W::ld(x, i)));
+    }
 }
 
 // p = z + beta p
 template <int R>
-__global__ void k_xpby(int64_t n, const double *scal, const double *z, double *p) {
+__global__ void k_xpby(int64_t n, const double *scal, const double *z, double *p, int rev = 0) {
     using W = V<R>;
     double b[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) b[c] = scal[S_BETA + c];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = rev ? n - 1 - j : j;
         W::st(p, i, vfma<R>(b, W::ld(p, i), W::ld(z, i)));
+    }
 }
 
 // Sum per-CTA partials in index order; then apply `what`.
@@ -854,6 +946,21 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
     np = std::max<int64_t>(np, (int64_t)kDotGrid * 8);  // batched FGMRES block dots (k_mdot, 8 vectors)
     h.partials.alloc(np * 2 + 64);
     h.scal.alloc(S_END);
+    if (h.structured && h.op->n_tiles > 0) {
+        // reach of the z neighbours in positions: a row to the end of the row
+        // one plane above (the same bound holds downwards)
+        const Operator &op = *h.op;
+        std::vector<int4> rows(op.n_rows);
+        SPFD_CUDA(cudaMemcpy(rows.data(), op.rows.get(), op.n_rows * sizeof(int4), cudaMemcpyDeviceToHost));
+        int64_t reach = 0;
+        for (int64_t r = 0; r + op.NY < op.n_rows; ++r) {
+            const int4 a = rows[r], b = rows[r + op.NY];
+            reach = std::max<int64_t>(reach, (int64_t)b.x + (b.z - b.y) - a.x);
+        }
+        h.fuse_dep = (int)(reach / kTile) + 2;
+        h.fuse_sync.alloc(op.n_tiles + 1);
+        SPFD_CUDA(cudaMemset(h.fuse_sync.get(), 0, (op.n_tiles + 1) * sizeof(int)));
+    }
     SPFD_CUDA(cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking));
     SPFD_CUDA(cudaEventCreateWithFlags(&h.ev_alpha, cudaEventDisableTiming));
     SPFD_CUDA(cudaEventCreateWithFlags(&h.ev_x, cudaEventDisableTiming));
@@ -876,6 +983,11 @@ namespace {
 // streamed arrays bulk-prefetched into L2 (default), 2 = without the
 // prefetch (A/B); round-1/2 variants measured slower are documented in
 // DESIGN.md
+// 4 = kind 3 plus the two dependent pass pairs of the V-cycle fused into one
+// persistent launch each (k_span_fused; measured slower on C3, opt-in:
+// pre+restriction 279-287 us vs 2 x 134 us, prolongation+post 338-353 us vs
+// 178 + 146 us -- the passes are not HBM-bound, so serving the second
+// pass from L2 does not pay for the persistent scheduling)
 int fine_kernel_kind() {
     if (g_fine_kind_override >= 0) return g_fine_kind_override;
     static int v = -1;
@@ -884,8 +996,35 @@ int fine_kernel_kind() {
         v = 3;
         if (e && std::string(e) == "flat") v = 2;
         if (e && std::string(e) == "pf") v = 3;
+        if (e && std::string(e) == "fused") v = 4;
     }
     return v;
+}
+
+bool fused_fine(const Amg &h) { return h.structured && fine_kernel_kind() == 4 && h.fuse_sync.n > 0; }
+
+// stage-1 lead over stage 2 in tiles: the dependency reach plus about half
+// the resident CTAs, so stage-2 items rarely find their inputs unfinished
+inline int fuse_lag(const Amg &h) {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_FUSE_LAG");
+        v = e ? atoi(e) : 0;
+    }
+    const int lag = v > 0 ? v : 148 * 3 + 16;
+    return std::max(lag, h.fuse_dep);
+}
+
+template <int R, int M1, int M2, bool DOT2>
+int launch_fused(Amg &h, const SpanArgs &a1, const SpanArgs &a2, cudaStream_t s) {
+    const Operator &op = *h.op;
+    const int T = (int)op.n_tiles;
+    SPFD_CUDA(cudaMemsetAsync(h.fuse_sync.get(), 0, (T + 1) * sizeof(int), s));
+    FuseCtl c{h.fuse_sync.get(), T, std::min(fuse_lag(h), T), h.fuse_dep};
+    const int grid = std::min(2 * T, 148 * 6);
+    k_span_fused<R, M1, M2, DOT2><<<grid, kSpanThreads, 0, s>>>(span_view(op), a1, a2, c);
+    SPFD_LAUNCH_CHECK();
+    return T;
 }
 
 // Launch one fine-level stencil pass over the owned positions [a.pb, a.pe).
@@ -898,6 +1037,21 @@ inline int pf_ahead() {
         if (v < 0) v = 0;
     }
     return v;
+}
+
+// Alternate sweep directions of consecutive fine-level passes (SPFD_REV=0:
+// all forward).  CTAs retire roughly in launch order, so when a pass ends
+// the L2 (126 MB) holds the tail of what it touched; the next pass starting
+// from that end finds its first ~100 MB of weights / vectors there.  Chain
+// per PCG iteration: pre-smooth R, restriction input F, aggregate sums R |
+// prolongation F, post-smooth R, p update F, SpMV R, r update F.
+bool alt_dirs() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_REV");
+        v = (e && std::string(e) == "0") ? 0 : 1;
+    }
+    return v == 1;
 }
 
 template <int R, int MODE, bool DOT>
@@ -929,13 +1083,15 @@ int launch_fine(const Operator &op, const SpanArgs &a_in, cudaStream_t s) {
 
 // returns number of partial blocks written when DOT
 template <int R>
-int level0_apply(Amg &h, int mode, bool dot, const double *x, const double *r, double *y, cudaStream_t s) {
+int level0_apply(Amg &h, int mode, bool dot, const double *x, const double *r, double *y, cudaStream_t s,
+                 bool rev = false) {
     Level &L = h.lv[0];
     double *part = h.partials.get();
     if (h.structured) {
         int g = (int)h.op->n_tiles;
         if (g == 0) return 0;
         SpanArgs sa{x, r, L.odinv.get(), nullptr, nullptr, nullptr, y, part};
+        sa.rev = rev && alt_dirs();
         const Operator &op = *h.op;
         if (mode == 0) g = dot ? launch_fine<R, 0, true>(op, sa, s) : launch_fine<R, 0, false>(op, sa, s);
         else if (mode == 1) g = dot ? launch_fine<R, 1, true>(op, sa, s) : launch_fine<R, 1, false>(op, sa, s);
@@ -971,6 +1127,21 @@ void level_apply(Amg &h, int l, int mode, const double *x, const double *r, doub
 template <int R>
 void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s);
 
+// fused coarse-level prolongation + post-smooth z = od r + P e + od (d - (A P) e)
+template <int R>
+void launch_pp(const Level &L, const double *e, const double *r, const double *d, double *z, cudaStream_t s) {
+    const int G = std::min(L.ap_group, 32);
+    const int grid = csr_grid(L.P.rows, G);
+    const bool pf = csr_prefetch_enabled();
+    switch (G) {
+        case 4: k_csr_pp<4, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), e, r, L.odinv.get(), d, z, pf); break;
+        case 8: k_csr_pp<8, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), e, r, L.odinv.get(), d, z, pf); break;
+        case 16: k_csr_pp<16, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), e, r, L.odinv.get(), d, z, pf); break;
+        default: k_csr_pp<32, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), e, r, L.odinv.get(), d, z, pf); break;
+    }
+    SPFD_LAUNCH_CHECK();
+}
+
 // Fine level of a structured hierarchy, transfers matrix-free through the
 // aggregates (P = (I - omega D^-1 A) T, R = P^T):
 //   d  = r - A(od r)                      pre-smooth + defect
@@ -989,8 +1160,16 @@ int vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
     const size_t bytes = (size_t)L.nvec * R * sizeof(double);
     const double *od = L.odinv.get();
     const double *xbase = nullptr;
-    if (h.pre <= 1) {
-        launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, r, od, nullptr, nullptr, nullptr, d, nullptr}, s);
+    const int rv = alt_dirs() ? 1 : 0;
+    const bool fused = fused_fine(h);
+    if (h.pre <= 1 && fused) {
+        // d = r - A(od r) and u = d - A(od d) in one launch
+        launch_fused<R, 2, 2, false>(h, SpanArgs{nullptr, r, od, nullptr, nullptr, nullptr, d, nullptr},
+                                     SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr}, s);
+    } else if (h.pre <= 1) {
+        SpanArgs sa{nullptr, r, od, nullptr, nullptr, nullptr, d, nullptr};
+        sa.rev = rv;
+        launch_fine<R, 2, false>(*h.op, sa, s);
     } else {
         k_odinv_r<R><<<grid_for(L.nvec, 256, 148 * 16), 256, 0, s>>>(L.nvec, od, r, t);
         for (int it = 1; it < h.pre; ++it) {
@@ -1001,14 +1180,20 @@ int vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
         xbase = t;
     }
     SPFD_LAUNCH_CHECK();
-    launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr}, s);
+    if (!(h.pre <= 1 && fused))
+        launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr}, s);
     SPFD_LAUNCH_CHECK();
     // level 1 gets r_1 and (when it smooths) its first Jacobi iterate od_1 r_1
     const bool x0 = h.pre <= 1 && (int)h.lv.size() > 2;
     k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n, u, C.vr.get(),
-                                                             C.odinv.get(), x0 ? C.vt.get() : nullptr);
+                                                             C.odinv.get(), x0 ? C.vt.get() : nullptr, rv);
     SPFD_LAUNCH_CHECK();
     vcycle_level<R>(h, 1, C.vr.get(), C.vx.get(), s);
+    if (fused && h.post == 1) {
+        // x1 = base + e - od A e and z = x1 + od (r - A x1) (+ r.z) in one launch
+        return launch_fused<R, 4, 3, true>(h, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr},
+                                           SpanArgs{d, r, od, nullptr, nullptr, nullptr, z, h.partials.get()}, s);
+    }
     launch_fine<R, 4, false>(*h.op, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr}, s);
     SPFD_LAUNCH_CHECK();
     if (h.post == 0) {
@@ -1021,6 +1206,7 @@ int vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
         const bool last = it == h.post - 1;
         double *dst = last ? z : (cur == d ? t : d);
         SpanArgs sa{cur, r, od, nullptr, nullptr, nullptr, dst, h.partials.get()};
+        sa.rev = (h.post - it) & 1 ? rv : 0;   // the last sweep runs reversed
         if (last) parts = launch_fine<R, 3, true>(*h.op, sa, s);
         else launch_fine<R, 3, false>(*h.op, sa, s);
         cur = dst;
@@ -1074,15 +1260,7 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
                             x0 ? C.vt.get() : nullptr);
     vcycle_level<R>(h, l + 1, C.vr.get(), C.vx.get(), s);
     if (L.AP.rows > 0 && h.pre == 1 && h.post == 1) {
-        // fused prolongation + post-smooth from the pre-smoothing defect d
-        const int grid = csr_grid(L.P.rows, std::min(L.ap_group, 32));
-        switch (std::min(L.ap_group, 32)) {
-            case 4: k_csr_pp<4, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z, csr_prefetch_enabled()); break;
-            case 8: k_csr_pp<8, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z, csr_prefetch_enabled()); break;
-            case 16: k_csr_pp<16, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z, csr_prefetch_enabled()); break;
-            default: k_csr_pp<32, R><<<grid, kCsrThreads, 0, s>>>(view(L.P), view(L.AP), C.vx.get(), r, L.odinv.get(), d, z, csr_prefetch_enabled()); break;
-        }
-        SPFD_LAUNCH_CHECK();
+        launch_pp<R>(L, C.vx.get(), r, d, z, s);  // fused prolongation + post-smooth from the defect d
         return;
     }
     // x1 = x + P e (linsolve.py:194) -> d
@@ -1164,7 +1342,9 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
             restart = false;
         }
         if (it >= cfg.max_iters) break;
-        int g = level0_apply<R>(h, 0, true, p, nullptr, q, s);  // q = A p, p.q
+        const bool fz = fused_fine(h);  // fused V-cycle passes run forward: flip the chain
+        const int rv = alt_dirs() && fz ? 1 : 0;
+        int g = level0_apply<R>(h, 0, true, p, nullptr, q, s, !fz);  // q = A p, p.q
         finalize<R>(h, g, S_PQ, F_ALPHA, s);
         // x += alpha p on the side stream, overlapping the V-cycle (which is
         // L1/latency-bound and leaves HBM bandwidth idle); joined before p changes
@@ -1173,7 +1353,7 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
         k_update_x<R><<<grid_for(n, 256, 148 * 8), 256, 0, h.side>>>(n, sc, x, p);
         SPFD_LAUNCH_CHECK();
         SPFD_CUDA(cudaEventRecord(h.ev_x, h.side));
-        k_update_r<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, r, q, h.partials.get());
+        k_update_r<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, r, q, h.partials.get(), rv);
         SPFD_LAUNCH_CHECK();
         finalize<R>(h, kDotGrid, S_RR, F_STORE, s);
         k_set_active<<<1, 1, 0, s>>>(sc, R, tol);
@@ -1211,7 +1391,7 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
         if (h.vc_partials > 0) finalize<R>(h, h.vc_partials, S_RZ, F_BETA, s);  // r.z fused into the post-smooth
         else dot<R>(h, n, r, z, S_RZ, F_BETA, s);
         SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));  // x += alpha p done before p changes
-        k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p);
+        k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, alt_dirs() && fused_fine(h) ? 1 : 0);
         SPFD_LAUNCH_CHECK();
     }
     SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
@@ -1258,11 +1438,13 @@ void pcg_body(Amg &h, cudaGraphConditionalHandle hnd, cudaStream_t s) {
     if (h.vc_partials > 0) finalize<R>(h, h.vc_partials, S_RZ, F_BETA_AUTO, s);
     else dot<R>(h, n, r, z, S_RZ, F_BETA_AUTO, s);
     SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
-    k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p);
+    const bool fz = fused_fine(h);  // fused V-cycle passes run forward: flip the chain
+    const int rv = alt_dirs() && fz ? 1 : 0;
+    k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, rv);
     SPFD_LAUNCH_CHECK();
-    const int g = level0_apply<R>(h, 0, true, p, nullptr, q, s);  // q = A p, p.q
+    const int g = level0_apply<R>(h, 0, true, p, nullptr, q, s, !fz);  // q = A p, p.q
     finalize<R>(h, g, S_PQ, F_ALPHA, s);
-    k_update_r<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, r, q, h.partials.get());
+    k_update_r<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, r, q, h.partials.get(), rv);
     SPFD_LAUNCH_CHECK();
     finalize<R>(h, kDotGrid, S_RR, F_STORE, s);
     k_check<<<1, 1, 0, s>>>(sc, R, h.pcg_trace.get(), hnd);
@@ -1932,36 +2114,160 @@ spfd_report fgmres1(Amg &h, const double *b, double *x, const spfd_config &cfg, 
 // Back-to-back launches of one level-0 kernel between two events on `s`
 // (bench.py roofline).  Returns ms per launch; *bytes = algorithmic bytes
 // per launch (each distinct array read or written once).
+// Algorithmic bytes per launch of the solve's kernels (each distinct array
+// counted once per launch; R = rhs batched).
+namespace {
+double csr_bytes(const Csr &m) { return m.rows > 0 ? 12.0 * (double)m.nnz + 8.0 * (double)(m.rows + 1) : 0.0; }
+
+struct KernelBytes {
+    double spmv = 0, presmooth = 0, postsmooth = 0, prolong = 0, aggsum = 0, blas1 = 0;
+    double l1_pre = 0, l1_pp = 0;
+};
+
+KernelBytes kernel_bytes(const Amg &h, double R) {
+    KernelBytes k;
+    const double n = (double)h.lv[0].nvec;
+    k.blas1 = n * 24.0 * R;  // r update / x update / p update: read 2, write 1
+    if (h.structured) {
+        const double mask = n / 8.0;
+        k.spmv = n * (24.0 + 16.0 * R) + mask;          // w; x -> y
+        k.presmooth = n * (32.0 + 16.0 * R) + mask;     // w, odinv; r -> d
+        k.postsmooth = n * (32.0 + 24.0 * R) + mask;    // w, odinv; x, r -> x'
+        if (h.lv.size() > 1) {
+            const double n1 = (double)h.lv[1].n;
+            k.prolong = n * (36.0 + 16.0 * R) + mask + n1 * 8.0 * R;  // w, odinv, agg; r -> x1; e_c
+            k.aggsum = n * (4.0 + 8.0 * R) + n1 * (8.0 + 8.0 + 16.0 * R);  // members, u; ptr, od_c -> r_c, x0_c
+        }
+    } else {
+        const Level &L = h.lv[0];
+        k.spmv = csr_bytes(L.A) + n * 16.0 * R;
+        k.presmooth = csr_bytes(L.A) + n * (8.0 + 16.0 * R);
+        k.postsmooth = csr_bytes(L.A) + n * (8.0 + 24.0 * R);
+    }
+    if (h.lv.size() > 2) {
+        const Level &L = h.lv[1];
+        const double n1 = (double)L.n, n2 = (double)h.lv[2].n;
+        k.l1_pre = csr_bytes(L.A) + n1 * 24.0 * R;                              // r, x0 -> d
+        if (L.AP.rows > 0) k.l1_pp = csr_bytes(L.P) + csr_bytes(L.AP) + n1 * (8.0 + 32.0 * R) + n2 * 8.0 * R;
+    }
+    return k;
+}
+
+// one V-cycle below level 0 (CSR levels) + the coarsest dense solve
+double coarse_vcycle_bytes(const Amg &h, int l0, double R) {
+    double b = 0.0;
+    const int nl = (int)h.lv.size();
+    for (int l = l0; l < nl - 1; ++l) {
+        const Level &L = h.lv[l];
+        const double n = (double)L.n, nc = (double)h.lv[l + 1].n;
+        b += csr_bytes(L.A) + n * 24.0 * R;                         // pre-smooth residual
+        b += csr_bytes(L.R) + n * 8.0 * R + nc * (8.0 + 16.0 * R);  // restriction (+ od r_c)
+        if (L.AP.rows > 0 && h.pre == 1 && h.post == 1) b += csr_bytes(L.P) + csr_bytes(L.AP) + n * (8.0 + 32.0 * R) + nc * 8.0 * R;
+        else b += csr_bytes(L.P) + csr_bytes(L.A) + n * (8.0 + 56.0 * R) + nc * 8.0 * R;
+    }
+    b += (double)h.nc * (double)h.nc * 8.0 + (double)h.nc * 16.0 * R;
+    return b;
+}
+}  // namespace
+
+double amg_iteration_bytes(const Amg &h, int nrhs) {
+    const double R = nrhs;
+    const KernelBytes k = kernel_bytes(h, R);
+    double b = k.spmv + 3.0 * k.blas1;  // q = A p; r, x, p updates
+    if (h.lv.size() == 1) return b + coarse_vcycle_bytes(h, 0, R);
+    const double pos = h.structured ? (double)h.op->L : 0.0;
+    if (h.structured && fused_fine(h) && h.pre <= 1 && h.post == 1)  // d and x1 written once, read from L2
+        b += k.presmooth + pos * 16.0 * R + k.aggsum + k.prolong + pos * 16.0 * R + coarse_vcycle_bytes(h, 1, R);
+    else if (h.structured) b += 2.0 * k.presmooth + k.aggsum + k.prolong + k.postsmooth + coarse_vcycle_bytes(h, 1, R);
+    else b += coarse_vcycle_bytes(h, 0, R);
+    return b;
+}
+
 double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cudaStream_t s) {
     SPFD_CHECK(nrhs >= 1 && nrhs <= h.max_nrhs && reps >= 1, SPFD_EINVAL, "bad bench arguments");
     Level &L = h.lv[0];
     int64_t n = L.nvec;
+    const bool two = h.lv.size() > 1, three = h.lv.size() > 2;
+    SPFD_CHECK(!(which == 4 || which == 5) || (h.structured && two), SPFD_EINVAL,
+               "kernel needs a structured hierarchy with a coarse level");
+    SPFD_CHECK(!(which == 6 || which == 7) || three, SPFD_EINVAL, "kernel needs three levels");
+    SPFD_CHECK(which != 7 || h.lv[1].AP.rows > 0, SPFD_EINVAL, "level 1 has no fused prolongation");
     SPFD_CUDA(cudaMemsetAsync(h.kp.get(), 0x3f, n * nrhs * sizeof(double), s));
     SPFD_CUDA(cudaMemsetAsync(h.kr.get(), 0x3e, n * nrhs * sizeof(double), s));
-    double R = nrhs;
-    double b = 0.0;
-    if (h.structured) {
-        double pos = (double)h.op->L;
-        double mask = pos / 8.0;
-        if (which == 0) b = pos * (24.0 + 16.0 * R) + mask;              // w, x -> y
-        else if (which == 1) b = pos * (32.0 + 16.0 * R) + mask;         // w, odinv, r -> d
-        else if (which == 2) b = pos * (32.0 + 24.0 * R) + mask;         // w, odinv, x, r -> x'
-        else b = 0.0;
-    } else {
-        double nnz = (double)L.A.nnz, rows = (double)L.A.rows;
-        double mat = nnz * 12.0 + (rows + 1) * 8.0;
-        if (which == 0) b = mat + rows * 16.0 * R;
-        else if (which == 1) b = mat + rows * (8.0 + 16.0 * R);
-        else if (which == 2) b = mat + rows * (8.0 + 24.0 * R);
+    SPFD_CUDA(cudaMemsetAsync(h.kz.get(), 0x3e, n * nrhs * sizeof(double), s));
+    SPFD_CUDA(cudaMemsetAsync(h.scal.get(), 0, S_END * sizeof(double), s));
+    for (int l = 1; l < (int)h.lv.size(); ++l) {
+        Level &C = h.lv[l];
+        const size_t vb = (size_t)C.nvec * nrhs * sizeof(double);
+        for (DevBuf<double> *v : {&C.vr, &C.vx, &C.vd, &C.vt}) SPFD_CUDA(cudaMemsetAsync(v->get(), 0x3e, vb, s));
     }
-    auto launch = [&]() {
-        if (which == 3) {
-            amg_vcycle(h, h.kr.get(), h.kz.get(), nrhs, s);
-            return;
+    SPFD_CHECK(which < 10 || (fused_fine(h) && two && h.pre <= 1 && h.post == 1), SPFD_EINVAL,
+               "fused fine passes are not in use");
+    const KernelBytes kb = kernel_bytes(h, nrhs);
+    const double Rd = nrhs, pos = h.structured ? (double)h.op->L : 0.0;
+    const double byt[12] = {kb.spmv, kb.presmooth, kb.postsmooth, 0.0, kb.prolong, kb.aggsum, kb.l1_pre, kb.l1_pp,
+                            kb.blas1, kb.blas1,
+                            kb.presmooth + pos * 16.0 * Rd,     // fused: r, od, w -> d, u
+                            kb.prolong + pos * 16.0 * Rd};      // fused: w, od, agg, r, e_c -> x1, z
+    auto launch2 = [&](auto rt) {
+        constexpr int R = decltype(rt)::value;
+        double *p = h.kp.get(), *r = h.kr.get(), *q = h.kq.get(), *z = h.kz.get();
+        switch (which) {
+            case 3: amg_vcycle(h, r, z, R, s); break;
+            case 4: {
+                Level &C = h.lv[1];
+                SpanArgs sa{nullptr, r, L.odinv.get(), nullptr, C.vx.get(), L.agg_pos.get(), q, nullptr};
+                launch_fine<R, 4, false>(*h.op, sa, s);
+                break;
+            }
+            case 5: {
+                Level &C = h.lv[1];
+                k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n, p,
+                                                                         C.vr.get(), C.odinv.get(), C.vt.get(), 0);
+                SPFD_LAUNCH_CHECK();
+                break;
+            }
+            case 6: {
+                Level &C = h.lv[1];
+                launch_csr<R, 1, false>(C.A, C.a_group, C.vt.get(), C.vr.get(), C.odinv.get(), nullptr, C.vd.get(),
+                                        nullptr, s);
+                break;
+            }
+            case 7: {
+                Level &C = h.lv[1];
+                launch_pp<R>(C, h.lv[2].vx.get(), C.vr.get(), C.vd.get(), C.vt.get(), s);
+                break;
+            }
+            case 8:
+                k_update_r<R><<<kDotGrid, kDotThreads, 0, s>>>(n, h.scal.get(), r, q, h.partials.get(), 0);
+                SPFD_LAUNCH_CHECK();
+                break;
+            case 9:
+                k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h.scal.get(), z, p);
+                SPFD_LAUNCH_CHECK();
+                break;
+            case 10: {
+                const double *od = L.odinv.get();
+                launch_fused<R, 2, 2, false>(h, SpanArgs{nullptr, r, od, nullptr, nullptr, nullptr, L.vd.get(), nullptr},
+                                             SpanArgs{nullptr, L.vd.get(), od, nullptr, nullptr, nullptr, q, nullptr}, s);
+                break;
+            }
+            case 11: {
+                const double *od = L.odinv.get();
+                Level &C = h.lv[1];
+                launch_fused<R, 4, 3, true>(h, SpanArgs{nullptr, r, od, nullptr, C.vx.get(), L.agg_pos.get(), L.vd.get(), nullptr},
+                                            SpanArgs{L.vd.get(), r, od, nullptr, nullptr, nullptr, q, h.partials.get()}, s);
+                break;
+            }
+            default: {
+                const int mode = which == 0 ? 0 : (which == 1 ? 2 : 3);
+                level0_apply<R>(h, mode, which != 1, p, r, q, s);
+            }
         }
-        int mode = which == 0 ? 0 : (which == 1 ? 2 : 3);
-        if (nrhs == 1) level0_apply<1>(h, mode, which == 0, h.kp.get(), h.kr.get(), h.kq.get(), s);
-        else level0_apply<2>(h, mode, which == 0, h.kp.get(), h.kr.get(), h.kq.get(), s);
+    };
+    auto launch = [&]() {
+        if (nrhs == 1) launch2(std::integral_constant<int, 1>{});
+        else launch2(std::integral_constant<int, 2>{});
     };
     for (int i = 0; i < 3; ++i) launch();
     cudaEvent_t e0, e1;
@@ -1975,7 +2281,8 @@ double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cu
     SPFD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    *bytes = b;
+    *bytes = byt[which];
+    if (which == 3) *bytes = amg_iteration_bytes(h, nrhs) - kb.spmv - 3.0 * kb.blas1;
     return ms / reps;
 }
 

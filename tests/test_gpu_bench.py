@@ -31,6 +31,7 @@ def test_bench_json_contract():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    assert 0 < r["step"]["frac"] < 1.5 and len(d["kernels"]) >= 4
     e = d["e2e"]
     assert e["value"] >= d["value"] * 0.9 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0

@@ -1,6 +1,7 @@
-"""GPU A/B of the fine-level stencil kernel with and without the tile's L2
-bulk prefetch (every stencil mode bit-identical, so V-cycles give the same
-bits; Krylov solves agree to tolerance), plus the graph / host-loop and
+"""GPU A/B of the fine-level stencil kernels: flat, with the tile's L2 bulk
+prefetch, and with the V-cycle's dependent pass pairs fused into one
+persistent launch (every stencil mode bit-identical, so V-cycles give the
+same bits; Krylov solves agree to tolerance), plus the graph / host-loop and
 block / MGS solver A/B tests.
 
 Every stencil mode must be bit-identical between the two kernels, so a
@@ -20,8 +21,8 @@ from conftest import golden_cases, golden_model, load_golden
 
 pytestmark = pytest.mark.gpu
 
-FLAT, PF = 2, 3
-KINDS = (PF, FLAT)
+FLAT, PF, FUSED = 2, 3, 4
+KINDS = (FUSED, PF, FLAT)
 
 
 def _set_kernel(kind):
