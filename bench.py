@@ -403,6 +403,16 @@ def main():
                 "reps": args.tol_reps}
             log(f"[bench] rel_tol {tv:g}: step {ms_s:.2f} ms ({rep_s.iterations} it), fgmres single rhs "
                 f"{ms_f:.2f} ms ({rep_f.iterations} it), fgmres pair {ms_fp:.2f} ms")
+        # the optional Chebyshev smoother (degree 2) on the same step, own hierarchy
+        c_ch = SolveConfig(rel_tol=REL_TOL, max_nrhs=2, smoother="chebyshev", chebyshev_degree=2)
+        sess_ch = Session(w.model, w.frequency_hz, c_ch)
+        ms_c, rep_c = _timed(lambda: sess_ch.snapshot(a_dev)[1], args.tol_reps)
+        tolerances["chebyshev_smoother"] = {
+            "rel_tol": REL_TOL, "degree": 2, "step_pcg_pair_s": ms_c / 1e3, "step_pcg_iterations": rep_c.iterations,
+            "setup_s": sess_ch.hierarchy.setup_seconds, "lambda_max": sess_ch.hierarchy.chebyshev_lmax,
+            "reps": args.tol_reps}
+        log(f"[bench] chebyshev(2) smoother: step {ms_c:.2f} ms ({rep_c.iterations} it)")
+        del sess_ch
 
     # per-kernel rooflines (each kernel timed alone, back to back on the solve
     # stream with CUDA events) and the kernel with the largest share of the step

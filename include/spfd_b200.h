@@ -151,9 +151,15 @@ typedef struct {
     int32_t max_levels;          /* 20                                       */
     int32_t method;              /* SPFD_METHOD_PCG | SPFD_METHOD_FGMRES     */
     int32_t max_nrhs;            /* workspace sizing: 1 or 2                 */
+    int32_t smoother;            /* SPFD_SMOOTHER_JACOBI (0, the reference's
+                                    damped Jacobi) | SPFD_SMOOTHER_CHEBYSHEV */
+    int32_t cheb_degree;         /* Chebyshev polynomial degree per sweep
+                                    (0 -> 2); pre/post_sweeps repeat it      */
 } spfd_config;
 #define SPFD_METHOD_PCG    0
 #define SPFD_METHOD_FGMRES 1
+#define SPFD_SMOOTHER_JACOBI    0
+#define SPFD_SMOOTHER_CHEBYSHEV 1
 
 typedef struct {
     int32_t n_levels;
@@ -163,6 +169,10 @@ typedef struct {
     double  setup_seconds;       /* device-timed                             */
     int64_t device_bytes;
     int32_t structured;          /* 1 = level 0 is the matrix-free stencil   */
+    int32_t smoother;            /* SPFD_SMOOTHER_*                          */
+    int32_t cheb_degree;
+    double  cheb_lmax[32];       /* Chebyshev: power-iteration estimate of
+                                    lambda_max(D^-1 A_l) per level           */
 } spfd_amg_info;
 
 /* Hierarchy on the operator (level 0 = matrix-free stencil) or on a

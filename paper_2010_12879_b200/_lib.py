@@ -40,6 +40,7 @@ EXPORT_DIAGONAL = 5
 
 METHOD_PCG = 0
 METHOD_FGMRES = 1
+SMOOTHER_JACOBI, SMOOTHER_CHEBYSHEV = 0, 1
 
 
 class OpInfo(ctypes.Structure):
@@ -71,6 +72,8 @@ class Config(ctypes.Structure):
         ("max_levels", ctypes.c_int32),
         ("method", ctypes.c_int32),
         ("max_nrhs", ctypes.c_int32),
+        ("smoother", ctypes.c_int32),
+        ("cheb_degree", ctypes.c_int32),
     ]
 
 
@@ -83,6 +86,9 @@ class AmgInfo(ctypes.Structure):
         ("setup_seconds", ctypes.c_double),
         ("device_bytes", ctypes.c_int64),
         ("structured", ctypes.c_int32),
+        ("smoother", ctypes.c_int32),
+        ("cheb_degree", ctypes.c_int32),
+        ("cheb_lmax", ctypes.c_double * 32),
     ]
 
 
@@ -261,4 +267,6 @@ def make_config(cfg, method=None, max_nrhs=None):
     m = method if method is not None else getattr(cfg, "method", "pcg")
     c.method = METHOD_FGMRES if m == "fgmres" else METHOD_PCG
     c.max_nrhs = int(max_nrhs if max_nrhs is not None else getattr(cfg, "max_nrhs", 2))
+    c.smoother = SMOOTHER_CHEBYSHEV if getattr(cfg, "smoother", "jacobi") == "chebyshev" else SMOOTHER_JACOBI
+    c.cheb_degree = int(getattr(cfg, "chebyshev_degree", 2))
     return c

@@ -56,6 +56,9 @@ struct Amg {
     DevBuf<double> cinv;      // dense inverse of the coarsest matrix (nc x nc)
     double omega = 2.0 / 3.0;
     int pre = 1, post = 1;
+    int smoother = 0;         // SPFD_SMOOTHER_JACOBI | SPFD_SMOOTHER_CHEBYSHEV
+    int cheb_deg = 2;         // Chebyshev polynomial degree per sweep
+    std::vector<double> cheb_lmax;  // lambda_max(D^-1 A_l) estimates (Chebyshev)
     int max_nrhs = 2;
     double setup_seconds = 0.0;
     // Krylov workspace (level-0 layout, interleaved nrhs)
@@ -115,6 +118,8 @@ void dist_info(const Amg &h, int64_t *out);  // pb, pe, voxel-row begin, end
 double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cudaStream_t s);
 // algorithmic bytes of one PCG iteration (SpMV, V-cycle, vector updates)
 double amg_iteration_bytes(const Amg &h, int nrhs);
+// Chebyshev smoother: power-iteration estimates of lambda_max(D^-1 A_l)
+void amg_estimate_lmax(Amg &h, cudaStream_t s);
 spfd_report krylov_solve(Amg &h, const double *b_inter, double *x_inter, int nrhs, const spfd_config &cfg,
                          double *h_trace, cudaStream_t s);
 

@@ -1021,6 +1021,11 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
     h->omega = cfg.jacobi_damping;
     h->pre = cfg.pre_sweeps;
     h->post = cfg.post_sweeps;
+    SPFD_CHECK(cfg.smoother == SPFD_SMOOTHER_JACOBI || cfg.smoother == SPFD_SMOOTHER_CHEBYSHEV, SPFD_EINVAL,
+               "unknown smoother");
+    SPFD_CHECK(cfg.cheb_degree >= 0 && cfg.cheb_degree <= 16, SPFD_EINVAL, "chebyshev degree must be in [1, 16]");
+    h->smoother = cfg.smoother;
+    h->cheb_deg = cfg.cheb_degree > 0 ? cfg.cheb_degree : 2;
     h->max_nrhs = cfg.max_nrhs < 1 ? 1 : (cfg.max_nrhs > 2 ? 2 : cfg.max_nrhs);
     int R = h->max_nrhs;
 
@@ -1101,7 +1106,7 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
         // defect replaces "x1 = x0 + P e; z = x1 + od (r - A x1)" -- one pass over
         // P and A P (whose gathers hit the small coarse vector) instead of P and A
         static const bool use_ap = !(getenv("SPFD_AP") && std::string(getenv("SPFD_AP")) == "0");
-        if (use_ap && l >= 1 && l < nl - 1 && h->pre == 1 && h->post == 1) {
+        if (use_ap && l >= 1 && l < nl - 1 && h->pre == 1 && h->post == 1 && h->smoother == SPFD_SMOOTHER_JACOBI) {
             spgemm(view(L.A), view(L.P), L.P.cols, L.AP, false, s);
             // only where A P is no larger than A (C3: levels 2-3; on level 1
             // the product holds ~1.3x A's entries and measured no faster)
@@ -1130,6 +1135,7 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
     if (!(getenv("SPFD_MORTON") && std::string(getenv("SPFD_MORTON")) == "0") && h->structured && nl > 2)
         morton_level1(*h, s);
     alloc_krylov(*h, h->lv[0].nvec, R);
+    if (h->smoother == SPFD_SMOOTHER_CHEBYSHEV) amg_estimate_lmax(*h, s);
     SPFD_CUDA(cudaEventRecord(e1, s));
     SPFD_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;

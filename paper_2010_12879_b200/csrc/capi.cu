@@ -219,6 +219,9 @@ int spfd_amg_info_get(spfd_amg_t h, spfd_amg_info *info) {
         info->setup_seconds = a.setup_seconds;
         info->device_bytes = a.device_bytes();
         info->structured = a.structured ? 1 : 0;
+        info->smoother = a.smoother;
+        info->cheb_degree = a.cheb_deg;
+        for (size_t l = 0; l < a.cheb_lmax.size() && l < 32; ++l) info->cheb_lmax[l] = a.cheb_lmax[l];
     });
 }
 

@@ -433,6 +433,7 @@ void amg_distribute_impl(Amg &h, Comm *comm, int64_t replicate_below, int64_t *r
     // validate everything before touching the hierarchy
     SPFD_CHECK(h.structured, SPFD_EINVAL, "distribution needs an operator (structured) hierarchy");
     SPFD_CHECK(h.pre <= 1 && h.post == 1, SPFD_EINVAL, "distributed V-cycle supports pre_sweeps <= 1, post_sweeps == 1");
+    SPFD_CHECK(h.smoother == SPFD_SMOOTHER_JACOBI, SPFD_EINVAL, "distributed V-cycle supports the Jacobi smoother");
     SPFD_CHECK(comm != nullptr && comm->size >= 1 && comm->rank >= 0 && comm->rank < comm->size, SPFD_EINVAL,
                "invalid communicator");
     SPFD_CHECK(h.op->NZ >= 2 * comm->size, SPFD_EINVAL, "fewer than two node planes per rank");

@@ -1279,12 +1279,216 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
     }
 }
 
+// ---- Chebyshev smoother (SPFD_SMOOTHER_CHEBYSHEV) -------------------------
+// Polynomial smoother in D^-1 A on [beta / 5, beta], beta = 1.1 x the
+// power-iteration estimate of lambda_max (lower end 0.2 beta, see
+// oracle/spfd_oracle.py chebyshev_coefficients), three-term
+// recurrence (Saad, Iterative Methods, alg. 12.1):
+//   d_0 = (1/theta) D^-1 r_0,  x_1 = x_0 + d_0
+//   rho_k = 1 / (2 sigma - rho_{k-1}),  d_k = rho_k rho_{k-1} d_{k-1} + (2 rho_k / delta) D^-1 r_k
+// with theta = (beta + alpha) / 2, delta = (beta - alpha) / 2, sigma = theta / delta,
+// rho_0 = 1 / sigma, r_k = b - A x_k.  The same polynomial before and after
+// the coarse correction keeps the V-cycle symmetric (a valid PCG
+// preconditioner).  The reference has damped Jacobi only (linsolve.py:184-197);
+// this is the north_star's optional smoother, restated in oracle/.
+template <int R>
+__global__ void k_cheb_first(int64_t n, const double *__restrict__ dinv, double c0, const double *t, double *d,
+                             const double *xin, double *xout) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double di = dinv[i];
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            const double dv = c0 * (di * t[i * R + c]);
+            d[i * R + c] = dv;
+            xout[i * R + c] = xin ? xin[i * R + c] + dv : dv;
+        }
+    }
+}
+
+template <int R>
+__global__ void k_cheb_step(int64_t n, const double *__restrict__ dinv, double c1, double c2,
+                            const double *__restrict__ t, double *__restrict__ d, double *__restrict__ x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double di = dinv[i];
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            const double dv = c1 * d[i * R + c] + c2 * (di * t[i * R + c]);
+            d[i * R + c] = dv;
+            x[i * R + c] += dv;
+        }
+    }
+}
+
+struct ChebCoef {
+    double c0;
+    double c1[16], c2[16];  // step k = 1 .. degree-1
+};
+
+ChebCoef cheb_coef(double lmax, int degree) {
+    const double beta = 1.1 * lmax, alpha = 0.2 * beta;
+    const double theta = 0.5 * (beta + alpha), delta = 0.5 * (beta - alpha), sigma = theta / delta;
+    ChebCoef c{};
+    c.c0 = 1.0 / theta;
+    double rho = 1.0 / sigma;
+    for (int k = 1; k < degree && k < 16; ++k) {
+        const double rn = 1.0 / (2.0 * sigma - rho);
+        c.c1[k] = rn * rho;
+        c.c2[k] = 2.0 * rn / delta;
+        rho = rn;
+    }
+    return c;
+}
+
+// residual y = b - A_l x on level l (span layout on a structured level 0)
+template <int R>
+void level_residual(Amg &h, int l, const double *x, const double *b, double *y, cudaStream_t s) {
+    if (l == 0) level0_apply<R>(h, 1, false, x, b, y, s);
+    else level_apply<R>(h, l, 1, x, b, y, s);
+}
+
+// one polynomial sweep on x (x == nullptr: from x = 0 into xout); t, d scratch
+template <int R>
+void cheb_sweep(Amg &h, int l, const ChebCoef &c, const double *b, const double *xin, double *xout, double *t,
+                double *d, cudaStream_t s) {
+    Level &L = h.lv[l];
+    const int64_t n = L.nvec;
+    const int g = grid_for(n, 256, 148 * 16);
+    if (xin) {
+        level_residual<R>(h, l, xin, b, t, s);
+        k_cheb_first<R><<<g, 256, 0, s>>>(n, L.dinv.get(), c.c0, t, d, xin, xout);
+    } else {
+        k_cheb_first<R><<<g, 256, 0, s>>>(n, L.dinv.get(), c.c0, b, d, nullptr, xout);
+    }
+    SPFD_LAUNCH_CHECK();
+    for (int k = 1; k < h.cheb_deg; ++k) {
+        level_residual<R>(h, l, xout, b, t, s);
+        k_cheb_step<R><<<g, 256, 0, s>>>(n, L.dinv.get(), c.c1[k], c.c2[k], t, d, xout);
+        SPFD_LAUNCH_CHECK();
+    }
+}
+
+template <int R>
+void vcycle_cheb(Amg &h, int l, const double *r, double *z, cudaStream_t s) {
+    const int nl = (int)h.lv.size();
+    if (l == nl - 1) {  // coarsest: the dense inverse
+        vcycle_level<R>(h, l, r, z, s);
+        return;
+    }
+    Level &L = h.lv[l];
+    Level &C = h.lv[l + 1];
+    double *d = L.vd.get(), *t = L.vt.get();
+    const ChebCoef c = cheb_coef(h.cheb_lmax[l], h.cheb_deg);
+    // pre-smoothing from x = 0 (z holds the iterate)
+    cheb_sweep<R>(h, l, c, r, nullptr, z, t, d, s);
+    for (int k = 1; k < h.pre; ++k) cheb_sweep<R>(h, l, c, r, z, z, t, d, s);
+    if (h.pre == 0) SPFD_CUDA(cudaMemsetAsync(z, 0, (size_t)L.nvec * R * sizeof(double), s));
+    // residual, restriction
+    level_residual<R>(h, l, z, r, t, s);
+    if (l == 0 && h.structured) {
+        double *u = L.vr.get();  // R t = T^T (t - A (omega D^-1 t))
+        launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, t, L.odinv.get(), nullptr, nullptr, nullptr, u, nullptr}, s);
+        k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n, u,
+                                                                 C.vr.get(), nullptr, nullptr, 0);
+        SPFD_LAUNCH_CHECK();
+    } else {
+        launch_csr<R, 0, false>(L.R, L.r_group, t, nullptr, nullptr, nullptr, C.vr.get(), nullptr, s);
+    }
+    vcycle_cheb<R>(h, l + 1, C.vr.get(), C.vx.get(), s);
+    // x1 = x + P e -> t
+    if (l == 0 && h.structured)
+        launch_fine<R, 4, false>(*h.op, SpanArgs{nullptr, r, L.odinv.get(), z, C.vx.get(), L.agg_pos.get(), t, nullptr},
+                                 s);
+    else
+        launch_csr<R, 5, false>(L.P, L.p_group, C.vx.get(), r, L.odinv.get(), z, t, nullptr, s);
+    SPFD_LAUNCH_CHECK();
+    // post-smoothing from x1 (the first sweep moves the iterate from t to z)
+    if (h.post == 0) {
+        SPFD_CUDA(cudaMemcpyAsync(z, t, (size_t)L.nvec * R * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    {
+        // residual into d, then d := c0 D^-1 d in place and z = t + d
+        level_residual<R>(h, l, t, r, d, s);
+        const int g = grid_for(L.nvec, 256, 148 * 16);
+        k_cheb_first<R><<<g, 256, 0, s>>>(L.nvec, L.dinv.get(), c.c0, d, d, t, z);
+        SPFD_LAUNCH_CHECK();
+        for (int k = 1; k < h.cheb_deg; ++k) {
+            level_residual<R>(h, l, z, r, t, s);
+            k_cheb_step<R><<<g, 256, 0, s>>>(L.nvec, L.dinv.get(), c.c1[k], c.c2[k], t, d, z);
+            SPFD_LAUNCH_CHECK();
+        }
+    }
+    for (int k = 1; k < h.post; ++k) cheb_sweep<R>(h, l, c, r, z, z, t, d, s);
+}
+
+__global__ void k_pi_init(int64_t n, const double *dinv, double *x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t hsh = (uint32_t)(i * 2654435761ull) >> 8;
+        x[i] = dinv[i] != 0.0 ? 0.5 + (double)(hsh & 0xffff) / 65536.0 : 0.0;
+    }
+}
+
+// y = scale * dinv * y (dinv may be null) ; x = y when x != null
+__global__ void k_pi_scale(int64_t n, const double *dinv, double scale, double *y, double *x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = scale * (dinv ? dinv[i] * y[i] : y[i]);
+        y[i] = v;
+        if (x) x[i] = v;
+    }
+}
+
 }  // namespace
 
 void amg_vcycle(Amg &h, const double *r, double *z, int nrhs, cudaStream_t s) {
     h.vc_partials = 0;
+    if (h.smoother == SPFD_SMOOTHER_CHEBYSHEV && h.lv.size() > 1) {
+        if (nrhs == 1) vcycle_cheb<1>(h, 0, r, z, s);
+        else vcycle_cheb<2>(h, 0, r, z, s);
+        return;
+    }
     if (nrhs == 1) vcycle_level<1>(h, 0, r, z, s);
     else vcycle_level<2>(h, 0, r, z, s);
+}
+
+// Power iteration on D^-1 A_l from a fixed pseudo-random start (20 steps,
+// ||D^-1 A x|| with ||x|| = 1 -> lambda_max from below; the Chebyshev
+// interval's 1.1 factor covers the gap).
+void amg_estimate_lmax(Amg &h, cudaStream_t s) {
+    const int nl = (int)h.lv.size();
+    h.cheb_lmax.assign(nl, 0.0);
+    double *sc = h.scal.get();
+    auto norm = [&](int64_t n, const double *v) {
+        k_dot<1><<<kDotGrid, kDotThreads, 0, s>>>(n, v, v, h.partials.get());
+        SPFD_LAUNCH_CHECK();
+        k_finalize<1><<<1, 256, 0, s>>>(h.partials.get(), kDotGrid, sc, S_TMP, F_STORE, 0.0);
+        SPFD_LAUNCH_CHECK();
+        double v2 = 0.0;
+        SPFD_CUDA(cudaMemcpyAsync(&v2, sc + S_TMP, sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPFD_CUDA(cudaStreamSynchronize(s));
+        return std::sqrt(v2);
+    };
+    for (int l = 0; l < nl - 1; ++l) {
+        Level &L = h.lv[l];
+        const int64_t n = L.nvec;
+        const int g = grid_for(n, 256, 148 * 16);
+        double *x = L.vx.get(), *y = L.vd.get();
+        k_pi_init<<<g, 256, 0, s>>>(n, L.dinv.get(), x);
+        SPFD_LAUNCH_CHECK();
+        double nx = norm(n, x), lam = 0.0;
+        SPFD_CHECK(nx > 0.0, SPFD_EINVAL, "empty level in the eigenvalue estimate");
+        k_pi_scale<<<g, 256, 0, s>>>(n, nullptr, 1.0 / nx, x, nullptr);
+        for (int it = 0; it < 20; ++it) {
+            if (l == 0) level0_apply<1>(h, 0, false, x, nullptr, y, s);
+            else launch_csr<1, 0, false>(L.A, L.a_group, x, nullptr, nullptr, nullptr, y, nullptr, s);
+            k_pi_scale<<<g, 256, 0, s>>>(n, L.dinv.get(), 1.0, y, nullptr);
+            SPFD_LAUNCH_CHECK();
+            lam = norm(n, y);
+            SPFD_CHECK(std::isfinite(lam) && lam > 0.0, SPFD_ENONFINITE, "eigenvalue estimate failed");
+            k_pi_scale<<<g, 256, 0, s>>>(n, nullptr, 1.0 / lam, y, x);
+            SPFD_LAUNCH_CHECK();
+        }
+        h.cheb_lmax[l] = lam;
+    }
 }
 
 // ------------------------------------------------------------------------

@@ -204,7 +204,7 @@ def sample_on_lattice(source, lattice: Lattice, frequency_hz: float) -> FieldSam
 
 def _cfg_key(cfg: SolveConfig):
     return (cfg.max_iters, cfg.restart, cfg.pre_sweeps, cfg.post_sweeps, cfg.jacobi_damping, cfg.strength_threshold,
-            cfg.coarse_cap, cfg.max_levels, cfg.method)
+            cfg.coarse_cap, cfg.max_levels, cfg.method, cfg.smoother, cfg.chebyshev_degree)
 
 
 class FieldOps:

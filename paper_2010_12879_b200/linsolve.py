@@ -32,8 +32,11 @@ from .errors import SolverError
 @dataclass
 class SolveConfig:
     """Solver parameters (linsolve.py:26-53) plus the B200 extensions
-    `method` ("pcg" | "fgmres") and `max_nrhs` (1 or 2 batched right-hand
-    sides, e.g. real/imaginary parts)."""
+    `method` ("pcg" | "fgmres"), `max_nrhs` (1 or 2 batched right-hand
+    sides, e.g. real/imaginary parts) and `smoother` ("jacobi", the
+    reference's damped Jacobi, or "chebyshev": a degree-`chebyshev_degree`
+    polynomial in D^-1 A on [beta/5, beta], beta = 1.1 x a power-iteration
+    estimate of lambda_max per level; `pre_sweeps`/`post_sweeps` repeat it)."""
 
     rel_tol: float = 1e-12
     max_iters: int = 1000
@@ -48,6 +51,8 @@ class SolveConfig:
     trace: object = field(default=None, repr=False, compare=False)
     method: str = "pcg"
     max_nrhs: int = 2
+    smoother: str = "jacobi"
+    chebyshev_degree: int = 2
 
     def __post_init__(self):
         if not self.rel_tol > 0.0:
@@ -64,6 +69,10 @@ class SolveConfig:
             raise ValueError("method must be 'pcg' or 'fgmres'")
         if self.max_nrhs not in (1, 2):
             raise ValueError("max_nrhs must be 1 or 2")
+        if self.smoother not in ("jacobi", "chebyshev"):
+            raise ValueError("smoother must be 'jacobi' or 'chebyshev'")
+        if not 1 <= self.chebyshev_degree <= 16:
+            raise ValueError("chebyshev_degree must be in [1, 16]")
 
 
 @dataclass
@@ -158,6 +167,11 @@ class AmgHierarchy:
         self.damping = cfg.jacobi_damping
         self.structured = bool(info.structured)
         self.device_bytes = int(info.device_bytes)
+        self.smoother = "chebyshev" if info.smoother == _lib.SMOOTHER_CHEBYSHEV else "jacobi"
+        self.chebyshev_degree = int(info.cheb_degree)
+        # lambda_max(D^-1 A_l) estimates behind the Chebyshev intervals (levels < coarsest)
+        self.chebyshev_lmax = ([float(info.cheb_lmax[i]) for i in range(info.n_levels - 1)]
+                               if self.smoother == "chebyshev" else [])
         self.max_nrhs = cfg.max_nrhs
         self.coarse_lu = None  # the coarsest level is applied as a dense device inverse
         self.levels = [AmgLevel(self, i) for i in range(info.n_levels)]
