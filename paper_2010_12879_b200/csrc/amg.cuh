@@ -56,6 +56,8 @@ struct Amg {
     DevBuf<double> cinv;      // dense inverse of the coarsest matrix (nc x nc)
     double omega = 2.0 / 3.0;
     int pre = 1, post = 1;
+    int64_t box[3] = {0, 0, 0};  // > 0: level 0 is the cell Laplacian div div^T of this voxel box
+    double box_od = 0.0;         // omega / 6, its (constant) omega D^-1
     int smoother = 0;         // SPFD_SMOOTHER_JACOBI | SPFD_SMOOTHER_CHEBYSHEV
     int cheb_deg = 2;         // Chebyshev polynomial degree per sweep
     std::vector<double> cheb_lmax;  // lambda_max(D^-1 A_l) estimates (Chebyshev)
@@ -120,6 +122,10 @@ double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cu
 double amg_iteration_bytes(const Amg &h, int nrhs);
 // Chebyshev smoother: power-iteration estimates of lambda_max(D^-1 A_l)
 void amg_estimate_lmax(Amg &h, cudaStream_t s);
+// Level 0 of a CSR hierarchy built on the cell Laplacian div div^T of an
+// nx x ny x nz voxel box (diagonal 6, -1 per shared face): apply it as a
+// matrix-free constant-coefficient stencil instead of reading the CSR.
+void amg_set_box_level0(Amg &h, const int64_t dims[3], cudaStream_t s);
 spfd_report krylov_solve(Amg &h, const double *b_inter, double *x_inter, int nrhs, const spfd_config &cfg,
                          double *h_trace, cudaStream_t s);
 

@@ -581,6 +581,10 @@ static void ensure_clean_amg(Field &F, cudaStream_t s) {
     c.max_nrhs = 2;   // re/im sample sets batched (field_clean)
     F.clean_amg = amg_setup_csr(nc, nnz, ptr.get(), col.get(), val.get(), c, s);
     F.clean_setup_seconds = F.clean_amg->setup_seconds;
+    // level 0 is the constant-coefficient cell Laplacian: matrix-free
+    // (SPFD_CLEAN_BOX=0 keeps the CSR path for A/B)
+    const bool box = !(getenv("SPFD_CLEAN_BOX") && std::string(getenv("SPFD_CLEAN_BOX")) == "0");
+    if (box) amg_set_box_level0(*F.clean_amg, F.g.n, s);
     pool_trim();
 }
 

@@ -733,6 +733,63 @@ __global__ void k_span_scatter(const int32_t *pos_to_dof, int64_t L, const doubl
     }
 }
 
+// ---- matrix-free cell Laplacian (divergence cleaning, level 0) ----------
+// div div^T on an nx x ny x nz box of cells: 6 on the diagonal, -1 per face
+// shared with a neighbour cell (field.cu k_normal_fill), applied in the CSR's
+// column order (z-, y-, x-, centre, x+, y+, z+).  Same MODEs as k_csr
+// (0: y = A x (+ x.y), 1: y = r - A x (+ y.y), 2: y = r - A(od r),
+// 3: y = x + od (r - A x) (+ r.y)); od is the constant omega / 6.
+template <int R, int MODE, bool DOT>
+__global__ void __launch_bounds__(256) k_box(int nx, int ny, int nz, double od, const double *__restrict__ x,
+                                             const double *__restrict__ r, double *__restrict__ y,
+                                             double *__restrict__ partials) {
+    using W = V<R>;
+    using T = typename W::T;
+    __shared__ double red[32 * R];
+    const int nxy = nx * ny, nc = nxy * nz;
+    double dot[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) dot[c] = 0.0;
+    const double *in = MODE == 2 ? r : x;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+        const int i = c % nx, t = c / nx, j = t % ny, k = t / ny;
+        auto ld = [&](int q) { return MODE == 2 ? W::scale(od, W::ld(in, q)) : W::ld(in, q); };
+        T v[7];
+        v[0] = k > 0 ? ld(c - nxy) : W::zero();
+        v[1] = j > 0 ? ld(c - nx) : W::zero();
+        v[2] = i > 0 ? ld(c - 1) : W::zero();
+        v[3] = ld(c);
+        v[4] = i < nx - 1 ? ld(c + 1) : W::zero();
+        v[5] = j < ny - 1 ? ld(c + nx) : W::zero();
+        v[6] = k < nz - 1 ? ld(c + nxy) : W::zero();
+        T s = W::zero();
+#pragma unroll
+        for (int q = 0; q < 3; ++q) s = W::sub(s, v[q]);
+        s = W::axpy(6.0, v[3], s);
+#pragma unroll
+        for (int q = 4; q < 7; ++q) s = W::sub(s, v[q]);
+        T out;
+        if (MODE == 0) out = s;
+        else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(r, c), s);
+        else out = W::add(W::ld(x, c), W::scale(od, W::sub(W::ld(r, c), s)));
+        W::st(y, c, out);
+        if (DOT) {
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) {
+                if (MODE == 0) dot[cc] += W::dot(W::ld(x, c), out, cc);
+                else if (MODE == 3) dot[cc] += W::dot(W::ld(r, c), out, cc);
+                else dot[cc] += W::dot(out, out, cc);
+            }
+        }
+    }
+    if (DOT) {
+        block_sum<R>(dot, red);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int cc = 0; cc < R; ++cc) partials[blockIdx.x * R + cc] = dot[cc];
+    }
+}
+
 // ---- elementwise / BLAS-1 ----------------------------------------------
 template <int R>
 __global__ void k_odinv_r(int64_t n, const double *od, const double *r, double *x) {
@@ -1099,6 +1156,22 @@ int level0_apply(Amg &h, int mode, bool dot, const double *x, const double *r, d
         else g = dot ? launch_fine<R, 3, true>(op, sa, s) : launch_fine<R, 3, false>(op, sa, s);
         return g;
     }
+    if (h.box[0] > 0) {  // matrix-free cell Laplacian
+        const int nx = (int)h.box[0], ny = (int)h.box[1], nz = (int)h.box[2];
+        const int g = grid_for(L.n, 256, 148 * 8);
+        const double od = h.box_od;
+        switch (mode) {
+            case 0: if (dot) k_box<R, 0, true><<<g, 256, 0, s>>>(nx, ny, nz, od, x, r, y, part);
+                    else k_box<R, 0, false><<<g, 256, 0, s>>>(nx, ny, nz, od, x, r, y, part); break;
+            case 1: if (dot) k_box<R, 1, true><<<g, 256, 0, s>>>(nx, ny, nz, od, x, r, y, part);
+                    else k_box<R, 1, false><<<g, 256, 0, s>>>(nx, ny, nz, od, x, r, y, part); break;
+            case 2: k_box<R, 2, false><<<g, 256, 0, s>>>(nx, ny, nz, od, x, r, y, part); break;
+            default: if (dot) k_box<R, 3, true><<<g, 256, 0, s>>>(nx, ny, nz, od, x, r, y, part);
+                     else k_box<R, 3, false><<<g, 256, 0, s>>>(nx, ny, nz, od, x, r, y, part); break;
+        }
+        SPFD_LAUNCH_CHECK();
+        return g;
+    }
     const double *od = L.odinv.get();
     switch (mode) {
         case 0: return dot ? launch_csr<R, 0, true>(L.A, L.a_group, x, r, od, nullptr, y, part, s)
@@ -1448,6 +1521,21 @@ void amg_vcycle(Amg &h, const double *r, double *z, int nrhs, cudaStream_t s) {
     }
     if (nrhs == 1) vcycle_level<1>(h, 0, r, z, s);
     else vcycle_level<2>(h, 0, r, z, s);
+}
+
+void amg_set_box_level0(Amg &h, const int64_t dims[3], cudaStream_t s) {
+    SPFD_CHECK(!h.structured && !h.lv.empty(), SPFD_EINVAL, "box level 0 needs a CSR hierarchy");
+    const int64_t nc = dims[0] * dims[1] * dims[2];
+    SPFD_CHECK(nc == h.lv[0].n && nc < (int64_t)1 << 31 && dims[0] > 0 && dims[1] > 0 && dims[2] > 0, SPFD_EINVAL,
+               "box dims do not match level 0");
+    // every cell has diagonal 6 (div div^T): omega D^-1 is one number
+    double od = 0.0;
+    SPFD_CUDA(cudaMemcpyAsync(&od, h.lv[0].odinv.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    SPFD_CHECK(od == h.omega * (1.0 / 6.0), SPFD_EINVAL, "level 0 is not the cell Laplacian");
+    h.box_od = od;
+    for (int a = 0; a < 3; ++a) h.box[a] = dims[a];
+    amg_drop_graphs(h);
 }
 
 // Power iteration on D^-1 A_l from a fixed pseudo-random start (20 steps,
