@@ -103,6 +103,65 @@ __device__ __forceinline__ Nbr neighbours(const SpanView &v, int p, int r, int4 
     return n;
 }
 
+// Conductances recomputed from the voxel tissue ids (fine kernel kind 6):
+// the 6 edges at a node touch only the 8 voxels around it, so one gather of
+// 8 ids (2 bytes each, x-consecutive across a warp; the id box is kept in
+// L2 with an evict-last policy) and a shared-memory LUT replace the 24-48
+// bytes of stored wx/wy/wz per position.  Same products, same order as
+// edge_w (op.cu, fit_operators.py:289-324): bit-identical weights.
+constexpr int kMaxLut = 1024;
+
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ int ld_id(const uint16_t *p, uint64_t pol) {
+    unsigned short v;
+    asm volatile("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return (int)v;
+}
+__device__ __forceinline__ double w4(double a0, double a1, double a2, double a3, double g) {
+    return mul_rn(mul_rn(add_rn(add_rn(add_rn(a0, a1), a2), a3), 0.25), g);
+}
+
+__device__ __forceinline__ Nbr neighbours_vox(const SpanView &v, const double *lut, uint64_t pol, int p, int r,
+                                              int4 q) {
+    Nbr n;
+    const int i = q.y + (p - q.x), j = q.w;
+    int k = (int)((float)r * v.inv_NY);  // plane of row r = j + NY k
+    if (k * v.NY > r) --k;
+    else if ((k + 1) * v.NY <= r) ++k;
+    n.pxm = (i > q.y) ? p - 1 : -1;
+    n.pxp = (i + 1 < q.z) ? p + 1 : -1;
+    n.pym = (j > 0) ? spos(v.rows, r - 1, i) : -1;
+    n.pyp = (j + 1 < v.NY) ? spos(v.rows, r + 1, i) : -1;
+    n.pzm = (r >= v.NY) ? spos(v.rows, r - v.NY, i) : -1;
+    n.pzp = (r + v.NY < v.n_rows) ? spos(v.rows, r + v.NY, i) : -1;
+    // K[di][dj][dk] = kappa of voxel (i - 1 + di, j - 1 + dj, k - 1 + dk), 0 outside the box
+    double K[2][2][2];
+    const int64_t nxy = (int64_t)v.nx * v.ny;
+    const uint16_t *b = v.vid + ((int64_t)(i - 1) + (int64_t)v.nx * ((j - 1) + (int64_t)v.ny * (k - 1)));
+#pragma unroll
+    for (int dk = 0; dk < 2; ++dk)
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+            for (int di = 0; di < 2; ++di) {
+                const bool ok = (unsigned)(i - 1 + di) < (unsigned)v.nx && (unsigned)(j - 1 + dj) < (unsigned)v.ny &&
+                                (unsigned)(k - 1 + dk) < (unsigned)v.nz;
+                K[di][dj][dk] = ok ? lut[ld_id(b + di + (int64_t)v.nx * dj + nxy * dk, pol)] : 0.0;
+            }
+    n.wxp = w4(K[1][0][0], K[1][0][1], K[1][1][0], K[1][1][1], v.gx);
+    n.wyp = w4(K[0][1][0], K[0][1][1], K[1][1][0], K[1][1][1], v.gy);
+    n.wzp = w4(K[0][0][1], K[0][1][1], K[1][0][1], K[1][1][1], v.gz);
+    n.wxm = n.pxm >= 0 ? w4(K[0][0][0], K[0][0][1], K[0][1][0], K[0][1][1], v.gx) : 0.0;
+    n.wym = n.pym >= 0 ? w4(K[0][0][0], K[0][0][1], K[1][0][0], K[1][0][1], v.gy) : 0.0;
+    n.wzm = n.pzm >= 0 ? w4(K[0][0][0], K[0][1][0], K[1][0][0], K[1][1][0], v.gz) : 0.0;
+    n.diag = add_rn(add_rn(add_rn(add_rn(add_rn(n.wxp, n.wyp), n.wzp), n.wxm), n.wym), n.wzm);
+    return n;
+}
+
 // (A x)_p in the reference's sorted-column order; X(pos) -> V<R>::T gives
 // the neighbour inputs, xc is the centre input (loaded once by the caller).
 template <int R, class X>
@@ -211,11 +270,13 @@ __device__ __forceinline__ void l2_prefetch(const void *base, int64_t p0, int64_
 // One thread of the CTA queues the tile's streamed (center-position) arrays
 // into L2, so the per-position dependent load chains below hit L2 instead
 // of waiting on DRAM (PF = true).
-template <int R, int MODE>
+template <int R, int MODE, bool VOX = false>
 __device__ __forceinline__ void tile_prefetch(const SpanView &v, const SpanArgs &a, int64_t p0, int64_t p1) {
-    l2_prefetch(v.wx, p0, p1, 8);
-    l2_prefetch(v.wy, p0, p1, 8);
-    l2_prefetch(v.wz, p0, p1, 8);
+    if (!VOX) {
+        l2_prefetch(v.wx, p0, p1, 8);
+        l2_prefetch(v.wy, p0, p1, 8);
+        l2_prefetch(v.wz, p0, p1, 8);
+    }
     if (MODE == 0 || MODE == 1 || MODE == 3) l2_prefetch(a.x, p0, p1, 8 * R);
     if (MODE != 0) l2_prefetch(a.r, p0, p1, 8 * R);
     if (MODE >= 2) l2_prefetch(a.od, p0, p1, 8);
@@ -224,9 +285,9 @@ __device__ __forceinline__ void tile_prefetch(const SpanView &v, const SpanArgs 
 
 // One tile of a fine-level stencil pass: positions [t * kTile, +kTile) that
 // lie in [pb, pend); accumulates the thread's dot contribution.
-template <int R, int MODE, bool DOT, bool RANGED>
+template <int R, int MODE, bool DOT, bool RANGED, bool VOX = false>
 __device__ __forceinline__ void span_tile(const SpanView &v, const SpanArgs &a, int t, int64_t pend,
-                                          double (&dot)[R]) {
+                                          double (&dot)[R], const double *lut = nullptr, uint64_t pol = 0) {
     using W = V<R>;
     using T = typename W::T;
     const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
@@ -237,7 +298,7 @@ __device__ __forceinline__ void span_tile(const SpanView &v, const SpanArgs &a, 
         if (RANGED && p < a.pb) continue;
         row = frow(v.rows, row, r1, p);
         const int4 q = v.rows[row];
-        const Nbr n = neighbours(v, p, row, q);
+        const Nbr n = VOX ? neighbours_vox(v, lut, pol, p, row, q) : neighbours(v, p, row, q);
         const bool dof = mbit(v.mask, p);
         T dotv = W::zero();
         T out = point_out<R, MODE>(a, n, p, dotv);
@@ -253,9 +314,16 @@ __device__ __forceinline__ void span_tile(const SpanView &v, const SpanArgs &a, 
     }
 }
 
-template <int R, int MODE, bool DOT, bool RANGED = false, bool PF = false, int MINB = 6>
+template <int R, int MODE, bool DOT, bool RANGED = false, bool PF = false, int MINB = 6, bool VOX = false>
 __global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArgs a) {
     __shared__ double red[32 * R];
+    __shared__ double lut_s[VOX ? kMaxLut : 1];
+    uint64_t pol = 0;
+    if (VOX) {
+        for (int k = threadIdx.x; k < v.lut_len; k += blockDim.x) lut_s[k] = v.vlut[k];
+        pol = l2_keep_policy();
+        __syncthreads();
+    }
     // blk: the tile's index within the launch (CTAs run in blockIdx order;
     // rev walks the tiles from the high end).  Dot partials are stored by
     // blk, so the reduction order does not depend on the direction.
@@ -265,18 +333,18 @@ __global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArg
     if (PF && threadIdx.x == 0) {
         if (a.pf_ahead <= 0 || blockIdx.x < a.pf_ahead) {  // first wave: its own tile
             const int64_t q0 = (int64_t)t * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
-            tile_prefetch<R, MODE>(v, a, q0, q1);
+            tile_prefetch<R, MODE, VOX>(v, a, q0, q1);
         }
         if (a.pf_ahead > 0) {  // later CTAs find their tile queued by an earlier one
             const int ta = a.rev ? t - a.pf_ahead : t + a.pf_ahead;
             const int64_t q0 = (int64_t)ta * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
-            if (ta >= 0) tile_prefetch<R, MODE>(v, a, q0, q1);
+            if (ta >= 0) tile_prefetch<R, MODE, VOX>(v, a, q0, q1);
         }
     }
     double dot[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) dot[c] = 0.0;
-    span_tile<R, MODE, DOT, RANGED>(v, a, t, pend, dot);
+    span_tile<R, MODE, DOT, RANGED, VOX>(v, a, t, pend, dot, lut_s, pol);
     if (DOT) {
         block_sum<R>(dot, red);
         if (threadIdx.x == 0)
@@ -356,6 +424,8 @@ __global__ void __launch_bounds__(kSpanThreads, 6) k_span_fused(SpanView v, Span
         }
     }
 }
+
+#include "span_tma.cuh"
 
 // Restriction r_c = T^T u: sequential sum over each aggregate's member
 // positions (ascending) -- deterministic, no atomics.  Optionally also
@@ -998,7 +1068,7 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
     int64_t n = nvec0 * R;
     h.kx.alloc(n); h.kr.alloc(n); h.kz.alloc(n); h.kp.alloc(n); h.kq.alloc(n); h.kb.alloc(n);
     int64_t np = kDotGrid;
-    if (h.structured) np = std::max<int64_t>(np, h.op->n_tiles);
+    if (h.structured) np = std::max<int64_t>(np, std::max<int64_t>(h.op->n_tiles, h.op->n_stages));
     np = std::max<int64_t>(np, 148 * 16);
     np = std::max<int64_t>(np, (int64_t)kDotGrid * 8);  // batched FGMRES block dots (k_mdot, 8 vectors)
     h.partials.alloc(np * 2 + 64);
@@ -1054,6 +1124,8 @@ int fine_kernel_kind() {
         if (e && std::string(e) == "flat") v = 2;
         if (e && std::string(e) == "pf") v = 3;
         if (e && std::string(e) == "fused") v = 4;
+        if (e && std::string(e) == "stg") v = 5;
+        if (e && std::string(e) == "vox") v = 6;
     }
     return v;
 }
@@ -1111,10 +1183,43 @@ bool alt_dirs() {
     return v == 1;
 }
 
+// kind 5: the staged persistent kernel (span_tma.cuh), whole range only.
+// Needs 16-byte aligned bases (bulk copies); returns false otherwise.
+inline bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <int R, int MODE, bool DOT>
+bool launch_stg(const Operator &op, const SpanArgs &a, cudaStream_t s, int &parts) {
+    constexpr int S = stg::Layout<R, MODE>::NST;
+    constexpr int smem = S * stg::Layout<R, MODE>::STAGE;
+    if (!(al16(a.x) && al16(a.r) && al16(a.od) && al16(a.aggp) && al16(a.base) && al16(op.wx.get()) &&
+          al16(op.wy.get()) && al16(op.wz.get()) && al16(op.dofmask.get()) && al16(op.rows.get())))
+        return false;
+    static int n_sm = 0;
+    if (n_sm == 0) {
+        auto k = k_span_stg<R, MODE, DOT, S>;
+        SPFD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int dev = 0;
+        SPFD_CUDA(cudaGetDevice(&dev));
+        SPFD_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int n = (int)op.n_stages;
+    parts = 0;
+    if (n == 0) return true;
+    const int grid = std::min(n, n_sm);
+    k_span_stg<R, MODE, DOT, S><<<grid, stg::kThreads, smem, s>>>(span_view(op), a, op.stage_desc.get(), n);
+    SPFD_LAUNCH_CHECK();
+    parts = grid;
+    return true;
+}
+
 template <int R, int MODE, bool DOT>
 int launch_fine(const Operator &op, const SpanArgs &a_in, cudaStream_t s) {
     SpanView v = span_view(op);
     SpanArgs a = a_in;
+    if (fine_kernel_kind() == 5 && a.pb <= 0 && a.pe >= op.L) {
+        int parts = 0;
+        if (launch_stg<R, MODE, DOT>(op, a, s, parts)) return parts;
+    }
     a.pf_ahead = pf_ahead();
     if (a.pb > 0 || a.pe < op.L) {  // owned z-slab range
         const int64_t pe = a.pe < op.L ? a.pe : op.L;
@@ -1123,15 +1228,20 @@ int launch_fine(const Operator &op, const SpanArgs &a_in, cudaStream_t s) {
         b.tile0 = t0;
         int g = t1 - t0;
         if (g > 0) {
-            if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, true, true><<<g, kSpanThreads, 0, s>>>(v, b);
+            if (fine_kernel_kind() == 6 && v.vid && v.lut_len <= kMaxLut)
+                k_span<R, MODE, DOT, true, true, 5, true><<<g, kSpanThreads, 0, s>>>(v, b);
+            else if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, true, true><<<g, kSpanThreads, 0, s>>>(v, b);
             else k_span<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, b);
         }
         SPFD_LAUNCH_CHECK();
         return g;
     }
     int g = (int)op.n_tiles;
+    const int kind = fine_kernel_kind();
     if (g > 0) {
-        if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, false, true><<<g, kSpanThreads, 0, s>>>(v, a);
+        if (kind == 6 && v.vid && v.lut_len <= kMaxLut)
+            k_span<R, MODE, DOT, false, true, 5, true><<<g, kSpanThreads, 0, s>>>(v, a);
+        else if (kind == 3 || kind >= 5) k_span<R, MODE, DOT, false, true><<<g, kSpanThreads, 0, s>>>(v, a);
         else k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
     }
     SPFD_LAUNCH_CHECK();

@@ -74,8 +74,9 @@ def test_config_struct_layout():
     from paper_2010_12879_b200 import SolveConfig, _lib
     c = _lib.make_config(SolveConfig(method="fgmres", max_nrhs=1))
     assert c.method == _lib.METHOD_FGMRES and c.max_nrhs == 1
-    # the C struct is 8+4*4+8+8+4*4 with natural alignment
-    assert ctypes.sizeof(_lib.Config) == 56
+    # the C struct is 8+4*4+8+8+6*4 with natural alignment
+    assert ctypes.sizeof(_lib.Config) == 64
+    assert _lib.Config.cheb_degree.offset == 60
     assert ctypes.sizeof(_lib.Report) == 40
 
 

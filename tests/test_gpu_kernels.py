@@ -21,8 +21,8 @@ from conftest import golden_cases, golden_model, load_golden
 
 pytestmark = pytest.mark.gpu
 
-FLAT, PF, FUSED = 2, 3, 4
-KINDS = (FUSED, PF, FLAT)
+FLAT, PF, FUSED, STG, VOX = 2, 3, 4, 5, 6
+KINDS = (FUSED, PF, FLAT, STG, VOX)
 
 
 def _set_kernel(kind):
