@@ -433,22 +433,14 @@ def main():
              (6, "level1_presmooth", "k_csr<4,2,1> level-1 pre-smooth residual", 1),
              (7, "level1_prolong_post", "k_csr_pp<4,2> level-1 fused prolongation + post-smooth", 1),
              (8, "pcg_r_update", "k_update_r<2> r -= alpha q (+ r.r)", 1),
-             (9, "pcg_p_update", "k_xpby<2> p = z + beta p", 1),
-             (10, "fine_presmooth_restriction_fused",
-              "k_span_fused<2,2,2> pre-smooth defect d + restriction input u = d - A(od d), one launch", 1),
-             (11, "fine_prolong_postsmooth_fused",
-              "k_span_fused<2,4,3> prolongation x1 + post-smooth z (+ r.z), one launch", 1)]
-    fused = lib.spfd_bench_kernel(h.handle, 10, 1, 2, ctypes.byref(ctypes.c_double()),
-                                  ctypes.byref(ctypes.c_double()), _lib.stream_ptr()) == 0
-    if fused:  # the separate passes are not launched by the solve (kept as standalone rooflines)
-        table = [(w_, k_, d_, 0 if w_ in (1, 2, 4) else n_) for (w_, k_, d_, n_) in table]
+             (9, "pcg_p_update", "k_xpby<2> p = z + beta p", 1)]
     kernels = {}
     iter_ms = ms / it_mean if it_mean else ms
     for which, key, desc, per_it in table:
         m_, b_ = ctypes.c_double(), ctypes.c_double()
         if lib.spfd_bench_kernel(h.handle, which, args.kernel_reps, 2, ctypes.byref(m_), ctypes.byref(b_),
                                  _lib.stream_ptr()) != 0:
-            continue  # kernel not used for this hierarchy (too few levels, fusion off)
+            continue  # kernel not used for this hierarchy (too few levels)
         gbs = b_.value / (m_.value * 1e-3) / 1e9
         kernels[key] = {"kernel": desc, "ms": round(m_.value, 4), "bytes": b_.value, "gbs": round(gbs, 1),
                         "frac": round(gbs / peak, 4), "launches_per_iteration": per_it,

@@ -384,14 +384,10 @@ int spfd_bench_kernel(spfd_amg_t amg, int which, int reps, int nrhs, double *h_m
 int spfd_iteration_bytes(spfd_amg_t amg, int nrhs, double *h_bytes);
 /* Tuning knob (not part of the reference API): select the fine-level
  * stencil kernel used by every later solve / V-cycle in this process.
- * kind = -1 default (environment SPFD_SPAN_KERNEL=flat|pf|fused, else
- * pf), 2 flat per-position kernel, 3 the same with the tile's streamed
- * arrays bulk-prefetched into L2, 4 = 3 plus the V-cycle's dependent pass
- * pairs (pre-smooth -> restriction input, prolongation -> post-smooth)
- * fused into one persistent launch each, 5 the staged persistent kernel
- * (each tile's stencil windows bulk-copied into shared memory, double
- * buffered).  All give bit-identical stencil outputs; this exists for A/B
- * tests. */
+ * kind = -1 default (environment SPFD_SPAN_KERNEL=flat|pf, else pf), 2 flat
+ * per-position kernel, 3 the same with the tile's streamed arrays
+ * bulk-prefetched into L2.  Both give bit-identical stencil outputs; this
+ * exists for A/B tests. */
 int spfd_set_fine_kernel(int kind);
 /* Tuning knob: run PCG as one CUDA graph with a device-side WHILE node
  * (mode 1, the default) or as the host-driven loop (mode 0); -1 restores the

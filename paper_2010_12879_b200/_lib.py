@@ -15,7 +15,7 @@ import torch
 from .errors import EmptySystemError, LatticeError, ProjectionError, SingularPointError, SolverError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspfd_b200.so")
+LIB_PATH = os.environ.get("SPFD_LIB") or os.path.join(_HERE, "libspfd_b200.so")  # SPFD_LIB: A/B builds
 
 SPFD_OK = 0
 SPFD_EINVAL = 1

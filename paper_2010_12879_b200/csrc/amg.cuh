@@ -81,8 +81,6 @@ struct Amg {
     cudaGraphExec_t pcg_exec[3] = {nullptr, nullptr, nullptr};
     int64_t pcg_body_launches[3] = {0, 0, 0};
     int pcg_kind[3] = {-1, -1, -1};         // fine-kernel kind captured in each graph
-    DevBuf<int> fuse_sync;    // fused fine passes: item counter + per-tile done flags
-    int fuse_dep = 0;         // z-neighbour reach of a tile, in tiles (structured level 0)
     DevBuf<double> pcg_trace;               // [cap_iters * 2] per-iteration residual estimates
     int64_t pcg_trace_cap = 0;
     // FGMRES restart cycle as one graph per rhs count (fgmres_graph.cuh)

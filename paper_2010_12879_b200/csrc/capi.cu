@@ -347,7 +347,7 @@ int spfd_iteration_bytes(spfd_amg_t h, int nrhs, double *h_bytes) {
 
 int spfd_set_fine_kernel(int kind) {
     return guarded([&] {
-        SPFD_CHECK(kind == -1 || (kind >= 2 && kind <= 6), SPFD_EINVAL, "fine kernel kind must be -1 or 2..6");
+        SPFD_CHECK(kind == -1 || kind == 2 || kind == 3, SPFD_EINVAL, "fine kernel kind must be -1, 2 or 3");
         g_fine_kind_override = kind;
     });
 }

@@ -9,8 +9,6 @@
 //   fit_operators.py:421-441 (COO->CSR assembly, bincount RHS),
 //   scipy csr_matvec (sorted-column accumulation),
 //   dosimetry.py:27-116 (edge voltages, node |E|, corner mean).
-#include <climits>
-
 #include <cub/cub.cuh>
 
 #include "op.cuh"
@@ -205,71 +203,6 @@ __global__ void k_tile_rows(const int4 *rows, int64_t n_rows, int64_t n_tiles, i
             if (rows[mid].x <= p) lo = mid; else hi = mid - 1;
         }
         tile_row[t] = lo;
-    }
-}
-
-// Staged-tile descriptors (span_tma.cuh): for each kStage tile of positions
-// [P0, P1) the exact position ranges its stencil reads outside the x-row
-// neighbours -- the in-plane window (y+-1 and x+-1 neighbours together with
-// the tile itself), the plane below (z-1) and the plane above (z+1) -- and
-// the rows of its first and last position.  One CTA per tile, min/max over
-// the tile's positions.
-__global__ void __launch_bounds__(256) k_stage_desc(const int4 *rows, int64_t n_rows, int NY, int64_t L,
-                                                    int64_t n_stages, int4 *desc) {
-    __shared__ int red[8][8];
-    const int64_t t = blockIdx.x;
-    const int64_t P0 = t * kStage, P1 = P0 + kStage < L ? P0 + kStage : L;
-    int lo_c = INT_MAX, hi_c = INT_MIN, lo_m = INT_MAX, hi_m = INT_MIN, lo_p = INT_MAX, hi_p = INT_MIN;
-    int rfirst = INT_MAX, rlast = INT_MIN;
-    for (int64_t p = P0 + threadIdx.x; p < P1; p += blockDim.x) {
-        int a = 0, b = (int)n_rows - 1;  // row of p
-        while (a < b) {
-            int mid = (a + b + 1) >> 1;
-            if (rows[mid].x <= p) a = mid; else b = mid - 1;
-        }
-        const int r = a;
-        const int4 q = rows[r];
-        const int i = q.y + (int)(p - q.x), j = q.w;
-        rfirst = min(rfirst, r); rlast = max(rlast, r);
-        int c0 = (int)p, c1 = (int)p;
-        if (i > q.y) c0 = (int)p - 1;
-        if (i + 1 < q.z) c1 = (int)p + 1;
-        if (j > 0) { int4 u = rows[r - 1]; if (i >= u.y && i < u.z) c0 = min(c0, u.x + (i - u.y)); }
-        if (j + 1 < NY) { int4 u = rows[r + 1]; if (i >= u.y && i < u.z) c1 = max(c1, u.x + (i - u.y)); }
-        lo_c = min(lo_c, c0); hi_c = max(hi_c, c1);
-        if (r >= NY) {
-            int4 u = rows[r - NY];
-            if (i >= u.y && i < u.z) { int pp = u.x + (i - u.y); lo_m = min(lo_m, pp); hi_m = max(hi_m, pp); }
-        }
-        if (r + NY < n_rows) {
-            int4 u = rows[r + NY];
-            if (i >= u.y && i < u.z) { int pp = u.x + (i - u.y); lo_p = min(lo_p, pp); hi_p = max(hi_p, pp); }
-        }
-    }
-    int v[8] = {-lo_c, hi_c, -lo_m, hi_m, -lo_p, hi_p, -rfirst, rlast};  // all max-reductions
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v[k] = max(v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) red[warp][k] = v[k];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-            for (int k = 0; k < 8; ++k) v[k] = max(v[k], red[w][k]);
-        auto win = [](int nlo, int hi) { return hi < -nlo ? make_int2(0, 0) : make_int2(-nlo, hi + 1); };
-        const int2 c = win(v[0], v[1]), m = win(v[2], v[3]), pz = win(v[4], v[5]);
-        const int r0 = -v[6], r1 = v[7];
-        // staged only if every window fits its slot and ends 4 positions
-        // before the arrays do (16-byte rounding stays inside the padding)
-        const int64_t safe = L - 4;
-        bool staged = c.y - c.x <= kStageCW && m.y - m.x <= kStageZW && pz.y - pz.x <= kStageZW &&
-                      c.y <= safe && m.y <= safe && pz.y <= safe && P1 <= safe && r1 - r0 + 3 <= kStageRW &&
-                      r1 + NY + 2 < n_rows;
-        desc[2 * t] = make_int4(c.x, c.y, m.x, m.y);
-        desc[2 * t + 1] = make_int4(pz.x, pz.y, r0, r1 | (staged ? 0 : kStageFlat));
     }
 }
 
@@ -484,12 +417,6 @@ Operator *op_create(const int64_t *dims, const double *spacing, const uint16_t *
                                                                    op->vox_cond.get(), bad.get());
         SPFD_LAUNCH_CHECK();
         SPFD_CHECK(read_scalar(bad.get(), s) == 0, SPFD_EINVAL, "tissue id outside the LUT");
-        // keep the ids and the LUT: the solve kernels recompute conductances from them
-        op->vid.alloc(op->n_vox + 8);
-        SPFD_CUDA(cudaMemcpyAsync(op->vid.get(), ids, op->n_vox * sizeof(uint16_t), cudaMemcpyDeviceToDevice, s));
-        op->lut_len = lut_len;
-        op->vlut.alloc(lut_len);
-        SPFD_CUDA(cudaMemcpyAsync(op->vlut.get(), lut, lut_len * sizeof(double), cudaMemcpyDeviceToDevice, s));
 
         // components (union-find over conductive edges)
         DevBuf<int32_t> parent;
@@ -554,19 +481,13 @@ Operator *op_create(const int64_t *dims, const double *spacing, const uint16_t *
         k_tile_rows<<<grid_for(op->n_tiles + 1, T), T, 0, s>>>(op->rows.get(), op->n_rows, op->n_tiles,
                                                               op->tile_row.get());
         SPFD_LAUNCH_CHECK();
-        op->n_stages = (op->L + kStage - 1) / kStage;
-        op->stage_desc.alloc(2 * op->n_stages + 2);
-        if (op->n_stages > 0)
-            k_stage_desc<<<(int)op->n_stages, 256, 0, s>>>(op->rows.get(), op->n_rows, (int)op->NY, op->L,
-                                                          op->n_stages, op->stage_desc.get());
-        SPFD_LAUNCH_CHECK();
 
         // span arrays
         int64_t L = op->L;
         op->wx.alloc(L + 4); op->wy.alloc(L + 4); op->wz.alloc(L + 4);  // +4: aligned bulk-copy supersets
         op->diag.alloc(L); op->dinv.alloc(L);
         op->pos_to_dof.alloc(L);
-        op->dofmask.alloc((L + 31) / 32 + 4);
+        op->dofmask.alloc((L + 31) / 32 + 1);
         SPFD_CUDA(cudaMemsetAsync(op->dofmask.get(), 0, op->dofmask.bytes(), s));
         DevBuf<int32_t> isdof, dofidx;
         isdof.alloc(L + 1); dofidx.alloc(L + 1);

@@ -14,11 +14,6 @@ namespace spfd {
 
 constexpr int kTile = 1024;          // positions per CTA in span kernels
 constexpr int kSpanThreads = 256;    // threads per CTA in span kernels
-constexpr int kStage = 512;          // positions per staged tile (bulk-copy span kernel, span_tma.cuh)
-constexpr int kStageCW = 1024;       // staged in-plane window (tile + x/y neighbours), positions
-constexpr int kStageZW = 640;        // staged z-1 / z+1 windows, positions
-constexpr int kStageRW = 64;         // staged row records per group
-constexpr int kStageFlat = 1 << 30;  // stage_desc flag (in the last-row field): tile computed unstaged
 
 struct Operator {
     int64_t nx, ny, nz;              // voxels
@@ -33,9 +28,6 @@ struct Operator {
 
     DevBuf<int4> rows;               // [n_rows+1] {off, lo, hi, j|k<<?>}  (sentinel at end)
     DevBuf<int32_t> tile_row;        // [n_tiles+1] first row of each tile
-    DevBuf<int4> stage_desc;         // [2*n_stages] per kStage tile: {in-plane window a,b, z-1 window a,b},
-                                     //   {z+1 window a,b, first row, last row | kStageFlat} (positions)
-    int64_t n_stages = 0;            // ceil(L / kStage)
     DevBuf<double> wx, wy, wz;       // [L] edge conductance of the +axis edge at each position
     DevBuf<double> diag;             // [L] reference-order diagonal (0 for non-DOF)
     DevBuf<double> dinv;             // [L] 1/diag (0 for non-DOF)
@@ -47,14 +39,11 @@ struct Operator {
     DevBuf<int32_t> vrow_off;        // [ny*nz+1] conductive-voxel offsets per voxel row
     DevBuf<int32_t> nnz_row;         // [N+1] CSR row pointer cache (int32 counts, built lazily)
     DevBuf<double> ws_a, ws_b;       // span workspaces [L*2]
-    DevBuf<uint16_t> vid;            // [n_vox] tissue ids (x-fastest): the solve kernels recompute the
-    DevBuf<double> vlut;             //   conductances from them (kind 6); [lut_len] kappa per id
-    int64_t lut_len = 0;
     int64_t device_bytes() const {
-        return rows.bytes() + tile_row.bytes() + stage_desc.bytes() + wx.bytes() + wy.bytes() + wz.bytes() +
+        return rows.bytes() + tile_row.bytes() + wx.bytes() + wy.bytes() + wz.bytes() +
                diag.bytes() + dinv.bytes() + dofmask.bytes() + pos_to_dof.bytes() +
                dof_to_pos.bytes() + pinned.bytes() + vox_cond.bytes() + vrow_off.bytes() +
-               nnz_row.bytes() + ws_a.bytes() + ws_b.bytes() + vid.bytes() + vlut.bytes();
+               nnz_row.bytes() + ws_a.bytes() + ws_b.bytes();
     }
 };
 
@@ -67,19 +56,11 @@ struct SpanView {
     int64_t L;
     int NY;        // rows per k-plane (= ny+1)
     int n_rows;
-    // voxel tissue ids + kappa LUT: conductances recomputed in the stencil
-    const uint16_t *vid;
-    const double *vlut;
-    int lut_len, nx, ny, nz;
-    double gx, gy, gz;
-    float inv_NY;  // 1 / NY (row -> plane k, corrected to the exact quotient)
 };
 
 inline SpanView span_view(const Operator &op) {
     return SpanView{op.rows.get(), op.tile_row.get(), op.wx.get(), op.wy.get(), op.wz.get(),
-                    op.dofmask.get(), op.L, (int)op.NY, (int)op.n_rows,
-                    op.vid.get(), op.vlut.get(), (int)op.lut_len, (int)op.nx, (int)op.ny, (int)op.nz,
-                    op.gx, op.gy, op.gz, 1.0f / (float)op.NY};
+                    op.dofmask.get(), op.L, (int)op.NY, (int)op.n_rows};
 }
 
 // Owned position range [pb, pe) of a span kernel launch (z-slab).

@@ -103,65 +103,6 @@ __device__ __forceinline__ Nbr neighbours(const SpanView &v, int p, int r, int4 
     return n;
 }
 
-// Conductances recomputed from the voxel tissue ids (fine kernel kind 6):
-// the 6 edges at a node touch only the 8 voxels around it, so one gather of
-// 8 ids (2 bytes each, x-consecutive across a warp; the id box is kept in
-// L2 with an evict-last policy) and a shared-memory LUT replace the 24-48
-// bytes of stored wx/wy/wz per position.  Same products, same order as
-// edge_w (op.cu, fit_operators.py:289-324): bit-identical weights.
-constexpr int kMaxLut = 1024;
-
-__device__ __forceinline__ uint64_t l2_keep_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ int ld_id(const uint16_t *p, uint64_t pol) {
-    unsigned short v;
-    asm volatile("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
-    return (int)v;
-}
-__device__ __forceinline__ double w4(double a0, double a1, double a2, double a3, double g) {
-    return mul_rn(mul_rn(add_rn(add_rn(add_rn(a0, a1), a2), a3), 0.25), g);
-}
-
-__device__ __forceinline__ Nbr neighbours_vox(const SpanView &v, const double *lut, uint64_t pol, int p, int r,
-                                              int4 q) {
-    Nbr n;
-    const int i = q.y + (p - q.x), j = q.w;
-    int k = (int)((float)r * v.inv_NY);  // plane of row r = j + NY k
-    if (k * v.NY > r) --k;
-    else if ((k + 1) * v.NY <= r) ++k;
-    n.pxm = (i > q.y) ? p - 1 : -1;
-    n.pxp = (i + 1 < q.z) ? p + 1 : -1;
-    n.pym = (j > 0) ? spos(v.rows, r - 1, i) : -1;
-    n.pyp = (j + 1 < v.NY) ? spos(v.rows, r + 1, i) : -1;
-    n.pzm = (r >= v.NY) ? spos(v.rows, r - v.NY, i) : -1;
-    n.pzp = (r + v.NY < v.n_rows) ? spos(v.rows, r + v.NY, i) : -1;
-    // K[di][dj][dk] = kappa of voxel (i - 1 + di, j - 1 + dj, k - 1 + dk), 0 outside the box
-    double K[2][2][2];
-    const int64_t nxy = (int64_t)v.nx * v.ny;
-    const uint16_t *b = v.vid + ((int64_t)(i - 1) + (int64_t)v.nx * ((j - 1) + (int64_t)v.ny * (k - 1)));
-#pragma unroll
-    for (int dk = 0; dk < 2; ++dk)
-#pragma unroll
-        for (int dj = 0; dj < 2; ++dj)
-#pragma unroll
-            for (int di = 0; di < 2; ++di) {
-                const bool ok = (unsigned)(i - 1 + di) < (unsigned)v.nx && (unsigned)(j - 1 + dj) < (unsigned)v.ny &&
-                                (unsigned)(k - 1 + dk) < (unsigned)v.nz;
-                K[di][dj][dk] = ok ? lut[ld_id(b + di + (int64_t)v.nx * dj + nxy * dk, pol)] : 0.0;
-            }
-    n.wxp = w4(K[1][0][0], K[1][0][1], K[1][1][0], K[1][1][1], v.gx);
-    n.wyp = w4(K[0][1][0], K[0][1][1], K[1][1][0], K[1][1][1], v.gy);
-    n.wzp = w4(K[0][0][1], K[0][1][1], K[1][0][1], K[1][1][1], v.gz);
-    n.wxm = n.pxm >= 0 ? w4(K[0][0][0], K[0][0][1], K[0][1][0], K[0][1][1], v.gx) : 0.0;
-    n.wym = n.pym >= 0 ? w4(K[0][0][0], K[0][0][1], K[1][0][0], K[1][0][1], v.gy) : 0.0;
-    n.wzm = n.pzm >= 0 ? w4(K[0][0][0], K[0][1][0], K[1][0][0], K[1][1][0], v.gz) : 0.0;
-    n.diag = add_rn(add_rn(add_rn(add_rn(add_rn(n.wxp, n.wyp), n.wzp), n.wxm), n.wym), n.wzm);
-    return n;
-}
-
 // (A x)_p in the reference's sorted-column order; X(pos) -> V<R>::T gives
 // the neighbour inputs, xc is the centre input (loaded once by the caller).
 template <int R, class X>
@@ -270,13 +211,11 @@ __device__ __forceinline__ void l2_prefetch(const void *base, int64_t p0, int64_
 // One thread of the CTA queues the tile's streamed (center-position) arrays
 // into L2, so the per-position dependent load chains below hit L2 instead
 // of waiting on DRAM (PF = true).
-template <int R, int MODE, bool VOX = false>
+template <int R, int MODE>
 __device__ __forceinline__ void tile_prefetch(const SpanView &v, const SpanArgs &a, int64_t p0, int64_t p1) {
-    if (!VOX) {
-        l2_prefetch(v.wx, p0, p1, 8);
-        l2_prefetch(v.wy, p0, p1, 8);
-        l2_prefetch(v.wz, p0, p1, 8);
-    }
+    l2_prefetch(v.wx, p0, p1, 8);
+    l2_prefetch(v.wy, p0, p1, 8);
+    l2_prefetch(v.wz, p0, p1, 8);
     if (MODE == 0 || MODE == 1 || MODE == 3) l2_prefetch(a.x, p0, p1, 8 * R);
     if (MODE != 0) l2_prefetch(a.r, p0, p1, 8 * R);
     if (MODE >= 2) l2_prefetch(a.od, p0, p1, 8);
@@ -285,9 +224,9 @@ __device__ __forceinline__ void tile_prefetch(const SpanView &v, const SpanArgs 
 
 // One tile of a fine-level stencil pass: positions [t * kTile, +kTile) that
 // lie in [pb, pend); accumulates the thread's dot contribution.
-template <int R, int MODE, bool DOT, bool RANGED, bool VOX = false>
+template <int R, int MODE, bool DOT, bool RANGED>
 __device__ __forceinline__ void span_tile(const SpanView &v, const SpanArgs &a, int t, int64_t pend,
-                                          double (&dot)[R], const double *lut = nullptr, uint64_t pol = 0) {
+                                          double (&dot)[R]) {
     using W = V<R>;
     using T = typename W::T;
     const int r0 = v.tile_row[t], r1 = v.tile_row[t + 1];
@@ -298,7 +237,7 @@ __device__ __forceinline__ void span_tile(const SpanView &v, const SpanArgs &a, 
         if (RANGED && p < a.pb) continue;
         row = frow(v.rows, row, r1, p);
         const int4 q = v.rows[row];
-        const Nbr n = VOX ? neighbours_vox(v, lut, pol, p, row, q) : neighbours(v, p, row, q);
+        const Nbr n = neighbours(v, p, row, q);
         const bool dof = mbit(v.mask, p);
         T dotv = W::zero();
         T out = point_out<R, MODE>(a, n, p, dotv);
@@ -314,16 +253,12 @@ __device__ __forceinline__ void span_tile(const SpanView &v, const SpanArgs &a, 
     }
 }
 
-template <int R, int MODE, bool DOT, bool RANGED = false, bool PF = false, int MINB = 6, bool VOX = false>
+#ifndef SPFD_SPAN_MINB
+#define SPFD_SPAN_MINB 6
+#endif
+template <int R, int MODE, bool DOT, bool RANGED = false, bool PF = false, int MINB = SPFD_SPAN_MINB>
 __global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArgs a) {
     __shared__ double red[32 * R];
-    __shared__ double lut_s[VOX ? kMaxLut : 1];
-    uint64_t pol = 0;
-    if (VOX) {
-        for (int k = threadIdx.x; k < v.lut_len; k += blockDim.x) lut_s[k] = v.vlut[k];
-        pol = l2_keep_policy();
-        __syncthreads();
-    }
     // blk: the tile's index within the launch (CTAs run in blockIdx order;
     // rev walks the tiles from the high end).  Dot partials are stored by
     // blk, so the reduction order does not depend on the direction.
@@ -333,18 +268,18 @@ __global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArg
     if (PF && threadIdx.x == 0) {
         if (a.pf_ahead <= 0 || blockIdx.x < a.pf_ahead) {  // first wave: its own tile
             const int64_t q0 = (int64_t)t * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
-            tile_prefetch<R, MODE, VOX>(v, a, q0, q1);
+            tile_prefetch<R, MODE>(v, a, q0, q1);
         }
         if (a.pf_ahead > 0) {  // later CTAs find their tile queued by an earlier one
             const int ta = a.rev ? t - a.pf_ahead : t + a.pf_ahead;
             const int64_t q0 = (int64_t)ta * kTile, q1 = q0 + kTile < pend ? q0 + kTile : pend;
-            if (ta >= 0) tile_prefetch<R, MODE, VOX>(v, a, q0, q1);
+            if (ta >= 0) tile_prefetch<R, MODE>(v, a, q0, q1);
         }
     }
     double dot[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) dot[c] = 0.0;
-    span_tile<R, MODE, DOT, RANGED, VOX>(v, a, t, pend, dot, lut_s, pol);
+    span_tile<R, MODE, DOT, RANGED>(v, a, t, pend, dot);
     if (DOT) {
         block_sum<R>(dot, red);
         if (threadIdx.x == 0)
@@ -352,80 +287,6 @@ __global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArg
             for (int c = 0; c < R; ++c) a.partials[blk * R + c] = dot[c];
     }
 }
-
-// Two dependent fine-level passes in one persistent launch, the second
-// reading the first's output while it is still in L2:
-//   stage 1: y1 = M1(...)      (a1; e.g. the pre-smoothing defect d)
-//   stage 2: y2 = M2(y1, ...)  (a2; e.g. the restriction input from d)
-// Work items are claimed in a fixed order from a counter: stage-1 tiles
-// run `lag` tiles ahead of stage-2 tiles.  Stage-2 tile t reads stage-1
-// output of tiles [t - dep, t + dep] (one node plane each way, the z
-// neighbours) and waits on their done flags; those tiles were claimed
-// earlier by running CTAs and stage-1 items never wait, so the launch
-// cannot deadlock whatever the residency.  Each tile is computed by the
-// same per-position code as k_span, dot partials stored per tile: the
-// results are bit-identical to the two separate passes.  The second pass's
-// reads of y1, the weights and omega D^-1 hit L2 instead of HBM
-// (C3: 48 of 128 B per position for pre-smooth + restriction input).
-struct FuseCtl {
-    int *sync;  // [0] item counter, [1 + t] stage-1 done flag of tile t (zeroed before each launch)
-    int tiles;  // tiles of the pass
-    int lag;    // stage-1 tile t + lag is claimed before stage-2 tile t
-    int dep;    // stage-2 dependency half-width in tiles (<= lag)
-};
-
-template <int R, int M1, int M2, bool DOT2>
-__global__ void __launch_bounds__(kSpanThreads, 6) k_span_fused(SpanView v, SpanArgs a1, SpanArgs a2, FuseCtl c) {
-    __shared__ double red[32 * R];
-    __shared__ int item_s;
-    const int T = c.tiles, lag = c.lag < T ? c.lag : T;
-    volatile int *flags = c.sync + 1;
-    while (true) {
-        if (threadIdx.x == 0) item_s = atomicAdd(c.sync, 1);
-        __syncthreads();
-        const int k = item_s;
-        __syncthreads();  // item_s is rewritten by the next claim
-        if (k >= 2 * T) break;
-        int stage, t;
-        if (k < lag) { stage = 1; t = k; }
-        else if (k < 2 * T - lag) {
-            const int m = k - lag;
-            stage = (m & 1) ? 2 : 1;
-            t = (m & 1) ? (m >> 1) : lag + (m >> 1);
-        } else { stage = 2; t = k - T; }
-        const int64_t q0 = (int64_t)t * kTile, q1 = q0 + kTile < v.L ? q0 + kTile : v.L;
-        double dot[R];
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc) dot[cc] = 0.0;
-        if (stage == 1) {
-            if (threadIdx.x == 0) tile_prefetch<R, M1>(v, a1, q0, q1);
-            span_tile<R, M1, false, false>(v, a1, t, v.L, dot);
-            __syncthreads();  // every store of the tile issued
-            if (threadIdx.x == 0) {
-                __threadfence();
-                flags[t] = 1;
-            }
-        } else {
-            if (threadIdx.x < 32) {  // one warp polls the dependency window
-                const int lo = t - c.dep > 0 ? t - c.dep : 0, hi = t + c.dep < T - 1 ? t + c.dep : T - 1;
-                for (int qq = lo + (int)threadIdx.x; qq <= hi; qq += 32)
-                    while (flags[qq] == 0) __nanosleep(64);
-                __syncwarp();
-                __threadfence();
-            }
-            __syncthreads();
-            span_tile<R, M2, DOT2, false>(v, a2, t, v.L, dot);
-            if (DOT2) {
-                block_sum<R>(dot, red);
-                if (threadIdx.x == 0)
-#pragma unroll
-                    for (int cc = 0; cc < R; ++cc) a2.partials[t * R + cc] = dot[cc];
-            }
-        }
-    }
-}
-
-#include "span_tma.cuh"
 
 // Restriction r_c = T^T u: sequential sum over each aggregate's member
 // positions (ascending) -- deterministic, no atomics.  Optionally also
@@ -1068,26 +929,11 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
     int64_t n = nvec0 * R;
     h.kx.alloc(n); h.kr.alloc(n); h.kz.alloc(n); h.kp.alloc(n); h.kq.alloc(n); h.kb.alloc(n);
     int64_t np = kDotGrid;
-    if (h.structured) np = std::max<int64_t>(np, std::max<int64_t>(h.op->n_tiles, h.op->n_stages));
+    if (h.structured) np = std::max<int64_t>(np, h.op->n_tiles);
     np = std::max<int64_t>(np, 148 * 16);
     np = std::max<int64_t>(np, (int64_t)kDotGrid * 8);  // batched FGMRES block dots (k_mdot, 8 vectors)
     h.partials.alloc(np * 2 + 64);
     h.scal.alloc(S_END);
-    if (h.structured && h.op->n_tiles > 0) {
-        // reach of the z neighbours in positions: a row to the end of the row
-        // one plane above (the same bound holds downwards)
-        const Operator &op = *h.op;
-        std::vector<int4> rows(op.n_rows);
-        SPFD_CUDA(cudaMemcpy(rows.data(), op.rows.get(), op.n_rows * sizeof(int4), cudaMemcpyDeviceToHost));
-        int64_t reach = 0;
-        for (int64_t r = 0; r + op.NY < op.n_rows; ++r) {
-            const int4 a = rows[r], b = rows[r + op.NY];
-            reach = std::max<int64_t>(reach, (int64_t)b.x + (b.z - b.y) - a.x);
-        }
-        h.fuse_dep = (int)(reach / kTile) + 2;
-        h.fuse_sync.alloc(op.n_tiles + 1);
-        SPFD_CUDA(cudaMemset(h.fuse_sync.get(), 0, (op.n_tiles + 1) * sizeof(int)));
-    }
     SPFD_CUDA(cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking));
     SPFD_CUDA(cudaEventCreateWithFlags(&h.ev_alpha, cudaEventDisableTiming));
     SPFD_CUDA(cudaEventCreateWithFlags(&h.ev_x, cudaEventDisableTiming));
@@ -1108,13 +954,9 @@ namespace {
 
 // fine-level stencil kernel: 3 = flat per-position k_span with the tile's
 // streamed arrays bulk-prefetched into L2 (default), 2 = without the
-// prefetch (A/B); round-1/2 variants measured slower are documented in
-// DESIGN.md
-// 4 = kind 3 plus the two dependent pass pairs of the V-cycle fused into one
-// persistent launch each (k_span_fused; measured slower on C3, opt-in:
-// pre+restriction 279-287 us vs 2 x 134 us, prolongation+post 338-353 us vs
-// 178 + 146 us -- the passes are not HBM-bound, so serving the second
-// pass from L2 does not pay for the persistent scheduling)
+// prefetch (A/B).  The variants measured slower (z-marching, smem/TMA
+// staging, fused pass pairs, lane shuffles, voxel-id conductances) are
+// documented in DESIGN.md and profiles/r02_fine_kernel_experiments.md.
 int fine_kernel_kind() {
     if (g_fine_kind_override >= 0) return g_fine_kind_override;
     static int v = -1;
@@ -1123,37 +965,8 @@ int fine_kernel_kind() {
         v = 3;
         if (e && std::string(e) == "flat") v = 2;
         if (e && std::string(e) == "pf") v = 3;
-        if (e && std::string(e) == "fused") v = 4;
-        if (e && std::string(e) == "stg") v = 5;
-        if (e && std::string(e) == "vox") v = 6;
     }
     return v;
-}
-
-bool fused_fine(const Amg &h) { return h.structured && fine_kernel_kind() == 4 && h.fuse_sync.n > 0; }
-
-// stage-1 lead over stage 2 in tiles: the dependency reach plus about half
-// the resident CTAs, so stage-2 items rarely find their inputs unfinished
-inline int fuse_lag(const Amg &h) {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SPFD_FUSE_LAG");
-        v = e ? atoi(e) : 0;
-    }
-    const int lag = v > 0 ? v : 148 * 3 + 16;
-    return std::max(lag, h.fuse_dep);
-}
-
-template <int R, int M1, int M2, bool DOT2>
-int launch_fused(Amg &h, const SpanArgs &a1, const SpanArgs &a2, cudaStream_t s) {
-    const Operator &op = *h.op;
-    const int T = (int)op.n_tiles;
-    SPFD_CUDA(cudaMemsetAsync(h.fuse_sync.get(), 0, (T + 1) * sizeof(int), s));
-    FuseCtl c{h.fuse_sync.get(), T, std::min(fuse_lag(h), T), h.fuse_dep};
-    const int grid = std::min(2 * T, 148 * 6);
-    k_span_fused<R, M1, M2, DOT2><<<grid, kSpanThreads, 0, s>>>(span_view(op), a1, a2, c);
-    SPFD_LAUNCH_CHECK();
-    return T;
 }
 
 // Launch one fine-level stencil pass over the owned positions [a.pb, a.pe).
@@ -1183,43 +996,10 @@ bool alt_dirs() {
     return v == 1;
 }
 
-// kind 5: the staged persistent kernel (span_tma.cuh), whole range only.
-// Needs 16-byte aligned bases (bulk copies); returns false otherwise.
-inline bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-template <int R, int MODE, bool DOT>
-bool launch_stg(const Operator &op, const SpanArgs &a, cudaStream_t s, int &parts) {
-    constexpr int S = stg::Layout<R, MODE>::NST;
-    constexpr int smem = S * stg::Layout<R, MODE>::STAGE;
-    if (!(al16(a.x) && al16(a.r) && al16(a.od) && al16(a.aggp) && al16(a.base) && al16(op.wx.get()) &&
-          al16(op.wy.get()) && al16(op.wz.get()) && al16(op.dofmask.get()) && al16(op.rows.get())))
-        return false;
-    static int n_sm = 0;
-    if (n_sm == 0) {
-        auto k = k_span_stg<R, MODE, DOT, S>;
-        SPFD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        int dev = 0;
-        SPFD_CUDA(cudaGetDevice(&dev));
-        SPFD_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-    }
-    const int n = (int)op.n_stages;
-    parts = 0;
-    if (n == 0) return true;
-    const int grid = std::min(n, n_sm);
-    k_span_stg<R, MODE, DOT, S><<<grid, stg::kThreads, smem, s>>>(span_view(op), a, op.stage_desc.get(), n);
-    SPFD_LAUNCH_CHECK();
-    parts = grid;
-    return true;
-}
-
 template <int R, int MODE, bool DOT>
 int launch_fine(const Operator &op, const SpanArgs &a_in, cudaStream_t s) {
     SpanView v = span_view(op);
     SpanArgs a = a_in;
-    if (fine_kernel_kind() == 5 && a.pb <= 0 && a.pe >= op.L) {
-        int parts = 0;
-        if (launch_stg<R, MODE, DOT>(op, a, s, parts)) return parts;
-    }
     a.pf_ahead = pf_ahead();
     if (a.pb > 0 || a.pe < op.L) {  // owned z-slab range
         const int64_t pe = a.pe < op.L ? a.pe : op.L;
@@ -1228,20 +1008,15 @@ int launch_fine(const Operator &op, const SpanArgs &a_in, cudaStream_t s) {
         b.tile0 = t0;
         int g = t1 - t0;
         if (g > 0) {
-            if (fine_kernel_kind() == 6 && v.vid && v.lut_len <= kMaxLut)
-                k_span<R, MODE, DOT, true, true, 5, true><<<g, kSpanThreads, 0, s>>>(v, b);
-            else if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, true, true><<<g, kSpanThreads, 0, s>>>(v, b);
+            if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, true, true><<<g, kSpanThreads, 0, s>>>(v, b);
             else k_span<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, b);
         }
         SPFD_LAUNCH_CHECK();
         return g;
     }
     int g = (int)op.n_tiles;
-    const int kind = fine_kernel_kind();
     if (g > 0) {
-        if (kind == 6 && v.vid && v.lut_len <= kMaxLut)
-            k_span<R, MODE, DOT, false, true, 5, true><<<g, kSpanThreads, 0, s>>>(v, a);
-        else if (kind == 3 || kind >= 5) k_span<R, MODE, DOT, false, true><<<g, kSpanThreads, 0, s>>>(v, a);
+        if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, false, true><<<g, kSpanThreads, 0, s>>>(v, a);
         else k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
     }
     SPFD_LAUNCH_CHECK();
@@ -1344,12 +1119,7 @@ int vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
     const double *od = L.odinv.get();
     const double *xbase = nullptr;
     const int rv = alt_dirs() ? 1 : 0;
-    const bool fused = fused_fine(h);
-    if (h.pre <= 1 && fused) {
-        // d = r - A(od r) and u = d - A(od d) in one launch
-        launch_fused<R, 2, 2, false>(h, SpanArgs{nullptr, r, od, nullptr, nullptr, nullptr, d, nullptr},
-                                     SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr}, s);
-    } else if (h.pre <= 1) {
+    if (h.pre <= 1) {
         SpanArgs sa{nullptr, r, od, nullptr, nullptr, nullptr, d, nullptr};
         sa.rev = rv;
         launch_fine<R, 2, false>(*h.op, sa, s);
@@ -1363,8 +1133,7 @@ int vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
         xbase = t;
     }
     SPFD_LAUNCH_CHECK();
-    if (!(h.pre <= 1 && fused))
-        launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr}, s);
+    launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr}, s);
     SPFD_LAUNCH_CHECK();
     // level 1 gets r_1 and (when it smooths) its first Jacobi iterate od_1 r_1
     const bool x0 = h.pre <= 1 && (int)h.lv.size() > 2;
@@ -1372,11 +1141,6 @@ int vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
                                                              C.odinv.get(), x0 ? C.vt.get() : nullptr, rv);
     SPFD_LAUNCH_CHECK();
     vcycle_level<R>(h, 1, C.vr.get(), C.vx.get(), s);
-    if (fused && h.post == 1) {
-        // x1 = base + e - od A e and z = x1 + od (r - A x1) (+ r.z) in one launch
-        return launch_fused<R, 4, 3, true>(h, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr},
-                                           SpanArgs{d, r, od, nullptr, nullptr, nullptr, z, h.partials.get()}, s);
-    }
     launch_fine<R, 4, false>(*h.op, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr}, s);
     SPFD_LAUNCH_CHECK();
     if (h.post == 0) {
@@ -1744,9 +1508,8 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
             restart = false;
         }
         if (it >= cfg.max_iters) break;
-        const bool fz = fused_fine(h);  // fused V-cycle passes run forward: flip the chain
-        const int rv = alt_dirs() && fz ? 1 : 0;
-        int g = level0_apply<R>(h, 0, true, p, nullptr, q, s, !fz);  // q = A p, p.q
+        const int rv = 0;
+        int g = level0_apply<R>(h, 0, true, p, nullptr, q, s, true);  // q = A p, p.q
         finalize<R>(h, g, S_PQ, F_ALPHA, s);
         // x += alpha p on the side stream, overlapping the V-cycle (which is
         // L1/latency-bound and leaves HBM bandwidth idle); joined before p changes
@@ -1793,7 +1556,7 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
         if (h.vc_partials > 0) finalize<R>(h, h.vc_partials, S_RZ, F_BETA, s);  // r.z fused into the post-smooth
         else dot<R>(h, n, r, z, S_RZ, F_BETA, s);
         SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));  // x += alpha p done before p changes
-        k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, alt_dirs() && fused_fine(h) ? 1 : 0);
+        k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, 0);
         SPFD_LAUNCH_CHECK();
     }
     SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
@@ -1840,11 +1603,10 @@ void pcg_body(Amg &h, cudaGraphConditionalHandle hnd, cudaStream_t s) {
     if (h.vc_partials > 0) finalize<R>(h, h.vc_partials, S_RZ, F_BETA_AUTO, s);
     else dot<R>(h, n, r, z, S_RZ, F_BETA_AUTO, s);
     SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
-    const bool fz = fused_fine(h);  // fused V-cycle passes run forward: flip the chain
-    const int rv = alt_dirs() && fz ? 1 : 0;
+    const int rv = 0;
     k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, rv);
     SPFD_LAUNCH_CHECK();
-    const int g = level0_apply<R>(h, 0, true, p, nullptr, q, s, !fz);  // q = A p, p.q
+    const int g = level0_apply<R>(h, 0, true, p, nullptr, q, s, true);  // q = A p, p.q
     finalize<R>(h, g, S_PQ, F_ALPHA, s);
     k_update_r<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, r, q, h.partials.get(), rv);
     SPFD_LAUNCH_CHECK();
@@ -2578,9 +2340,7 @@ double amg_iteration_bytes(const Amg &h, int nrhs) {
     double b = k.spmv + 3.0 * k.blas1;  // q = A p; r, x, p updates
     if (h.lv.size() == 1) return b + coarse_vcycle_bytes(h, 0, R);
     const double pos = h.structured ? (double)h.op->L : 0.0;
-    if (h.structured && fused_fine(h) && h.pre <= 1 && h.post == 1)  // d and x1 written once, read from L2
-        b += k.presmooth + pos * 16.0 * R + k.aggsum + k.prolong + pos * 16.0 * R + coarse_vcycle_bytes(h, 1, R);
-    else if (h.structured) b += 2.0 * k.presmooth + k.aggsum + k.prolong + k.postsmooth + coarse_vcycle_bytes(h, 1, R);
+    if (h.structured) b += 2.0 * k.presmooth + k.aggsum + k.prolong + k.postsmooth + coarse_vcycle_bytes(h, 1, R);
     else b += coarse_vcycle_bytes(h, 0, R);
     return b;
 }
@@ -2603,14 +2363,10 @@ double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cu
         const size_t vb = (size_t)C.nvec * nrhs * sizeof(double);
         for (DevBuf<double> *v : {&C.vr, &C.vx, &C.vd, &C.vt}) SPFD_CUDA(cudaMemsetAsync(v->get(), 0x3e, vb, s));
     }
-    SPFD_CHECK(which < 10 || (fused_fine(h) && two && h.pre <= 1 && h.post == 1), SPFD_EINVAL,
-               "fused fine passes are not in use");
+    SPFD_CHECK(which >= 0 && which < 10, SPFD_EINVAL, "unknown kernel");
     const KernelBytes kb = kernel_bytes(h, nrhs);
-    const double Rd = nrhs, pos = h.structured ? (double)h.op->L : 0.0;
-    const double byt[12] = {kb.spmv, kb.presmooth, kb.postsmooth, 0.0, kb.prolong, kb.aggsum, kb.l1_pre, kb.l1_pp,
-                            kb.blas1, kb.blas1,
-                            kb.presmooth + pos * 16.0 * Rd,     // fused: r, od, w -> d, u
-                            kb.prolong + pos * 16.0 * Rd};      // fused: w, od, agg, r, e_c -> x1, z
+    const double byt[10] = {kb.spmv, kb.presmooth, kb.postsmooth, 0.0, kb.prolong, kb.aggsum, kb.l1_pre, kb.l1_pp,
+                            kb.blas1, kb.blas1};
     auto launch2 = [&](auto rt) {
         constexpr int R = decltype(rt)::value;
         double *p = h.kp.get(), *r = h.kr.get(), *q = h.kq.get(), *z = h.kz.get();
@@ -2648,19 +2404,6 @@ double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cu
                 k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h.scal.get(), z, p);
                 SPFD_LAUNCH_CHECK();
                 break;
-            case 10: {
-                const double *od = L.odinv.get();
-                launch_fused<R, 2, 2, false>(h, SpanArgs{nullptr, r, od, nullptr, nullptr, nullptr, L.vd.get(), nullptr},
-                                             SpanArgs{nullptr, L.vd.get(), od, nullptr, nullptr, nullptr, q, nullptr}, s);
-                break;
-            }
-            case 11: {
-                const double *od = L.odinv.get();
-                Level &C = h.lv[1];
-                launch_fused<R, 4, 3, true>(h, SpanArgs{nullptr, r, od, nullptr, C.vx.get(), L.agg_pos.get(), L.vd.get(), nullptr},
-                                            SpanArgs{L.vd.get(), r, od, nullptr, nullptr, nullptr, q, h.partials.get()}, s);
-                break;
-            }
             default: {
                 const int mode = which == 0 ? 0 : (which == 1 ? 2 : 3);
                 level0_apply<R>(h, mode, which != 1, p, r, q, s);

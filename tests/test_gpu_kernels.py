@@ -1,7 +1,6 @@
-"""GPU A/B of the fine-level stencil kernels: flat, with the tile's L2 bulk
-prefetch, and with the V-cycle's dependent pass pairs fused into one
-persistent launch (every stencil mode bit-identical, so V-cycles give the
-same bits; Krylov solves agree to tolerance), plus the graph / host-loop and
+"""GPU A/B of the fine-level stencil kernels: flat and with the tile's L2
+bulk prefetch (every stencil mode bit-identical, so V-cycles give the same
+bits; Krylov solves agree to tolerance), plus the graph / host-loop and
 block / MGS solver A/B tests.
 
 Every stencil mode must be bit-identical between the two kernels, so a
@@ -21,8 +20,8 @@ from conftest import golden_cases, golden_model, load_golden
 
 pytestmark = pytest.mark.gpu
 
-FLAT, PF, FUSED, STG, VOX = 2, 3, 4, 5, 6
-KINDS = (FUSED, PF, FLAT, STG, VOX)
+FLAT, PF = 2, 3
+KINDS = (PF, FLAT)
 
 
 def _set_kernel(kind):
