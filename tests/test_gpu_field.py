@@ -230,6 +230,7 @@ def test_cleaning_box_level0_matches_csr(g, grid, monkeypatch):
     from paper_2010_12879_b200 import SolveConfig
     from paper_2010_12879_b200.field_source import FieldOps
     out = []
+    monkeypatch.setenv("SPFD_CLEAN_SOLVER", "amg")
     for flag in ("1", "0"):
         monkeypatch.setenv("SPFD_CLEAN_BOX", flag)
         ops = FieldOps(grid, SolveConfig())
@@ -239,3 +240,32 @@ def test_cleaning_box_level0_matches_csr(g, grid, monkeypatch):
     fn = np.linalg.norm(g["flux"])
     assert np.linalg.norm(out[0][0] - out[1][0]) <= 1e-10 * fn
     assert abs(out[0][1] - out[1][1]) <= 1
+
+
+@pytest.mark.parametrize("dims", [(7, 5, 9), (24, 17, 40), (1, 6, 11)])
+def test_cleaning_spectral_matches_amg(dims, rng, monkeypatch):
+    """The default projection solve (sine transforms in x and y, one
+    tridiagonal solve per mode along z) against the reference's method
+    (AMG + Krylov on div div^T at rel_tol <= 1e-12) on random fluxes:
+    same projection to the Krylov tolerance, residual at rounding level,
+    identical skip / post-check decisions."""
+    from paper_2010_12879_b200 import SolveConfig, StaggeredGrid
+    from paper_2010_12879_b200.field_source import FieldOps
+    grid = StaggeredGrid(dims, (0.002, 0.003, 0.0025))
+    nf = sum(int(np.prod([d + (1 if a == ax else 0) for a, d in enumerate(dims)])) for ax in range(3))
+    flux = rng.standard_normal((2, nf))
+    out = {}
+    for solver in ("spectral", "amg"):
+        monkeypatch.setenv("SPFD_CLEAN_SOLVER", solver)
+        ops = FieldOps(grid, SolveConfig())
+        c = ops.clean(torch.from_numpy(flux).cuda(), 1e-10).cpu().numpy()
+        out[solver] = (c, ops.last_clean)
+    c_s, i_s = out["spectral"]
+    c_a, i_a = out["amg"]
+    for k in range(2):
+        fn = np.linalg.norm(flux[k])
+        assert np.linalg.norm(c_s[k] - c_a[k]) <= 1e-10 * fn
+        assert i_s[k].solved == 1 and i_s[k].iterations == 0 and i_s[k].solve_rel_residual <= 1e-13
+        assert i_s[k].rel_after <= 1e-12
+    d = oracle.divergence_matrix(dims)
+    assert np.abs(d @ c_s[0]).max() <= 1e-11 * np.abs(flux[0]).max()
