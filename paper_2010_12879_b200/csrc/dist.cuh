@@ -731,6 +731,49 @@ int apply_dist(Amg &h, int mode, bool dot, double *x, const double *r, double *y
     return dot ? launch_fine_ov<R, 1, true>(D, op, sa, x, s) : launch_fine_ov<R, 1, false>(D, op, sa, x, s);
 }
 
+// Convergence test of one distributed PCG iteration on the device (the
+// host loop's test): counts the iteration, records the estimates, and once
+// the loop would stop (all rhs converged, a non-finite estimate or the
+// iteration cap) freezes the solve -- every rhs inactive, so the alpha of
+// the iterations still queued behind it is 0 and x, r stay as they are.
+// The host reads the scalars once per batch of iterations instead of once
+// per iteration.
+__global__ void k_dist_check(double *scal, int R, double *trace) {
+    if (scal[S_G_DONE] != 0.0) return;
+    const int it = (int)scal[S_G_IT] + 1;
+    scal[S_G_IT] = it;
+    const double tol = scal[S_G_TOL];
+    const int maxit = (int)scal[S_G_MAXIT];
+    bool done = true, bad = false;
+    for (int c = 0; c < R; ++c) {
+        const double bb = scal[S_BB + c], rr = scal[S_RR + c];
+        const double bn = sqrt(bb);
+        const double est = bn > 0 ? sqrt(rr) / bn : 0.0;
+        if (!isfinite(est)) bad = true;
+        trace[(int64_t)(it - 1) * R + c] = est;
+        if (est > tol) done = false;
+        const bool conv = bb == 0.0 || sqrt(rr) <= tol * bn;
+        scal[S_ACTIVE + c] = conv ? 0.0 : 1.0;
+    }
+    if (bad) scal[S_G_STATUS] = 1.0;
+    if (done || bad || it >= maxit) {
+        scal[S_G_DONE] = 1.0;
+        for (int c = 0; c < R; ++c) scal[S_ACTIVE + c] = 0.0;
+    }
+}
+
+// iterations queued per host read (SPFD_DIST_BATCH, default 4; 1 = the
+// per-iteration loop)
+inline int dist_batch() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_DIST_BATCH");
+        v = e ? atoi(e) : 4;
+        if (v < 1) v = 1;
+    }
+    return v;
+}
+
 template <int R>
 spfd_report pcg_dist(Amg &h, const double *b, double *x, const spfd_config &cfg, double *h_trace, cudaStream_t s) {
     Dist &D = *h.dist;
@@ -755,12 +798,24 @@ spfd_report pcg_dist(Amg &h, const double *b, double *x, const spfd_config &cfg,
     for (int c = 0; c < R; ++c) all_zero = all_zero && bnorm[c] == 0.0;
     if (all_zero) { rep.converged = 1; return rep; }
     const double tol = cfg.rel_tol;
+    if (h.pcg_trace_cap < cfg.max_iters) {
+        h.pcg_trace_cap = std::max<int64_t>(cfg.max_iters, 1024);
+        h.pcg_trace.alloc(h.pcg_trace_cap * 2);
+    }
+    {
+        // S_G_TOL, S_G_MAXIT, S_G_IT, S_G_INIT, S_G_STATUS, S_G_DONE, (2 spare)
+        const double g[8] = {tol, (double)cfg.max_iters, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        static_assert(S_G_DONE - S_G < 8 && S_END - S_G == 8, "graph scalar slots");
+        SPFD_CUDA(cudaMemcpyAsync(sc + S_G, g, sizeof g, cudaMemcpyHostToDevice, s));
+    }
     int it = 0;
     bool restart = true;
     while (true) {
         if (restart) {
             apply_dist<R>(h, 1, false, x, b, r, s);                 // r = b - A x (own range)
             SPFD_CUDA(cudaMemcpyAsync(sc + S_ACTIVE, ones, R * sizeof(double), cudaMemcpyHostToDevice, s));
+            const double zero = 0.0;
+            SPFD_CUDA(cudaMemcpyAsync(sc + S_G_DONE, &zero, sizeof(double), cudaMemcpyHostToDevice, s));
             int g = vcycle_dist_fine<R>(h, r, z, s);
             if (g > 0) finalize_dist<R>(h, g, S_RZ, F_BETA_INIT, s);
             else dot_dist<R>(h, r, z, S_RZ, F_BETA_INIT, s);
@@ -768,23 +823,35 @@ spfd_report pcg_dist(Amg &h, const double *b, double *x, const spfd_config &cfg,
             restart = false;
         }
         if (it >= cfg.max_iters) break;
-        int g = apply_dist<R>(h, 0, true, p, nullptr, q, s);        // q = A p, p.q
-        finalize_dist<R>(h, g, S_PQ, F_ALPHA, s);
-        k_update_xr<R><<<kDotGrid, kDotThreads, 0, s>>>(no, sc, x + off, r + off, p + off, q + off, h.partials.get());
-        SPFD_LAUNCH_CHECK();
-        finalize_dist<R>(h, kDotGrid, S_RR, F_STORE, s);
-        k_set_active<<<1, 1, 0, s>>>(sc, R, tol);
-        SPFD_CUDA(cudaMemcpyAsync(hs, sc, S_H * sizeof(double), cudaMemcpyDeviceToHost, s));
-        SPFD_CUDA(cudaStreamSynchronize(s));
-        ++it;
-        bool done = true;
-        for (int c = 0; c < R; ++c) {
-            double est = bnorm[c] > 0 ? std::sqrt(hs[S_RR + c]) / bnorm[c] : 0.0;
-            if (!std::isfinite(est)) { rep.status = SPFD_ENONFINITE; rep.iterations = it; return rep; }
-            if (h_trace) h_trace[(int64_t)(it - 1) * R + c] = est;
-            if (est > tol) done = false;
+        // a batch of iterations, the convergence test on the device; the
+        // ones queued behind a stop are no-ops (k_dist_check)
+        const int nb = std::min(dist_batch(), cfg.max_iters - it);
+        for (int k = 0; k < nb; ++k) {
+            int g = apply_dist<R>(h, 0, true, p, nullptr, q, s);    // q = A p, p.q
+            finalize_dist<R>(h, g, S_PQ, F_ALPHA, s);
+            k_update_xr<R><<<kDotGrid, kDotThreads, 0, s>>>(no, sc, x + off, r + off, p + off, q + off,
+                                                           h.partials.get());
+            SPFD_LAUNCH_CHECK();
+            finalize_dist<R>(h, kDotGrid, S_RR, F_STORE, s);
+            k_dist_check<<<1, 1, 0, s>>>(sc, R, h.pcg_trace.get());
+            SPFD_LAUNCH_CHECK();
+            if (k + 1 == nb) break;  // the host decides what follows the batch's last test
+            int gz = vcycle_dist_fine<R>(h, r, z, s);
+            if (gz > 0) finalize_dist<R>(h, gz, S_RZ, F_BETA, s);
+            else dot_dist<R>(h, r, z, S_RZ, F_BETA, s);
+            k_xpby<R><<<grid_for(no, 256, 148 * 16), 256, 0, s>>>(no, sc, z + off, p + off);
+            SPFD_LAUNCH_CHECK();
         }
-        if (done || it >= cfg.max_iters) {
+        double gs[8];
+        SPFD_CUDA(cudaMemcpyAsync(gs, sc + S_G, sizeof gs, cudaMemcpyDeviceToHost, s));
+        SPFD_CUDA(cudaStreamSynchronize(s));
+        const int nit = (int)gs[S_G_IT - S_G];
+        if (h_trace && nit > it)
+            SPFD_CUDA(cudaMemcpy(h_trace + (int64_t)it * R, h.pcg_trace.get() + (int64_t)it * R,
+                                 (size_t)(nit - it) * R * sizeof(double), cudaMemcpyDeviceToHost));
+        it = nit;
+        if (gs[S_G_STATUS - S_G] != 0.0) { rep.status = SPFD_ENONFINITE; rep.iterations = it; return rep; }
+        if (gs[S_G_DONE - S_G] != 0.0 || it >= cfg.max_iters) {
             int gt = apply_dist<R>(h, 1, true, x, b, q, s);
             finalize_dist<R>(h, gt, S_TMP, F_STORE, s);
             SPFD_CUDA(cudaMemcpyAsync(hs, sc, S_H * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -27,6 +27,7 @@ enum {
     S_TMP = 16, S_LOC = 20, S_H = 32,  // S_LOC: per-rank partial scalars; FGMRES Hessenberg column from S_H
     S_G = S_H + 256,                    // graph PCG: tol, max_iters, iteration, init flag, status
     S_G_TOL = S_G, S_G_MAXIT = S_G + 1, S_G_IT = S_G + 2, S_G_INIT = S_G + 3, S_G_STATUS = S_G + 4,
+    S_G_DONE = S_G + 5,  // distributed PCG: iterations batched between host reads (pcg_dist)
     S_END = S_G + 8
 };
 

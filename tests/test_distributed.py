@@ -68,17 +68,22 @@ def test_slab_balancing_rule():
         assert max(counts) - min(counts) <= 50  # balanced to one plane
 
 
-def _solve_worker(rank, size, port, out, name, replicate_below):
+def _solve_worker(rank, size, port, out, name, replicate_below, transport="host"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from paper_2010_12879_b200 import Session, SolveConfig, workloads
     from paper_2010_12879_b200.distributed import Communicator
-    torch.cuda.set_device(0)
-    _init(rank, size, port)
+    if transport == "nccl":  # one GPU per rank
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=size,
+                                device_id=torch.device("cuda", rank))
+    else:
+        torch.cuda.set_device(0)
+        _init(rank, size, port)
     w = getattr(workloads, name)()
     sess = Session(w.model, w.frequency_hz, SolveConfig(rel_tol=1e-10))
     a = torch.from_numpy(w.a).cuda()
-    comm = Communicator.host()
+    comm = Communicator.host() if transport == "host" else Communicator.nccl()
     sess.distribute(comm, replicate_below=replicate_below)
     vox, rep, psi = sess.snapshot(a, keep_psi=True)
     v0, v1 = sess.vox_range
@@ -146,3 +151,41 @@ def test_nccl_transport_single_rank():
         d = torch.load(os.path.join(out, "n.pt"))
     assert d["it"][0] == d["it"][1]
     assert torch.allclose(d["vox"], d["ref"], rtol=1e-10, atol=0)
+
+
+@pytest.mark.gpu
+def test_distributed_iteration_batching_is_exact(monkeypatch):
+    """The distributed PCG queues several iterations per host read, with the
+    convergence test on the device freezing the iterations behind a stop:
+    batches of 1 and 4 give the same iteration count and the same bits."""
+    res = {}
+    for batch in ("1", "4"):
+        monkeypatch.setenv("SPFD_DIST_BATCH", batch)
+        with tempfile.TemporaryDirectory() as out:
+            mp.spawn(_solve_worker, args=(2, _port(), out, "c2_small", 1000), nprocs=2, join=True)
+            res[batch] = [torch.load(os.path.join(out, f"s{r}.pt")) for r in range(2)]
+    for r in range(2):
+        assert res["1"][r]["it"] == res["4"][r]["it"]
+        assert torch.equal(res["1"][r]["psi"], res["4"][r]["psi"])
+        assert torch.equal(res["1"][r]["vox"], res["4"][r]["vox"])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_distributed_nccl_two_gpus():
+    """Two ranks on two GPUs over NCCL (NVLink): the z-slab solve against
+    the single-GPU snapshot (same bar as the host-transport test)."""
+    from paper_2010_12879_b200 import Session, SolveConfig, workloads
+    w = workloads.c2_small()
+    sess = Session(w.model, w.frequency_hz, SolveConfig(rel_tol=1e-10))
+    vox, rep, psi = sess.snapshot(torch.from_numpy(w.a).cuda(), keep_psi=True)
+    vox, psi = vox.cpu().numpy(), psi.cpu().numpy()
+    with tempfile.TemporaryDirectory() as out:
+        mp.spawn(_solve_worker, args=(2, _port(), out, "c2_small", 1000, "nccl"), nprocs=2, join=True)
+        parts = [torch.load(os.path.join(out, f"s{r}.pt")) for r in range(2)]
+    vd = np.concatenate([p["vox"].numpy() for p in parts], axis=1)
+    pd = np.concatenate([p["psi"].numpy() for p in parts], axis=1)
+    for p in parts:
+        assert abs(p["it"] - rep.iterations) <= 1 and max(p["rel"]) <= 1e-10
+    assert np.linalg.norm(pd - psi) <= 1e-8 * np.linalg.norm(psi)
+    assert np.abs(vd - vox).max() <= 1e-7 * np.abs(vox).max()
