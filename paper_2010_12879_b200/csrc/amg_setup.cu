@@ -15,6 +15,19 @@
 
 namespace spfd {
 
+// SPFD_SETUP_TRACE=1: per-phase wall times of the setup on stderr (each mark
+// synchronises the stream; for diagnosing setup-time spread only)
+static void setup_mark(const char *what, cudaStream_t s) {
+    static const bool on = getenv("SPFD_SETUP_TRACE") != nullptr;
+    if (!on) return;
+    static auto last = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[setup] %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
+
 namespace {
 
 template <class T>
@@ -300,7 +313,8 @@ struct Pieces {
     std::vector<int64_t> counts;
 };
 
-constexpr int64_t kChunkProducts = 192ll << 20;  // products per ESC chunk
+constexpr int64_t kChunkProducts = 48ll << 20;  // products per ESC chunk (~1.5 GB of keys/values + sort
+                                                // scratch: stays inside the pool's kept floor, see pool_trim)
 
 // C = A * B (sorted columns, optional zero dropping).
 void spgemm(const CsrView &a, const CsrView &b, int64_t bcols, Csr &c, bool drop_zero, cudaStream_t s) {
@@ -672,6 +686,7 @@ bool coarsen(Level &L, const Csr &A, double theta, double omega, Csr &Ac, Csr &P
     k_scatter_t<<<grid_for(n, T), T, 0, s>>>(sptr.get(), scol.get(), n, cursor.get(), tcol.get());
     SPFD_LAUNCH_CHECK();
 
+    setup_mark("strength + transpose", s);
     // pass 1
     DevBuf<int8_t> state;
     DevBuf<int32_t> claimed;
@@ -700,6 +715,7 @@ bool coarsen(Level &L, const Csr &A, double theta, double omega, Csr &Ac, Csr &P
         if (read1(n_cur, s) == 0) break;
         SPFD_CHECK(round < 4 * (int)n + 1000, SPFD_ECUDA, "aggregation did not terminate");
     }
+    setup_mark("aggregation pass 1", s);
     // pass 2 + numbering
     DevBuf<int32_t> best, single, rootflag, root_rank, single_rank;
     best.alloc(n); single.alloc(n + 1); rootflag.alloc(n + 1); root_rank.alloc(n + 1); single_rank.alloc(n + 1);
@@ -732,6 +748,7 @@ bool coarsen(Level &L, const Csr &A, double theta, double omega, Csr &Ac, Csr &P
         SPFD_CUDA(cudaStreamSynchronize(s));
     }
     Csr AT;
+    setup_mark("aggregation pass 2", s);
     spgemm(av, view(Tm), n_agg, AT, false, s);
     Tm = Csr();
     // P
@@ -766,8 +783,10 @@ bool coarsen(Level &L, const Csr &A, double theta, double omega, Csr &Ac, Csr &P
     AT = Csr();
     transpose(view(P), n_agg, R, s);
     Csr AP;
+    setup_mark("prolongator P, R", s);
     spgemm(av, view(P), n_agg, AP, true, s);
     spgemm(view(R), view(AP), n_agg, Ac, true, s);
+    setup_mark("Galerkin R A P", s);
     (void)L;
     return true;
 }
@@ -1017,6 +1036,7 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
     SPFD_CUDA(cudaEventCreate(&e0));
     SPFD_CUDA(cudaEventCreate(&e1));
     SPFD_CUDA(cudaEventRecord(e0, s));
+    setup_mark("(setup start)", s);
     auto wall0 = std::chrono::steady_clock::now();
     h->omega = cfg.jacobi_damping;
     h->pre = cfg.pre_sweeps;
@@ -1051,6 +1071,7 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
         ++depth;
     }
     int nl = (int)h->lv.size();
+    setup_mark("levels built", s);
     // per-level solve data
     for (int l = 0; l < nl; ++l) {
         Level &L = h->lv[l];
@@ -1119,6 +1140,7 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
         L.vd.alloc(L.nvec * R);
         L.vt.alloc(L.nvec * R);
     }
+    setup_mark("per-level solve data", s);
     // coarsest dense inverse
     {
         Level &C = h->lv[nl - 1];
@@ -1134,7 +1156,9 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
     // path see the reference numbering (export_level1, level1_unpermute)
     if (!(getenv("SPFD_MORTON") && std::string(getenv("SPFD_MORTON")) == "0") && h->structured && nl > 2)
         morton_level1(*h, s);
+    setup_mark("dense inverse + Morton", s);
     alloc_krylov(*h, h->lv[0].nvec, R);
+    setup_mark("workspace", s);
     if (h->smoother == SPFD_SMOOTHER_CHEBYSHEV) amg_estimate_lmax(*h, s);
     SPFD_CUDA(cudaEventRecord(e1, s));
     SPFD_CUDA(cudaEventSynchronize(e1));
