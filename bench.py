@@ -444,7 +444,8 @@ def main():
         gbs = b_.value / (m_.value * 1e-3) / 1e9
         kernels[key] = {"kernel": desc, "ms": round(m_.value, 4), "bytes": b_.value, "gbs": round(gbs, 1),
                         "frac": round(gbs / peak, 4), "launches_per_iteration": per_it,
-                        "share_of_iteration": round(m_.value * per_it / iter_ms, 4)}
+                        "share_of_iteration": round(m_.value * per_it / iter_ms, 4),
+                        "traffic": traffic_db.get(f"{args.config}_{key}_dram_bytes")}
     m_, b_ = ctypes.c_double(), ctypes.c_double()
     _lib.check(lib.spfd_bench_kernel(h.handle, 3, args.kernel_reps, 2, ctypes.byref(m_), ctypes.byref(b_),
                                      _lib.stream_ptr()))

@@ -315,10 +315,14 @@ typedef struct {
 
 /* f2: divergence_clean (field_source.py:292-329): out = in if the relative
  * cell-outflux norm is <= tol, else in - divT phi with
- * (div divT) phi = div in solved by AMG + Krylov at
- * rel_tol = min(1e-12, tol/(4 rel)).  The hierarchy on div divT is built on
- * the first call and kept by the handle.  SPFD_EPROJECTION on
- * non-convergence or a violated postcondition.  out may alias in. */
+ * (div divT) phi = div in.  Default: a direct spectral solve (div divT is the
+ * 7-point cell Laplacian with zero exterior: sine transforms in x and y, one
+ * tridiagonal solve per mode along z), residual at rounding level, i.e.
+ * within the reference's rel_tol = min(1e-12, tol/(4 rel)); h_info
+ * iterations = 0.  SPFD_CLEAN_SOLVER=amg: the reference's method, AMG +
+ * Krylov at that rel_tol, the hierarchy on div divT built on the first call
+ * and kept by the handle.  SPFD_EPROJECTION on non-convergence or a
+ * violated postcondition.  out may alias in. */
 int spfd_field_clean(spfd_field_t f, const double *in, double *out, double tol,
                      spfd_clean_info *h_info, void *stream);
 /* The same for nrhs = 1 or 2 flux vectors (planar [nrhs][n_faces], e.g.
