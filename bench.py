@@ -496,6 +496,8 @@ def main():
         "dof_iter_per_s": n_dofs * it_mean * 2 / (ms / 1e3),
         "setup_s": h.setup_seconds,
         "setup_s_repeat": setup_repeat,
+        "device_bytes": {"operator": int(sess.op.info.device_bytes), "hierarchy": int(h.device_bytes),
+                         "note": "library-owned device memory per rank (operator + AMG hierarchy with solve workspace)"},
         "levels": h.level_sizes,
         "gpu_launches": int(launches),
         "roofline": roofline,

@@ -919,7 +919,8 @@ void level1_permute(Amg &h, const int32_t *P, cudaStream_t s) {
     for (DevBuf<double> *b : {&L1.odinv, &L1.dinv}) {
         DevBuf<double> nb;
         nb.alloc(b->n);
-        SPFD_CUDA(cudaMemcpyAsync(nb.get(), b->get(), b->bytes(), cudaMemcpyDeviceToDevice, s));
+        if (b->n > (size_t)n1)  // alignment padding beyond the rows
+            SPFD_CUDA(cudaMemsetAsync(nb.get() + n1, 0, (b->n - n1) * sizeof(double), s));
         k_gather_d<<<grid_for(n1, T), T, 0, s>>>(b->get(), P, n1, nb.get());
         SPFD_LAUNCH_CHECK();
         *b = std::move(nb);

@@ -185,6 +185,7 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double *smem /* [32*K]
             v[k] = t;
         }
     }
+    __syncwarp();      // reconverge warp 0 after its reduction (synccheck)
     __syncthreads();
 }
 

@@ -234,8 +234,7 @@ __device__ __forceinline__ void span_tile(const SpanView &v, const SpanArgs &a, 
     int row = r0;
     for (int u = 0; u < kTile / kSpanThreads; ++u) {
         const int p = t * kTile + u * kSpanThreads + threadIdx.x;
-        if (p >= pend) break;
-        if (RANGED && p < a.pb) continue;
+        if (p >= pend || (RANGED && p < a.pb)) continue;  // no divergent loop exit before block_sum
         row = frow(v.rows, row, r1, p);
         const int4 q = v.rows[row];
         const Nbr n = neighbours(v, p, row, q);
@@ -277,6 +276,7 @@ __global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArg
             if (ta >= 0) tile_prefetch<R, MODE>(v, a, q0, q1);
         }
     }
+    if (PF) __syncwarp();  // warp 0 reconverges after thread 0's prefetch (synccheck)
     double dot[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) dot[c] = 0.0;
