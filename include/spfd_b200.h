@@ -173,6 +173,8 @@ typedef struct {
     int32_t cheb_degree;
     double  cheb_lmax[32];       /* Chebyshev: power-iteration estimate of
                                     lambda_max(D^-1 A_l) per level           */
+    int32_t restriction_csr;     /* 1 = the fine restriction runs as R = P^T
+                                    in CSR (else matrix-free through T)     */
 } spfd_amg_info;
 
 /* Hierarchy on the operator (level 0 = matrix-free stencil) or on a

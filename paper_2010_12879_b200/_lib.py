@@ -89,6 +89,7 @@ class AmgInfo(ctypes.Structure):
         ("smoother", ctypes.c_int32),
         ("cheb_degree", ctypes.c_int32),
         ("cheb_lmax", ctypes.c_double * 32),
+        ("restriction_csr", ctypes.c_int32),
     ]
 
 

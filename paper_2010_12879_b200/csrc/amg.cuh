@@ -43,6 +43,8 @@ struct Level {
     int p_group = 4, r_group = 32, a_group = 32;  // lanes per row in CSR kernels
     Csr AP;                   // coarse levels, V(1,1): A_l P_l for the fused prolongation + post-smooth
     int ap_group = 4;
+    Csr Rspan;                // structured level 0: R = P^T with span-position columns and rows in the
+    int rspan_group = 4;      //   level-1 solve order (build_rspan; the V-cycle's restriction)
 };
 
 struct Dist;   // z-slab decomposition (dist.cuh)
@@ -111,6 +113,7 @@ void amg_from_level0(Amg &h, const double *inter, double *planar, int nrhs, cuda
 
 int csr_group(int64_t nnz, int64_t rows);  // lanes per row of the CSR kernels
 void level1_unpermute(Amg &h, cudaStream_t s);  // reference level-1 numbering (amg_setup.cu)
+void build_rspan(Amg &h, cudaStream_t s);  // CSR restriction over span positions (amg_setup.cu)
 void amg_drop_graphs(Amg &h);  // destroy captured solve graphs (buffers changed; solve.cu)
 void amg_distribute(Amg &h, Comm *comm, int64_t replicate_below, int64_t *range, cudaStream_t s);
 void dist_range_exchange(Amg &h, double *v, int nrhs, cudaStream_t s);

@@ -799,7 +799,7 @@ int64_t Amg::device_bytes() const {
     int64_t b = cinv.bytes() + kx.bytes() + kr.bytes() + kz.bytes() + kp.bytes() + kq.bytes() + kb.bytes() +
                 partials.bytes() + scal.bytes() + fg_basis.bytes() + fg_prec.bytes();
     for (auto &l : lv)
-        b += l.A.bytes() + l.P.bytes() + l.R.bytes() + l.P_dof.bytes() + l.R_dof.bytes() + l.agg.bytes() +
+        b += l.A.bytes() + l.P.bytes() + l.R.bytes() + l.P_dof.bytes() + l.R_dof.bytes() + l.Rspan.bytes() + l.agg.bytes() +
              l.dinv.bytes() + l.odinv.bytes() + l.agg_pos.bytes() + l.mem_ptr.bytes() + l.mem_pos.bytes() + l.vr.bytes() + l.vx.bytes() + l.vd.bytes() + l.vt.bytes() + l.AP.bytes();
     return b;
 }
@@ -955,6 +955,7 @@ void level1_permute(Amg &h, const int32_t *P, cudaStream_t s) {
     }
     if (ident) h.l1_perm.clear();
     else h.l1_perm = std::move(comp);
+    build_rspan(h, s);  // rows follow the new level-1 numbering
 }
 
 // back to the reference numbering (before distributing the hierarchy)
@@ -970,6 +971,66 @@ void level1_unpermute(Amg &h, cudaStream_t s) {
 }
 
 // Morton order of the level-1 aggregates' root nodes (device keys + CUB sort)
+// The fine-level restriction r_c = R d as the reference computes it
+// (linsolve.py:190-195, R = P^T), on a CSR whose columns are span positions
+// and whose rows follow the level-1 solve numbering: one gather-SpMV over
+// nnz(P) entries instead of the matrix-free form's stencil pass over d plus
+// the aggregate sums.  The entries of each row keep R's order, so the result
+// does not depend on the level-1 numbering.  SPFD_RSPAN=0: matrix-free.
+__global__ void k_rspan_len(const int64_t *__restrict__ rptr, const int32_t *__restrict__ perm, int64_t n1,
+                            int64_t *__restrict__ len) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n1; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = perm ? perm[g] : g;
+        len[g] = rptr[r + 1] - rptr[r];
+    }
+}
+
+__global__ void k_rspan_fill(CsrView R, const int32_t *__restrict__ perm, const int32_t *__restrict__ dof_to_pos,
+                             const int64_t *__restrict__ optr, int64_t n1, int32_t *__restrict__ col,
+                             double *__restrict__ val) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n1; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = perm ? perm[g] : g;
+        const int64_t a = R.ptr[r], b = R.ptr[r + 1], o = optr[g];
+        for (int64_t q = a; q < b; ++q) {
+            col[o + (q - a)] = dof_to_pos[R.col[q]];
+            val[o + (q - a)] = R.val[q];
+        }
+    }
+}
+
+void build_rspan(Amg &h, cudaStream_t s) {
+    static const bool on = !(getenv("SPFD_RSPAN") && std::string(getenv("SPFD_RSPAN")) == "0");
+    if (h.lv.empty()) return;
+    Level &L0 = h.lv[0];
+    L0.Rspan = Csr{};
+    if (!on || !h.structured || h.lv.size() < 2 || L0.R_dof.rows == 0) return;
+    const int T = 256;
+    const int64_t n1 = h.lv[1].n;
+    DevBuf<int32_t> perm;
+    if (!h.l1_perm.empty()) {
+        perm.alloc(n1);
+        SPFD_CUDA(cudaMemcpyAsync(perm.get(), h.l1_perm.data(), n1 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    }
+    DevBuf<int64_t> len;
+    len.alloc(n1 + 1);
+    SPFD_CUDA(cudaMemsetAsync(len.get() + n1, 0, sizeof(int64_t), s));
+    k_rspan_len<<<grid_for(n1, T), T, 0, s>>>(L0.R_dof.ptr.get(), perm.n ? perm.get() : nullptr, n1, len.get());
+    SPFD_LAUNCH_CHECK();
+    Csr &M = L0.Rspan;
+    M.rows = n1;
+    M.cols = L0.nvec;
+    M.ptr.alloc(n1 + 1);
+    scan_excl(len.get(), M.ptr.get(), n1 + 1, s);
+    M.nnz = read1(M.ptr.get() + n1, s);
+    M.col.alloc(M.nnz);
+    M.val.alloc(M.nnz);
+    k_rspan_fill<<<grid_for(n1, T), T, 0, s>>>(view(L0.R_dof), perm.n ? perm.get() : nullptr,
+                                               h.op->dof_to_pos.get(), M.ptr.get(), n1, M.col.get(), M.val.get());
+    SPFD_LAUNCH_CHECK();
+    L0.rspan_group = pick_group(M.nnz, M.rows);
+    if (const char *e = getenv("SPFD_GROUP_RSPAN")) L0.rspan_group = atoi(e);
+}
+
 static void morton_level1(Amg &h, cudaStream_t s) {
     const int T = 256;
     Level &L0 = h.lv[0], &L1 = h.lv[1];
@@ -1157,6 +1218,7 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
     // path see the reference numbering (export_level1, level1_unpermute)
     if (!(getenv("SPFD_MORTON") && std::string(getenv("SPFD_MORTON")) == "0") && h->structured && nl > 2)
         morton_level1(*h, s);
+    build_rspan(*h, s);
     setup_mark("dense inverse + Morton", s);
     alloc_krylov(*h, h->lv[0].nvec, R);
     setup_mark("workspace", s);

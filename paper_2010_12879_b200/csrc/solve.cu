@@ -1134,12 +1134,20 @@ int vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
         xbase = t;
     }
     SPFD_LAUNCH_CHECK();
-    launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr}, s);
-    SPFD_LAUNCH_CHECK();
     // level 1 gets r_1 and (when it smooths) its first Jacobi iterate od_1 r_1
     const bool x0 = h.pre <= 1 && (int)h.lv.size() > 2;
-    k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n, u, C.vr.get(),
-                                                             C.odinv.get(), x0 ? C.vt.get() : nullptr, rv);
+    if (L.Rspan.rows) {
+        // r_1 = R d, R = P^T as a CSR over span positions (build_rspan)
+        launch_csr<R, 0, false>(L.Rspan, L.rspan_group, d, nullptr, nullptr, nullptr, C.vr.get(), nullptr, s,
+                                C.odinv.get(), x0 ? C.vt.get() : nullptr);
+    } else {
+        // matrix-free: u = d - A(od d), r_1 = T^T u
+        launch_fine<R, 2, false>(*h.op, SpanArgs{nullptr, d, od, nullptr, nullptr, nullptr, u, nullptr}, s);
+        SPFD_LAUNCH_CHECK();
+        k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n, u,
+                                                                 C.vr.get(), C.odinv.get(), x0 ? C.vt.get() : nullptr,
+                                                                 rv);
+    }
     SPFD_LAUNCH_CHECK();
     vcycle_level<R>(h, 1, C.vr.get(), C.vx.get(), s);
     launch_fine<R, 4, false>(*h.op, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr}, s);
@@ -2301,7 +2309,9 @@ KernelBytes kernel_bytes(const Amg &h, double R) {
         if (h.lv.size() > 1) {
             const double n1 = (double)h.lv[1].n;
             k.prolong = n * (36.0 + 16.0 * R) + mask + n1 * 8.0 * R;  // w, odinv, agg; r -> x1; e_c
-            k.aggsum = n * (4.0 + 8.0 * R) + n1 * (8.0 + 8.0 + 16.0 * R);  // members, u; ptr, od_c -> r_c, x0_c
+            k.aggsum = h.lv[0].Rspan.rows
+                           ? csr_bytes(h.lv[0].Rspan) + n * 8.0 * R + n1 * (8.0 + 16.0 * R)  // R; d; od_c -> r_c, x0_c
+                           : n * (4.0 + 8.0 * R) + n1 * (8.0 + 8.0 + 16.0 * R);  // members, u; ptr, od_c -> r_c, x0_c
         }
     } else {
         const Level &L = h.lv[0];
@@ -2341,7 +2351,9 @@ double amg_iteration_bytes(const Amg &h, int nrhs) {
     double b = k.spmv + 3.0 * k.blas1;  // q = A p; r, x, p updates
     if (h.lv.size() == 1) return b + coarse_vcycle_bytes(h, 0, R);
     const double pos = h.structured ? (double)h.op->L : 0.0;
-    if (h.structured) b += 2.0 * k.presmooth + k.aggsum + k.prolong + k.postsmooth + coarse_vcycle_bytes(h, 1, R);
+    if (h.structured)
+        b += (h.lv[0].Rspan.rows ? 1.0 : 2.0) * k.presmooth + k.aggsum + k.prolong + k.postsmooth +
+             coarse_vcycle_bytes(h, 1, R);
     else b += coarse_vcycle_bytes(h, 0, R);
     return b;
 }
@@ -2381,8 +2393,13 @@ double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cu
             }
             case 5: {
                 Level &C = h.lv[1];
-                k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n, p,
-                                                                         C.vr.get(), C.odinv.get(), C.vt.get(), 0);
+                if (L.Rspan.rows)
+                    launch_csr<R, 0, false>(L.Rspan, L.rspan_group, p, nullptr, nullptr, nullptr, C.vr.get(),
+                                            nullptr, s, C.odinv.get(), C.vt.get());
+                else
+                    k_agg_sum<R><<<grid_for(C.n, 256, 148 * 16), 256, 0, s>>>(L.mem_ptr.get(), L.mem_pos.get(), C.n,
+                                                                             p, C.vr.get(), C.odinv.get(),
+                                                                             C.vt.get(), 0);
                 SPFD_LAUNCH_CHECK();
                 break;
             }
