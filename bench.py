@@ -428,7 +428,8 @@ def main():
     table = [(0, "fine_spmv", "k_span<2,0,1> fine SpMV q = A p (+ p.q)", 1),
              (1, "fine_presmooth", "k_span<2,2> pre-smooth + defect d = r - A(od r)"
               + ("" if h.restriction_csr else " (also the restriction input)"), 1 if h.restriction_csr else 2),
-             (4, "fine_prolongation", "k_span<2,4> matrix-free prolongation x1 = od r + e - od A e", 1),
+             (4, "fine_prolongation", "k_csr<1,2,4> prolongation x1 = od r + P e, P over span positions"
+              if h.prolongation_csr else "k_span<2,4> matrix-free prolongation x1 = od r + e - od A e", 1),
              (2, "fine_postsmooth", "k_span<2,3,1> post-smooth z = x1 + od (r - A x1) (+ r.z)", 1),
              (5, "fine_restriction", "k_csr<4,2,0> restriction r_c = R d, R = P^T over span positions"
               if h.restriction_csr else "k_agg_sum<2> restriction sums r_c = T^T u", 1),

@@ -173,8 +173,9 @@ typedef struct {
     int32_t cheb_degree;
     double  cheb_lmax[32];       /* Chebyshev: power-iteration estimate of
                                     lambda_max(D^-1 A_l) per level           */
-    int32_t restriction_csr;     /* 1 = the fine restriction runs as R = P^T
-                                    in CSR (else matrix-free through T)     */
+    int32_t restriction_csr;     /* bit 0: the fine restriction runs as R = P^T
+                                    in CSR (else matrix-free through T);
+                                    bit 1: the fine prolongation as P in CSR */
 } spfd_amg_info;
 
 /* Hierarchy on the operator (level 0 = matrix-free stencil) or on a

@@ -799,7 +799,7 @@ int64_t Amg::device_bytes() const {
     int64_t b = cinv.bytes() + kx.bytes() + kr.bytes() + kz.bytes() + kp.bytes() + kq.bytes() + kb.bytes() +
                 partials.bytes() + scal.bytes() + fg_basis.bytes() + fg_prec.bytes();
     for (auto &l : lv)
-        b += l.A.bytes() + l.P.bytes() + l.R.bytes() + l.P_dof.bytes() + l.R_dof.bytes() + l.Rspan.bytes() + l.agg.bytes() +
+        b += l.A.bytes() + l.P.bytes() + l.R.bytes() + l.P_dof.bytes() + l.R_dof.bytes() + l.Rspan.bytes() + l.Pspan.bytes() + l.agg.bytes() +
              l.dinv.bytes() + l.odinv.bytes() + l.agg_pos.bytes() + l.mem_ptr.bytes() + l.mem_pos.bytes() + l.vr.bytes() + l.vx.bytes() + l.vd.bytes() + l.vt.bytes() + l.AP.bytes();
     return b;
 }
@@ -998,12 +998,83 @@ __global__ void k_rspan_fill(CsrView R, const int32_t *__restrict__ perm, const 
     }
 }
 
+// The fine-level prolongation x1 = x0 + P e on the reference's P (rows: span
+// positions, empty for non-DOF positions; columns: level-1 solve indices),
+// each row's entries in P's stored order.  About 3.6 entries per row: a
+// short-row gather-SpMV from the L2-resident coarse vector instead of the
+// matrix-free (I - omega D^-1 A) T e, whose 7-point stencil re-reads the
+// aggregate map and the conductances at every neighbour.  SPFD_PSPAN=0:
+// matrix-free.
+__global__ void k_inv_perm_i(const int32_t *__restrict__ solve_to_ref, int64_t n, int32_t *__restrict__ ref_to_solve) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x)
+        ref_to_solve[solve_to_ref[g]] = (int32_t)g;
+}
+
+__global__ void k_pspan_len(const int64_t *__restrict__ pptr, const int32_t *__restrict__ pos_to_dof, int64_t L,
+                            int64_t *__restrict__ len) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L; p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t d = pos_to_dof[p];
+        len[p] = d >= 0 ? pptr[d + 1] - pptr[d] : 0;
+    }
+}
+
+__global__ void k_pspan_fill(CsrView P, const int32_t *__restrict__ pos_to_dof, const int32_t *__restrict__ ref_to_solve,
+                             const int64_t *__restrict__ optr, int64_t L, int32_t *__restrict__ col,
+                             double *__restrict__ val) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L; p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t d = pos_to_dof[p];
+        if (d < 0) continue;
+        const int64_t a = P.ptr[d], b = P.ptr[d + 1], o = optr[p];
+        for (int64_t q = a; q < b; ++q) {
+            const int32_t c = P.col[q];
+            col[o + (q - a)] = ref_to_solve ? ref_to_solve[c] : c;
+            val[o + (q - a)] = P.val[q];
+        }
+    }
+}
+
+void build_pspan(Amg &h, const int32_t *solve_to_ref, cudaStream_t s) {
+    static const bool on = !(getenv("SPFD_PSPAN") && std::string(getenv("SPFD_PSPAN")) == "0");
+    Level &L0 = h.lv[0];
+    L0.Pspan = Csr{};
+    if (!on || !h.structured || h.lv.size() < 2 || L0.P_dof.rows == 0) return;
+    const int T = 256;
+    const int64_t n1 = h.lv[1].n, L = L0.nvec;
+    DevBuf<int32_t> r2s;
+    if (solve_to_ref) {
+        r2s.alloc(n1);
+        k_inv_perm_i<<<grid_for(n1, T), T, 0, s>>>(solve_to_ref, n1, r2s.get());
+        SPFD_LAUNCH_CHECK();
+    }
+    DevBuf<int64_t> len;
+    len.alloc(L + 1);
+    SPFD_CUDA(cudaMemsetAsync(len.get() + L, 0, sizeof(int64_t), s));
+    k_pspan_len<<<grid_for(L, T), T, 0, s>>>(L0.P_dof.ptr.get(), h.op->pos_to_dof.get(), L, len.get());
+    SPFD_LAUNCH_CHECK();
+    Csr &M = L0.Pspan;
+    M.rows = L;
+    M.cols = n1;
+    M.ptr.alloc(L + 1);
+    scan_excl(len.get(), M.ptr.get(), L + 1, s);
+    M.nnz = read1(M.ptr.get() + L, s);
+    M.col.alloc(M.nnz);
+    M.val.alloc(M.nnz);
+    k_pspan_fill<<<grid_for(L, T), T, 0, s>>>(view(L0.P_dof), h.op->pos_to_dof.get(), r2s.n ? r2s.get() : nullptr,
+                                              M.ptr.get(), L, M.col.get(), M.val.get());
+    SPFD_LAUNCH_CHECK();
+    // ~3.6 entries per row: one thread per row (coalesced epilogue; measured
+    // 161 us vs 195 us with 2 lanes and 316 us with 4 on C3)
+    L0.pspan_group = 1;
+    if (const char *e = getenv("SPFD_GROUP_PSPAN")) L0.pspan_group = atoi(e);
+}
+
 void build_rspan(Amg &h, cudaStream_t s) {
     static const bool on = !(getenv("SPFD_RSPAN") && std::string(getenv("SPFD_RSPAN")) == "0");
     if (h.lv.empty()) return;
     Level &L0 = h.lv[0];
     L0.Rspan = Csr{};
-    if (!on || !h.structured || h.lv.size() < 2 || L0.R_dof.rows == 0) return;
+    L0.Pspan = Csr{};
+    if (!h.structured || h.lv.size() < 2 || L0.R_dof.rows == 0) return;
     const int T = 256;
     const int64_t n1 = h.lv[1].n;
     DevBuf<int32_t> perm;
@@ -1011,6 +1082,8 @@ void build_rspan(Amg &h, cudaStream_t s) {
         perm.alloc(n1);
         SPFD_CUDA(cudaMemcpyAsync(perm.get(), h.l1_perm.data(), n1 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     }
+    build_pspan(h, perm.n ? perm.get() : nullptr, s);
+    if (!on) return;
     DevBuf<int64_t> len;
     len.alloc(n1 + 1);
     SPFD_CUDA(cudaMemsetAsync(len.get() + n1, 0, sizeof(int64_t), s));

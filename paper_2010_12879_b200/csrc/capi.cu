@@ -223,6 +223,7 @@ int spfd_amg_info_get(spfd_amg_t h, spfd_amg_info *info) {
         info->cheb_degree = a.cheb_deg;
         for (size_t l = 0; l < a.cheb_lmax.size() && l < 32; ++l) info->cheb_lmax[l] = a.cheb_lmax[l];
         info->restriction_csr = (a.structured && a.lv.size() > 1 && a.lv[0].Rspan.rows > 0) ? 1 : 0;
+        if (a.structured && a.lv.size() > 1 && a.lv[0].Pspan.rows > 0) info->restriction_csr |= 2;
     });
 }
 

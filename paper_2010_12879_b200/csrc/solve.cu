@@ -614,6 +614,8 @@ int launch_csr(const Csr &m, int G, const double *x, const double *r, const doub
                const int32_t *rowmap = nullptr) {
     int grid = csr_grid(m.rows, G);
     switch (G) {
+        case 1: launch_csr_g<1, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
+        case 2: launch_csr_g<2, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
         case 4: launch_csr_g<4, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
         case 8: launch_csr_g<8, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
         case 16: launch_csr_g<16, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
@@ -1150,7 +1152,12 @@ int vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
     }
     SPFD_LAUNCH_CHECK();
     vcycle_level<R>(h, 1, C.vr.get(), C.vx.get(), s);
-    launch_fine<R, 4, false>(*h.op, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr}, s);
+    if (L.Pspan.rows) {  // x1 = x0 + P e, P in CSR over span positions (build_pspan)
+        if (xbase) launch_csr<R, 5, false>(L.Pspan, L.pspan_group, C.vx.get(), r, od, xbase, d, nullptr, s);
+        else launch_csr<R, 4, false>(L.Pspan, L.pspan_group, C.vx.get(), r, od, nullptr, d, nullptr, s);
+    } else {
+        launch_fine<R, 4, false>(*h.op, SpanArgs{nullptr, r, od, xbase, C.vx.get(), L.agg_pos.get(), d, nullptr}, s);
+    }
     SPFD_LAUNCH_CHECK();
     if (h.post == 0) {
         SPFD_CUDA(cudaMemcpyAsync(z, d, bytes, cudaMemcpyDeviceToDevice, s));
@@ -2308,7 +2315,9 @@ KernelBytes kernel_bytes(const Amg &h, double R) {
         k.postsmooth = n * (32.0 + 24.0 * R) + mask;    // w, odinv; x, r -> x'
         if (h.lv.size() > 1) {
             const double n1 = (double)h.lv[1].n;
-            k.prolong = n * (36.0 + 16.0 * R) + mask + n1 * 8.0 * R;  // w, odinv, agg; r -> x1; e_c
+            k.prolong = h.lv[0].Pspan.rows
+                            ? csr_bytes(h.lv[0].Pspan) + n * (8.0 + 16.0 * R) + n1 * 8.0 * R  // P; odinv; r -> x1; e_c
+                            : n * (36.0 + 16.0 * R) + mask + n1 * 8.0 * R;  // w, odinv, agg; r -> x1; e_c
             k.aggsum = h.lv[0].Rspan.rows
                            ? csr_bytes(h.lv[0].Rspan) + n * 8.0 * R + n1 * (8.0 + 16.0 * R)  // R; d; od_c -> r_c, x0_c
                            : n * (4.0 + 8.0 * R) + n1 * (8.0 + 8.0 + 16.0 * R);  // members, u; ptr, od_c -> r_c, x0_c
@@ -2387,8 +2396,13 @@ double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cu
             case 3: amg_vcycle(h, r, z, R, s); break;
             case 4: {
                 Level &C = h.lv[1];
-                SpanArgs sa{nullptr, r, L.odinv.get(), nullptr, C.vx.get(), L.agg_pos.get(), q, nullptr};
-                launch_fine<R, 4, false>(*h.op, sa, s);
+                if (L.Pspan.rows) {
+                    launch_csr<R, 4, false>(L.Pspan, L.pspan_group, C.vx.get(), r, L.odinv.get(), nullptr, q, nullptr,
+                                            s);
+                } else {
+                    SpanArgs sa{nullptr, r, L.odinv.get(), nullptr, C.vx.get(), L.agg_pos.get(), q, nullptr};
+                    launch_fine<R, 4, false>(*h.op, sa, s);
+                }
                 break;
             }
             case 5: {

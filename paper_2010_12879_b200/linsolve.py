@@ -167,7 +167,8 @@ class AmgHierarchy:
         self.damping = cfg.jacobi_damping
         self.structured = bool(info.structured)
         self.device_bytes = int(info.device_bytes)
-        self.restriction_csr = bool(info.restriction_csr)  # fine restriction as R = P^T in CSR
+        self.restriction_csr = bool(info.restriction_csr & 1)    # fine restriction as R = P^T in CSR
+        self.prolongation_csr = bool(info.restriction_csr & 2)   # fine prolongation as P in CSR
         self.smoother = "chebyshev" if info.smoother == _lib.SMOOTHER_CHEBYSHEV else "jacobi"
         self.chebyshev_degree = int(info.cheb_degree)
         # lambda_max(D^-1 A_l) estimates behind the Chebyshev intervals (levels < coarsest)
