@@ -315,38 +315,60 @@ __global__ void __launch_bounds__(256) k_dgemm_strided(GemmArgs g) {
         }
 }
 
-// Thomas sweep along z for every (x, y) mode and nrhs right-hand sides
-// (planar [nrhs][nz][ny][nx], in place), d scaled by `scale` on input;
-// cp: [nz][ny*nx] scratch for the eliminated super-diagonal.
-__global__ void k_tridiag_z(int64_t nx, int64_t ny, int64_t nz, int nrhs, const double *__restrict__ lx,
-                            const double *__restrict__ ly, double scale, double *d, double *cp) {
-    const int64_t plane = nx * ny, nc = plane * nz;
+// The eliminated pivots of every mode's z system depend only on the mode:
+// inv_k = 1 / (mu + c_{k-1}), c_k = -inv_k, computed once per grid
+// (k_tridiag_pivots); the per-snapshot solve (k_tridiag_apply) is then
+// division-free, one thread per (mode, rhs):
+//   forward  d'_k = (scale d_k + d'_{k-1}) inv_k
+//   backward x_k  = d'_k + inv_k x_{k+1}
+__global__ void k_tridiag_pivots(int64_t nx, int64_t ny, int64_t nz, const double *__restrict__ lx,
+                                 const double *__restrict__ ly, double *__restrict__ inv) {
+    const int64_t plane = nx * ny;
     const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (col >= plane) return;
     const double mu = 2.0 + lx[col % nx] + ly[col / nx];
-    double c = 0.0, dp0 = 0.0, dp1 = 0.0;
+    double c = 0.0;
     for (int64_t k = 0; k < nz; ++k) {
-        const int64_t q = k * plane + col;
-        const double inv = 1.0 / (mu + c);
-        c = -inv;
-        cp[q] = c;
-        dp0 = (d[q] * scale + dp0) * inv;
-        d[q] = dp0;
-        if (nrhs > 1) {
-            dp1 = (d[nc + q] * scale + dp1) * inv;
-            d[nc + q] = dp1;
-        }
+        const double iv = 1.0 / (mu + c);
+        c = -iv;
+        inv[k * plane + col] = iv;
     }
-    double x0 = 0.0, x1 = 0.0;
-    for (int64_t k = nz - 1; k >= 0; --k) {
-        const int64_t q = k * plane + col;
-        const double ck = cp[q];
-        x0 = d[q] - ck * x0;
-        d[q] = x0;
-        if (nrhs > 1) {
-            x1 = d[nc + q] - ck * x1;
-            d[nc + q] = x1;
-        }
+}
+
+__global__ void k_tridiag_apply(int64_t nx, int64_t ny, int64_t nz, int nrhs, const double *__restrict__ inv,
+                                double scale, double *__restrict__ d) {
+    constexpr int B = 8;  // z planes per batch: all loads of a batch in flight before its recurrence steps
+    const int64_t plane = nx * ny, nc = plane * nz;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= plane * nrhs) return;
+    const int64_t col = t % plane;
+    double *x = d + (t / plane) * nc + col;
+    const double *iv = inv + col;
+    double dp = 0.0;
+    for (int64_t k0 = 0; k0 < nz; k0 += B) {
+        double xv[B], vv[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            if (k0 + u < nz) { xv[u] = x[(k0 + u) * plane]; vv[u] = iv[(k0 + u) * plane]; }
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            if (k0 + u < nz) {
+                dp = (xv[u] * scale + dp) * vv[u];
+                x[(k0 + u) * plane] = dp;
+            }
+    }
+    double xn = 0.0;
+    for (int64_t k1 = nz; k1 > 0; k1 -= B) {
+        double xv[B], vv[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            if (k1 - 1 - u >= 0) { xv[u] = x[(k1 - 1 - u) * plane]; vv[u] = iv[(k1 - 1 - u) * plane]; }
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            if (k1 - 1 - u >= 0) {
+                xn = xv[u] + vv[u] * xn;
+                x[(k1 - 1 - u) * plane] = xn;
+            }
     }
 }
 
@@ -517,6 +539,50 @@ __global__ void __launch_bounds__(kRedThreads) k_sumsq_partial(int64_t n, const 
     if (threadIdx.x == 0) part[blockIdx.x] = v[0];
 }
 
+// Sum of squares of the circulation defect (k_circulation) without storing
+// it: blocks walk face rows (axis, j, k) with threads along i, so the face
+// index needs one division per row instead of 64-bit div/mod per face;
+// per-block partials, summed on the host in block order.
+__global__ void __launch_bounds__(kRedThreads) k_circ_sumsq(Box g, const double *__restrict__ a,
+                                                            const double *__restrict__ flux,
+                                                            double *__restrict__ part) {
+    __shared__ double red[32];
+    const int64_t nx = g.n[0], ny = g.n[1], nz = g.n[2];
+    const int64_t E0 = nx * (ny + 1) * (nz + 1), E1 = (nx + 1) * ny * (nz + 1);
+    const int64_t eoff[3] = {0, E0, E0 + E1};
+    double v[1] = {0.0};
+    int64_t fbase = 0, rbase = 0;
+    for (int ax = 0; ax < 3; ++ax) {
+        int64_t fd[3] = {nx, ny, nz};
+        fd[ax] += 1;
+        const int64_t nrow = fd[1] * fd[2];
+        const int e1 = (ax + 1) % 3, e2 = (ax + 2) % 3;
+        int64_t ed1[3] = {nx + 1, ny + 1, nz + 1}, ed2[3] = {nx + 1, ny + 1, nz + 1};
+        ed1[e1] -= 1;
+        ed2[e2] -= 1;
+        auto eidx = [&](const int64_t *ed, int64_t i, int64_t j, int64_t k) { return i + ed[0] * (j + ed[1] * k); };
+        for (int64_t row = blockIdx.x; row < nrow; row += gridDim.x) {
+            const int64_t j = row % fd[1], k = row / fd[1];
+            for (int64_t i = threadIdx.x; i < fd[0]; i += blockDim.x) {
+                int64_t c[3] = {i, j, k}, s1[3] = {i, j, k}, s2[3] = {i, j, k};
+                s1[e1] += 1;
+                s2[e2] += 1;
+                double circ = a[eoff[e1] + eidx(ed1, c[0], c[1], c[2])];
+                circ += a[eoff[e2] + eidx(ed2, s1[0], s1[1], s1[2])];
+                circ -= a[eoff[e1] + eidx(ed1, s2[0], s2[1], s2[2])];
+                circ -= a[eoff[e2] + eidx(ed2, c[0], c[1], c[2])];
+                const double d = circ - flux[fbase + row * fd[0] + i];
+                v[0] = fma(d, d, v[0]);
+            }
+        }
+        fbase += nrow * fd[0];
+        rbase += nrow;
+    }
+    (void)rbase;
+    block_sum<1>(v, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+}
+
 // lowest index of the largest |x| (np.argmax(np.abs(x)))
 __global__ void __launch_bounds__(kRedThreads) k_argmax_partial(int64_t n, const double *__restrict__ x,
                                                                 double *__restrict__ pv, int64_t *__restrict__ pi) {
@@ -586,7 +652,8 @@ struct Field {
     Amg *clean_amg = nullptr; // AMG on div divᵀ (built on first use; SPFD_CLEAN_SOLVER=amg)
     double clean_setup_seconds = 0.0;
     DevBuf<double> sx, sy, lx, ly;  // spectral projection: DST-I matrices and 1-D eigenvalues
-    DevBuf<double> spec_ws;         // [2][nc] transform ping-pong + [nc] Thomas scratch
+    DevBuf<double> spec_ws;         // [2][nc] transform ping-pong
+    DevBuf<double> spec_inv;        // [nc] eliminated pivots of the z systems (per mode, k)
     ~Field() { delete clean_amg; }
     int64_t n_cells() const { return g.n[0] * g.n[1] * g.n[2]; }
     int64_t n_faces() const { return face_count(g, 0) + face_count(g, 1) + face_count(g, 2); }
@@ -756,7 +823,12 @@ static void ensure_spectral(Field &F, cudaStream_t s) {
     };
     build(nx, F.sx, F.lx);
     build(ny, F.sy, F.ly);
-    F.spec_ws.alloc(3 * F.n_cells());
+    F.spec_ws.alloc(2 * F.n_cells());
+    F.spec_inv.alloc(F.n_cells());
+    const int64_t plane = nx * ny;
+    k_tridiag_pivots<<<(unsigned)((plane + 127) / 128), 128, 0, s>>>(nx, ny, F.g.n[2], F.lx.get(), F.ly.get(),
+                                                                    F.spec_inv.get());
+    SPFD_LAUNCH_CHECK();
 }
 
 static void gemm(const GemmArgs &g, int64_t batch, cudaStream_t s) {
@@ -770,7 +842,7 @@ static void spectral_solve(Field &F, int na, const double *d, double *phi, cudaS
     ensure_spectral(F, s);
     const int64_t nx = F.g.n[0], ny = F.g.n[1], nz = F.g.n[2], plane = nx * ny, nc = plane * nz;
     SPFD_CHECK(ny * nz <= (int64_t)65535 * kGBN && nz * na <= 65535, SPFD_EINVAL, "grid too large for the spectral solve");
-    double *buf = F.spec_ws.get(), *cp = F.spec_ws.get() + 2 * nc;
+    double *buf = F.spec_ws.get();
     const double *Sx = F.sx.get(), *Sy = F.sy.get();
     // along x: out(p, col) = sum_i Sx(p, i) in(i, col), col = (j, k)
     auto along_x = [&](const double *in, double *out) {
@@ -782,8 +854,8 @@ static void spectral_solve(Field &F, int na, const double *d, double *phi, cudaS
     };
     along_x(d, buf);
     along_y(buf, phi);
-    k_tridiag_z<<<(unsigned)((plane + 127) / 128), 128, 0, s>>>(nx, ny, nz, na, F.lx.get(), F.ly.get(),
-                                                               4.0 / ((double)(nx + 1) * (double)(ny + 1)), phi, cp);
+    k_tridiag_apply<<<(unsigned)((plane * na + 127) / 128), 128, 0, s>>>(
+        nx, ny, nz, na, F.spec_inv.get(), 4.0 / ((double)(nx + 1) * (double)(ny + 1)), phi);
     SPFD_LAUNCH_CHECK();
     along_y(phi, buf);
     along_x(buf, phi);
@@ -958,11 +1030,21 @@ void field_gauge(Field &F, int tree, const double *flux, double *a, double tol, 
             SPFD_LAUNCH_CHECK();
         }
     }
-    // postcondition: circulation residual over every face (gauging.py:167-171)
-    if (F.wf.n < (size_t)nf) F.wf.alloc(nf);
-    field_circulation(F, a, flux, F.wf.get(), s);
-    info->rel_residual = std::sqrt(sumsq(F, F.wf.get(), nf, s)) / fnorm;
+    // postcondition: circulation residual over every face (gauging.py:167-171);
+    // the defect array is only materialised to locate the worst face
+    k_circ_sumsq<<<kRedBlocks, kRedThreads, 0, s>>>(F.g, a, flux, F.part.get());
+    SPFD_LAUNCH_CHECK();
+    {
+        std::vector<double> h(kRedBlocks);
+        SPFD_CUDA(cudaMemcpyAsync(h.data(), F.part.get(), kRedBlocks * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPFD_CUDA(cudaStreamSynchronize(s));
+        double t = 0.0;
+        for (double v : h) t += v;  // fixed order
+        info->rel_residual = std::sqrt(t) / fnorm;
+    }
     if (info->rel_residual > tol) {
+        if (F.wf.n < (size_t)nf) F.wf.alloc(nf);
+        field_circulation(F, a, flux, F.wf.get(), s);
         info->worst_face = argmax_abs(F, F.wf.get(), nf, &info->worst_defect, s);
         char msg[200];
         snprintf(msg, sizeof msg, "incompatible fluxes: relative circulation residual %.3e (worst face %lld, defect %.3e)",
