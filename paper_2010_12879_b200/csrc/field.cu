@@ -118,6 +118,56 @@ __global__ void k_interp_faces(Box g, Box lat, int a, const double *__restrict__
     }
 }
 
+// The trilinear parameters of a face depend on one coordinate each, so they
+// are tabulated per axis (k_axis_params: d0 + d1 + d2 entries) and the face
+// kernel walks face rows (j, k) with threads along i -- the same values and
+// the same product order as k_interp_faces, without its per-face divisions
+// and 64-bit div/mod.
+__global__ void k_axis_params(Box g, Box lat, int a, AxisParam *tab) {
+    int64_t d[3] = {g.n[0], g.n[1], g.n[2]};
+    d[a] += 1;
+    const int64_t tot = d[0] + d[1] + d[2];
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < tot; q += (int64_t)gridDim.x * blockDim.x) {
+        const int ax = q < d[0] ? 0 : (q < d[0] + d[1] ? 1 : 2);
+        const int64_t i = ax == 0 ? q : (ax == 1 ? q - d[0] : q - d[0] - d[1]);
+        tab[q] = axis_param(face_coord(g, a, ax, i), lat.o[ax], lat.h[ax], lat.n[ax]);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_interp_rows(Box g, Box lat, int a, const AxisParam *__restrict__ tab,
+                                                     const double *__restrict__ b, double area,
+                                                     double *__restrict__ flux) {
+    int64_t d[3] = {g.n[0], g.n[1], g.n[2]};
+    d[a] += 1;
+    const int64_t nrow = d[1] * d[2];
+    const AxisParam *tx = tab, *ty = tab + d[0], *tz = tab + d[0] + d[1];
+    for (int64_t row = blockIdx.x; row < nrow; row += gridDim.x) {
+        const int64_t j = row % d[1], k = row / d[1];
+        const AxisParam py = ty[j], pz = tz[k];
+        for (int64_t i = threadIdx.x; i < d[0]; i += blockDim.x) {
+            const AxisParam px = tx[i];
+            double out = 0.0;
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                const double wx = dx ? px.t : __dsub_rn(1.0, px.t);
+#pragma unroll
+                for (int dy = 0; dy < 2; ++dy) {
+                    const double wy = dy ? py.t : __dsub_rn(1.0, py.t);
+                    const double wxy = __dmul_rn(wx, wy);
+#pragma unroll
+                    for (int dz = 0; dz < 2; ++dz) {
+                        const double wz = dz ? pz.t : __dsub_rn(1.0, pz.t);
+                        const int64_t p = (px.i0 + dx * px.s) +
+                                          lat.n[0] * ((py.i0 + dy * py.s) + lat.n[1] * (pz.i0 + dz * pz.s));
+                        out = __dadd_rn(out, __dmul_rn(__dmul_rn(wxy, wz), b[3 * p + a]));
+                    }
+                }
+            }
+            flux[row * d[0] + i] = __dmul_rn(out, area);
+        }
+    }
+}
+
 // Biot-Savart field of a closed polyline (coil_field, field_source.py:163-197):
 // exact finite straight-wire expression per segment.  flag[0] is set when a
 // point lies within `eps` of a wire segment (SingularPointError).
@@ -649,6 +699,7 @@ struct Field {
     DevBuf<double> part;      // reduction partials
     DevBuf<int64_t> parti;
     DevBuf<double> wc, wf;    // cell / face workspaces
+    DevBuf<AxisParam> wt;     // per-axis trilinear parameters (field_interpolate)
     Amg *clean_amg = nullptr; // AMG on div divᵀ (built on first use; SPFD_CLEAN_SOLVER=amg)
     double clean_setup_seconds = 0.0;
     DevBuf<double> sx, sy, lx, ly;  // spectral projection: DST-I matrices and 1-D eigenvalues
@@ -732,7 +783,14 @@ void field_interpolate(Field &F, const spfd_box &lat, const double *b, double *f
         const double area = F.g.h[t0] * F.g.h[t1];
         const int64_t nf = face_count(F.g, a);
         if (nf) {
-            k_interp_faces<<<blocks(nf), 256, 0, s>>>(F.g, L, a, b, area, flux + off);
+            int64_t d[3] = {F.g.n[0], F.g.n[1], F.g.n[2]};
+            d[a] += 1;
+            const int64_t nt = d[0] + d[1] + d[2];
+            if (F.wt.n < (size_t)nt) F.wt.alloc(nt);
+            k_axis_params<<<blocks(nt), 256, 0, s>>>(F.g, L, a, F.wt.get());
+            const int grid = (int)std::min<int64_t>(d[1] * d[2], 148 * 16);
+            k_interp_rows<<<grid, d[0] >= 256 ? 256 : (int)((d[0] + 31) / 32 * 32), 0, s>>>(F.g, L, a, F.wt.get(), b,
+                                                                                           area, flux + off);
             SPFD_LAUNCH_CHECK();
         }
         off += nf;
