@@ -1034,7 +1034,7 @@ __global__ void k_pspan_fill(CsrView P, const int32_t *__restrict__ pos_to_dof, 
 }
 
 void build_pspan(Amg &h, const int32_t *solve_to_ref, cudaStream_t s) {
-    static const bool on = !(getenv("SPFD_PSPAN") && std::string(getenv("SPFD_PSPAN")) == "0");
+    const bool on = !(getenv("SPFD_PSPAN") && std::string(getenv("SPFD_PSPAN")) == "0");
     Level &L0 = h.lv[0];
     L0.Pspan = Csr{};
     if (!on || !h.structured || h.lv.size() < 2 || L0.P_dof.rows == 0) return;
@@ -1069,7 +1069,7 @@ void build_pspan(Amg &h, const int32_t *solve_to_ref, cudaStream_t s) {
 }
 
 void build_rspan(Amg &h, cudaStream_t s) {
-    static const bool on = !(getenv("SPFD_RSPAN") && std::string(getenv("SPFD_RSPAN")) == "0");
+    const bool on = !(getenv("SPFD_RSPAN") && std::string(getenv("SPFD_RSPAN")) == "0");
     if (h.lv.empty()) return;
     Level &L0 = h.lv[0];
     L0.Rspan = Csr{};

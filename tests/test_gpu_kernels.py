@@ -271,3 +271,35 @@ def test_fgmres_graph_restarts_and_max_iters(monkeypatch):
         assert res[0][:2] == res[1][:2]
         assert np.linalg.norm(res[0][2] - res[1][2]) <= 1e-10 * np.linalg.norm(res[1][2])
     assert res[0][0] == 4 and not res[0][1]
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_fine_transfers_csr_vs_matrix_free(name, monkeypatch, rng):
+    """The fine-level restriction R d and prolongation x0 + P e run on the
+    reference's R = P^T and P as CSRs over span positions by default
+    (SPFD_RSPAN / SPFD_PSPAN) and matrix-free through the aggregates when
+    disabled: the same V-cycle to rounding (different summation orders), the
+    same PCG iteration counts and solutions to the solve tolerance; the info
+    flags report the layout in use."""
+    import paper_2010_12879_b200 as p
+    from paper_2010_12879_b200 import workloads
+    w = getattr(workloads, name)()
+    grid = p.StaggeredGrid.from_model(w.model)
+    system = p.assemble_poisson(w.model, grid, w.a[0], w.frequency_hz)
+    cfg = p.SolveConfig(rel_tol=1e-10)
+    r = rng.standard_normal((2, system.matrix.shape[0]))
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SPFD_RSPAN", flag)
+        monkeypatch.setenv("SPFD_PSPAN", flag)
+        h = p.amg_setup(system.matrix, cfg)
+        assert h.restriction_csr == (flag == "1") and h.prolongation_csr == (flag == "1")
+        z = p.v_cycle(h, r)
+        x, rep = p.solve(system.matrix, system.rhs, h, cfg)
+        assert rep.converged
+        out[flag] = (z, x, rep.iterations)
+    z1, x1, i1 = out["1"]
+    z0, x0, i0 = out["0"]
+    assert np.linalg.norm(z1 - z0) <= 1e-13 * np.linalg.norm(z0)
+    assert i1 == i0
+    assert np.linalg.norm(x1 - x0) <= 1e-9 * np.linalg.norm(x0)
