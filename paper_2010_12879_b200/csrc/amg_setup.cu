@@ -182,6 +182,63 @@ __global__ void k_agg_round(Graph g, int8_t *state, int32_t *claimed, int *queue
     }
 }
 
+// The same round with one warp per worklist node: the lanes split each
+// node's 2-hop scan (claimers of {i} U S(i)) and its dependant
+// notifications; warp votes give the node's decision.  On the coarser
+// levels, whose strong graphs are dense (hundreds to thousands of 2-hop
+// pairs per node), a thread-per-node round is one long serial loop per
+// node; on level 0 the warp form also wins (shorter rounds).  Same
+// per-node rule, same fixed point.
+__global__ void k_agg_round_warp(Graph g, int8_t *state, int32_t *claimed, int *queued, int round, const int *cur,
+                                 const int *n_cur_p, int *next, int *n_next, int full_n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int n_cur = full_n > 0 ? full_n : *n_cur_p;
+    for (int64_t idx = wid; idx < n_cur; idx += nw) {
+        const int i = full_n > 0 ? (int)idx : cur[idx];
+        if (*(volatile int8_t *)&state[i] != 0) continue;
+        bool blocked = false, waiting = false;
+        for (int64_t a = g.sp[i] - 1; a < g.sp[i + 1]; ++a) {
+            const int x = a < g.sp[i] ? i : g.sc[a];
+            bool bl = false;
+            for (int64_t b = g.tp[x] - 1 + lane; b < g.tp[x + 1]; b += 32) {
+                const int r = b < g.tp[x] ? x : g.tc[b];
+                const int8_t st = *(volatile int8_t *)&state[r];
+                if (st == 1) bl = true;
+                if (st == 0 && r < i) waiting = true;
+            }
+            if (__any_sync(0xffffffffu, bl)) { blocked = true; break; }
+        }
+        waiting = __any_sync(0xffffffffu, waiting);
+        if (blocked) {
+            if (lane == 0) state[i] = 2;
+        } else if (!waiting) {
+            if (lane == 0) claimed[i] = i;
+            for (int64_t a = g.sp[i] + lane; a < g.sp[i + 1]; a += 32) claimed[g.sc[a]] = i;
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) state[i] = 1;
+        } else {
+            continue;
+        }
+        __syncwarp();
+        // dependants: j > i with j in {x} U ST(x) for x in {i} U S(i)
+        for (int64_t a = g.sp[i] - 1; a < g.sp[i + 1]; ++a) {
+            const int x = a < g.sp[i] ? i : g.sc[a];
+            for (int64_t b = g.tp[x] - 1 + lane; b < g.tp[x + 1]; b += 32) {
+                const int j = b < g.tp[x] ? x : g.tc[b];
+                if (j <= i) continue;
+                if (*(volatile int8_t *)&state[j] != 0) continue;
+                if (atomicExch(&queued[j], round + 1) != round + 1) {
+                    const int slot = atomicAdd(n_next, 1);
+                    next[slot] = j;
+                }
+            }
+        }
+    }
+}
+
 __global__ void k_swap_counts(int *n_cur, int *n_next) {
     *n_cur = *n_next;
     *n_next = 0;
@@ -647,6 +704,14 @@ int pick_group(int64_t nnz, int64_t rows) {
 
 // One coarsening step on level l (CSR A in level numbering).  Returns false
 // on stagnation.
+// tentative prolongator T: one unit entry per row (column = aggregate)
+__global__ void k_tent_fill(int64_t n, int64_t *ptr, double *val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+        ptr[i] = i;
+        if (i < n) val[i] = 1.0;
+    }
+}
+
 bool coarsen(Level &L, const Csr &A, double theta, double omega, Csr &Ac, Csr &P, Csr &R, DevBuf<int32_t> &agg,
              cudaStream_t s) {
     const int T = 256;
@@ -700,14 +765,29 @@ bool coarsen(Level &L, const Csr &A, double theta, double omega, Csr &Ac, Csr &P
     int *cur = wl0.get(), *nxt = wl1.get();
     int *n_cur = counts.get(), *n_next = counts.get() + 1;
     const int G = 148 * 8;
-    k_agg_round<<<grid_for(n, T, G), T, 0, s>>>(g, state.get(), claimed.get(), queued.get(), 0, cur, n_cur, nxt,
-                                               n_next, (int)n);
+    // warp per node where the strong graph is dense (see k_agg_round_warp;
+    // SPFD_AGG_WARP=0: thread per node everywhere)
+    // one warp per node on every level (C3 pass 1: level 0 259 -> 111 ms,
+    // level 1 430 -> 47 ms, level 2 270 -> 19 ms); SPFD_AGG_WARP=0: one thread
+    const char *aw = getenv("SPFD_AGG_WARP");
+    const bool warp_round = !(aw && std::string(aw) == "0");
+    if (warp_round)
+        k_agg_round_warp<<<G, T, 0, s>>>(g, state.get(), claimed.get(), queued.get(), 0, cur, n_cur, nxt, n_next,
+                                         (int)n);
+    else
+        k_agg_round<<<grid_for(n, T, G), T, 0, s>>>(g, state.get(), claimed.get(), queued.get(), 0, cur, n_cur, nxt,
+                                                   n_next, (int)n);
     k_swap_counts<<<1, 1, 0, s>>>(n_cur, n_next);
     std::swap(cur, nxt);
     int round = 1;
     while (true) {
         for (int b = 0; b < 64; ++b, ++round) {
-            k_agg_round<<<G, T, 0, s>>>(g, state.get(), claimed.get(), queued.get(), round, cur, n_cur, nxt, n_next, 0);
+            if (warp_round)
+                k_agg_round_warp<<<G, T, 0, s>>>(g, state.get(), claimed.get(), queued.get(), round, cur, n_cur, nxt,
+                                                 n_next, 0);
+            else
+                k_agg_round<<<G, T, 0, s>>>(g, state.get(), claimed.get(), queued.get(), round, cur, n_cur, nxt,
+                                            n_next, 0);
             k_swap_counts<<<1, 1, 0, s>>>(n_cur, n_next);
             std::swap(cur, nxt);
         }
@@ -738,15 +818,9 @@ bool coarsen(Level &L, const Csr &A, double theta, double omega, Csr &Ac, Csr &P
     // tentative T (n x n_agg, ones) and AT = A * T (zeros kept)
     Csr Tm;
     Tm.alloc(n, n_agg, n);
-    {
-        std::vector<int64_t> hp(n + 1);
-        for (int64_t i = 0; i <= n; ++i) hp[i] = i;
-        SPFD_CUDA(cudaMemcpyAsync(Tm.ptr.get(), hp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        std::vector<double> hv((size_t)n, 1.0);
-        SPFD_CUDA(cudaMemcpyAsync(Tm.val.get(), hv.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
-        SPFD_CUDA(cudaMemcpyAsync(Tm.col.get(), agg.get(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        SPFD_CUDA(cudaStreamSynchronize(s));
-    }
+    k_tent_fill<<<grid_for(n + 1, T), T, 0, s>>>(n, Tm.ptr.get(), Tm.val.get());  // ptr = 0..n, values 1
+    SPFD_LAUNCH_CHECK();
+    SPFD_CUDA(cudaMemcpyAsync(Tm.col.get(), agg.get(), n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     Csr AT;
     setup_mark("aggregation pass 2", s);
     spgemm(av, view(Tm), n_agg, AT, false, s);
