@@ -434,7 +434,8 @@ def main():
              (5, "fine_restriction", "k_csr<4,2,0> restriction r_c = R d, R = P^T over span positions"
               if h.restriction_csr else "k_agg_sum<2> restriction sums r_c = T^T u", 1),
              (6, "level1_presmooth", "k_csr<4,2,1> level-1 pre-smooth residual", 1),
-             (7, "level1_prolong_post", "k_csr_pp<4,2> level-1 fused prolongation + post-smooth", 1),
+             (7, "level1_prolong_post", "k_csr<4,2,6> level-1 prolongation + post-smooth z = od (r + d) + Q e, "
+              "Q = P - od A P", 1),
              (8, "pcg_r_update", "k_update_r<2> r -= alpha q (+ r.r)", 1),
              (9, "pcg_p_update", "k_xpby<2> p = z + beta p", 1)]
     kernels = {}

@@ -45,6 +45,8 @@ struct Level {
     int ap_group = 4;
     Csr Rspan;                // structured level 0: R = P^T with span-position columns and rows in the
     int rspan_group = 4;      //   level-1 solve order (build_rspan; the V-cycle's restriction)
+    Csr Q;                    // coarse levels, V(1,1): Q = P - diag(omega D^-1) A P (pattern of A P), so the
+    int q_group = 4;          //   prolongation + post-smooth is z = omega D^-1 (r + d) + Q e (build_q)
     Csr Pspan;                // structured level 0: P with span-position rows and level-1 solve columns
     int pspan_group = 4;      //   (build_rspan; the V-cycle's prolongation)
 };
@@ -117,6 +119,7 @@ int csr_group(int64_t nnz, int64_t rows);  // lanes per row of the CSR kernels
 void level1_unpermute(Amg &h, cudaStream_t s);  // reference level-1 numbering (amg_setup.cu)
 void build_rspan(Amg &h, cudaStream_t s);  // CSR restriction + prolongation over span positions (amg_setup.cu)
 void build_pspan(Amg &h, const int32_t *solve_to_ref, cudaStream_t s);
+void build_q(Amg &h, cudaStream_t s);  // combined coarse prolongation + post-smooth operators (amg_setup.cu)
 void amg_drop_graphs(Amg &h);  // destroy captured solve graphs (buffers changed; solve.cu)
 void amg_distribute(Amg &h, Comm *comm, int64_t replicate_below, int64_t *range, cudaStream_t s);
 void dist_range_exchange(Amg &h, double *v, int nrhs, cudaStream_t s);

@@ -873,7 +873,7 @@ int64_t Amg::device_bytes() const {
     int64_t b = cinv.bytes() + kx.bytes() + kr.bytes() + kz.bytes() + kp.bytes() + kq.bytes() + kb.bytes() +
                 partials.bytes() + scal.bytes() + fg_basis.bytes() + fg_prec.bytes();
     for (auto &l : lv)
-        b += l.A.bytes() + l.P.bytes() + l.R.bytes() + l.P_dof.bytes() + l.R_dof.bytes() + l.Rspan.bytes() + l.Pspan.bytes() + l.agg.bytes() +
+        b += l.A.bytes() + l.P.bytes() + l.R.bytes() + l.P_dof.bytes() + l.R_dof.bytes() + l.Rspan.bytes() + l.Pspan.bytes() + l.Q.bytes() + l.agg.bytes() +
              l.dinv.bytes() + l.odinv.bytes() + l.agg_pos.bytes() + l.mem_ptr.bytes() + l.mem_pos.bytes() + l.vr.bytes() + l.vx.bytes() + l.vd.bytes() + l.vt.bytes() + l.AP.bytes();
     return b;
 }
@@ -1030,6 +1030,7 @@ void level1_permute(Amg &h, const int32_t *P, cudaStream_t s) {
     if (ident) h.l1_perm.clear();
     else h.l1_perm = std::move(comp);
     build_rspan(h, s);  // rows follow the new level-1 numbering
+    build_q(h, s);
 }
 
 // back to the reference numbering (before distributing the hierarchy)
@@ -1140,6 +1141,55 @@ void build_pspan(Amg &h, const int32_t *solve_to_ref, cudaStream_t s) {
     // 161 us vs 195 us with 2 lanes and 316 us with 4 on C3)
     L0.pspan_group = 1;
     if (const char *e = getenv("SPFD_GROUP_PSPAN")) L0.pspan_group = atoi(e);
+}
+
+// Coarse-level V(1,1) prolongation + post-smooth as one operator:
+//   z = od r + P e + od (d - (A P) e) = od (r + d) + Q e,  Q = P - diag(od) A P
+// with the pattern of A P (which contains P's: A has a full diagonal and the
+// product keeps zeros).  One gather-SpMV over nnz(A P) entries instead of
+// P and A P (k_csr_pp).  A row of P outside A P's pattern drops Q for the
+// level.  SPFD_Q=0 keeps k_csr_pp.
+__global__ void k_q_fill(CsrView P, CsrView AP, const double *__restrict__ od, double *__restrict__ qv,
+                         int *__restrict__ bad) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < AP.rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const double o = od[r];
+        int64_t p = P.ptr[r];
+        const int64_t p1 = P.ptr[r + 1];
+        for (int64_t q = AP.ptr[r]; q < AP.ptr[r + 1]; ++q) {
+            double v = -(o * AP.val[q]);
+            if (p < p1 && P.col[p] == AP.col[q]) v += P.val[p++];
+            qv[q] = v;
+        }
+        if (p != p1) *bad = 1;
+    }
+}
+
+void build_q(Amg &h, cudaStream_t s) {
+    const bool on = !(getenv("SPFD_Q") && std::string(getenv("SPFD_Q")) == "0");
+    const int T = 256;
+    for (size_t l = 0; l < h.lv.size(); ++l) {
+        Level &L = h.lv[l];
+        L.Q = Csr{};
+        if (!on || L.AP.rows == 0 || L.P.rows != L.AP.rows) continue;
+        Csr &Q = L.Q;
+        Q.rows = L.AP.rows;
+        Q.cols = L.AP.cols;
+        Q.nnz = L.AP.nnz;
+        Q.ptr.alloc(Q.rows + 1);
+        Q.col.alloc(Q.nnz);
+        Q.val.alloc(Q.nnz);
+        SPFD_CUDA(cudaMemcpyAsync(Q.ptr.get(), L.AP.ptr.get(), (Q.rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+        SPFD_CUDA(cudaMemcpyAsync(Q.col.get(), L.AP.col.get(), Q.nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        DevBuf<int> bad;
+        bad.alloc(1);
+        SPFD_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+        k_q_fill<<<grid_for(Q.rows, T), T, 0, s>>>(view(L.P), view(L.AP), L.odinv.get(), Q.val.get(), bad.get());
+        SPFD_LAUNCH_CHECK();
+        if (read1(bad.get(), s) != 0) { L.Q = Csr{}; continue; }
+        L.q_group = L.ap_group;
+        const std::string key = std::string("SPFD_GROUP_Q") + std::to_string(l);
+        if (const char *e = getenv(key.c_str())) L.q_group = atoi(e);
+    }
 }
 
 void build_rspan(Amg &h, cudaStream_t s) {
@@ -1366,6 +1416,7 @@ static Amg *build(Amg *h, Csr &&A0, const spfd_config &cfg, cudaStream_t s) {
     if (!(getenv("SPFD_MORTON") && std::string(getenv("SPFD_MORTON")) == "0") && h->structured && nl > 2)
         morton_level1(*h, s);
     build_rspan(*h, s);
+    build_q(*h, s);
     setup_mark("dense inverse + Morton", s);
     alloc_krylov(*h, h->lv[0].nvec, R);
     setup_mark("workspace", s);

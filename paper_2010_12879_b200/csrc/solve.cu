@@ -321,6 +321,7 @@ __global__ void k_agg_sum(const int64_t *mptr, const int32_t *mpos, int64_t n_ag
 // MODE 0: y = M x (aux: also od_aux * y);  1: y = r - M x;  2: y = r - M(odinv r);
 // MODE 3: y = x + odinv (r - M x);  4: y = odinv r + M e (prolongation, x=e)
 // MODE 5: y = base + M e (prolongation on a materialised smoother iterate)
+// MODE 6: y = odinv (r + base) + M e (coarse prolongation + post-smooth through Q, build_q)
 // L2 bulk prefetch of the column/value ranges of rows [row, row + n) (the
 // warp's next rows in the grid-stride loop).
 __device__ __forceinline__ void csr_prefetch(const CsrView &m, int64_t row, int n) {
@@ -394,6 +395,7 @@ __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__r
             else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(r, gr), sum);
             else if (MODE == 3) out = W::add(W::ld(x, gr), W::scale(od[gr], W::sub(W::ld(r, gr), sum)));
             else if (MODE == 4) out = W::add(W::scale(od[gr], W::ld(r, gr)), sum);
+            else if (MODE == 6) out = W::add(W::scale(od[gr], W::add(W::ld(r, gr), W::ld(base, gr))), sum);
             else out = W::add(W::ld(base, gr), sum);
             W::st(y, gr, out);
             if (MODE == 0 && aux) W::st(aux, gr, W::scale(od_aux[gr], out));
@@ -556,6 +558,7 @@ __global__ void __launch_bounds__(kCsrThreads) k_csr_wide(CsrView m, const doubl
             else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(r, gr), sum);
             else if (MODE == 3) out = W::add(W::ld(x, gr), W::scale(od[gr], W::sub(W::ld(r, gr), sum)));
             else if (MODE == 4) out = W::add(W::scale(od[gr], W::ld(r, gr)), sum);
+            else if (MODE == 6) out = W::add(W::scale(od[gr], W::add(W::ld(r, gr), W::ld(base, gr))), sum);
             else out = W::add(W::ld(base, gr), sum);
             W::st(y, gr, out);
             if (MODE == 0 && aux) W::st(aux, gr, W::scale(od_aux[gr], out));
@@ -1091,6 +1094,10 @@ void vcycle_level(Amg &h, int l, const double *r, double *z, cudaStream_t s);
 // fused coarse-level prolongation + post-smooth z = od r + P e + od (d - (A P) e)
 template <int R>
 void launch_pp(const Level &L, const double *e, const double *r, const double *d, double *z, cudaStream_t s) {
+    if (L.Q.rows) {  // z = od (r + d) + Q e (build_q)
+        launch_csr<R, 6, false>(L.Q, L.q_group, e, r, L.odinv.get(), d, z, nullptr, s);
+        return;
+    }
     const int G = std::min(L.ap_group, 32);
     const int grid = csr_grid(L.P.rows, G);
     const bool pf = csr_prefetch_enabled();
@@ -2332,7 +2339,8 @@ KernelBytes kernel_bytes(const Amg &h, double R) {
         const Level &L = h.lv[1];
         const double n1 = (double)L.n, n2 = (double)h.lv[2].n;
         k.l1_pre = csr_bytes(L.A) + n1 * 24.0 * R;                              // r, x0 -> d
-        if (L.AP.rows > 0) k.l1_pp = csr_bytes(L.P) + csr_bytes(L.AP) + n1 * (8.0 + 32.0 * R) + n2 * 8.0 * R;
+        if (L.Q.rows > 0) k.l1_pp = csr_bytes(L.Q) + n1 * (8.0 + 32.0 * R) + n2 * 8.0 * R;  // Q; od, r, d -> z; e
+        else if (L.AP.rows > 0) k.l1_pp = csr_bytes(L.P) + csr_bytes(L.AP) + n1 * (8.0 + 32.0 * R) + n2 * 8.0 * R;
     }
     return k;
 }
@@ -2346,7 +2354,8 @@ double coarse_vcycle_bytes(const Amg &h, int l0, double R) {
         const double n = (double)L.n, nc = (double)h.lv[l + 1].n;
         b += csr_bytes(L.A) + n * 24.0 * R;                         // pre-smooth residual
         b += csr_bytes(L.R) + n * 8.0 * R + nc * (8.0 + 16.0 * R);  // restriction (+ od r_c)
-        if (L.AP.rows > 0 && h.pre == 1 && h.post == 1) b += csr_bytes(L.P) + csr_bytes(L.AP) + n * (8.0 + 32.0 * R) + nc * 8.0 * R;
+        if (L.Q.rows > 0 && h.pre == 1 && h.post == 1) b += csr_bytes(L.Q) + n * (8.0 + 32.0 * R) + nc * 8.0 * R;
+        else if (L.AP.rows > 0 && h.pre == 1 && h.post == 1) b += csr_bytes(L.P) + csr_bytes(L.AP) + n * (8.0 + 32.0 * R) + nc * 8.0 * R;
         else b += csr_bytes(L.P) + csr_bytes(L.A) + n * (8.0 + 56.0 * R) + nc * 8.0 * R;
     }
     b += (double)h.nc * (double)h.nc * 8.0 + (double)h.nc * 16.0 * R;
