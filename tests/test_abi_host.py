@@ -144,3 +144,39 @@ def test_snapshot_fields_unit_norm():
     assert f.shape == (100, 3)
     assert np.allclose(np.linalg.norm(f, axis=1), 1e-6)
     assert np.array_equal(f, workloads.snapshot_fields(100))
+
+
+def _header_struct_fields(name):
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    end = re.search(r"\}\s*" + name + ";", text)
+    assert end, name
+    start = text.rindex("typedef struct {", 0, end.start())
+    body = text[start + len("typedef struct {"):end.start()]
+    fields = []
+    for line in body.split(";"):
+        line = line.strip()
+        if not line:
+            continue
+        fields.append(re.sub(r"\[.*\]", "", line.split()[-1]))
+    return fields
+
+
+@pytest.mark.parametrize("cname,pyname", [("spfd_config", "Config"), ("spfd_report", "Report"),
+                                          ("spfd_amg_info", "AmgInfo"), ("spfd_op_info", "OpInfo")])
+def test_ctypes_structs_match_header(cname, pyname):
+    """Every ctypes mirror of a header struct lists the same fields in the same
+    order (a drifted mirror would let the library write past the Python
+    object)."""
+    from paper_2010_12879_b200 import _lib
+    py = [f[0] for f in getattr(_lib, pyname)._fields_]
+    assert py == _header_struct_fields(cname)
+
+
+def test_integration_doc_config_stub_matches_header():
+    """INTEGRATION.md's reference-side ctypes stub declares spfd_config with
+    the header's fields (the maintainer copies it verbatim)."""
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = text[text.index("class Config(ctypes.Structure):"):text.index("class Report(ctypes.Structure):")]
+    names = re.findall(r'\("([a-z_0-9]+)",', block)
+    assert names == _header_struct_fields("spfd_config")
