@@ -63,6 +63,7 @@ const char *spfd_version(void) { return "spfd_b200 0.1 (sm_100a, fp64)"; }
 
 int spfd_op_create(const int64_t *h_dims, const double *h_spacing, const uint16_t *ids, const double *lut,
                    int64_t lut_len, int pin, void *stream, spfd_op_t *out) {
+    NvtxRange range_("spfd_op_create");
     return guarded([&] {
         SPFD_CHECK(out != nullptr && h_dims != nullptr && h_spacing != nullptr, SPFD_EINVAL, "null argument");
         Operator *op = op_create(h_dims, h_spacing, ids, lut, lut_len, pin, S(stream));
@@ -122,6 +123,7 @@ int spfd_stencil_apply(spfd_op_t h, const double *x, double *y, int nrhs, void *
 }
 
 int spfd_rhs_assemble(spfd_op_t h, const double *a, double *rhs, int nrhs, void *stream) {
+    NvtxRange range_("spfd_rhs_assemble");
     return guarded([&] {
         SPFD_CHECK(h && a && rhs && (nrhs == 1 || nrhs == 2), SPFD_EINVAL, "bad argument");
         Operator &op = *h->op;
@@ -156,6 +158,7 @@ int spfd_voxel_average(spfd_op_t h, const double *node, double *vox, int nrhs, v
 
 int spfd_efield_voxavg(spfd_op_t h, const double *a, const double *psi, double omega, double *vox, int nrhs,
                        void *stream) {
+    NvtxRange range_("spfd_efield_voxavg");
     return guarded([&] {
         SPFD_CHECK(h && a && psi && vox && (nrhs == 1 || nrhs == 2), SPFD_EINVAL, "bad argument");
         Operator &op = *h->op;
@@ -174,6 +177,7 @@ static void check_cfg(const spfd_config *c) {
 }
 
 int spfd_amg_setup_op(spfd_op_t h, const spfd_config *cfg, void *stream, spfd_amg_t *out) {
+    NvtxRange range_("spfd_amg_setup_op");
     return guarded([&] {
         SPFD_CHECK(h && out, SPFD_EINVAL, "null argument");
         check_cfg(cfg);
@@ -186,6 +190,7 @@ int spfd_amg_setup_op(spfd_op_t h, const spfd_config *cfg, void *stream, spfd_am
 
 int spfd_amg_setup_csr(int64_t n, int64_t nnz, const int64_t *indptr, const int32_t *indices, const double *data,
                        const spfd_config *cfg, void *stream, spfd_amg_t *out) {
+    NvtxRange range_("spfd_amg_setup_csr");
     return guarded([&] {
         SPFD_CHECK(out && indptr && (nnz == 0 || (indices && data)), SPFD_EINVAL, "null argument");
         check_cfg(cfg);
@@ -243,6 +248,7 @@ int spfd_amg_level_agg(spfd_amg_t h, int level, int32_t *agg, void *stream) {
 }
 
 int spfd_vcycle(spfd_amg_t h, const double *r, double *z, int nrhs, void *stream) {
+    NvtxRange range_("spfd_vcycle");
     return guarded([&] {
         SPFD_CHECK(h && r && z && nrhs >= 1 && nrhs <= h->amg->max_nrhs, SPFD_EINVAL, "bad argument");
         Amg &a = *h->amg;
@@ -254,6 +260,7 @@ int spfd_vcycle(spfd_amg_t h, const double *r, double *z, int nrhs, void *stream
 
 int spfd_solve(spfd_amg_t h, const double *b, double *x, int nrhs, const spfd_config *cfg, spfd_report *rep,
                double *h_trace, void *stream) {
+    NvtxRange range_("spfd_solve");
     return guarded([&] {
         SPFD_CHECK(h && b && x && rep && nrhs >= 1 && nrhs <= h->amg->max_nrhs, SPFD_EINVAL, "bad argument");
         check_cfg(cfg);
@@ -268,6 +275,7 @@ int spfd_solve(spfd_amg_t h, const double *b, double *x, int nrhs, const spfd_co
 
 int spfd_snapshot(spfd_op_t hop, spfd_amg_t h, const double *a, double omega, double *psi, double *vox, int nrhs,
                   const spfd_config *cfg, spfd_report *rep, void *stream) {
+    NvtxRange range_("spfd_snapshot");
     return guarded([&] {
         SPFD_CHECK(hop && h && a && vox && rep && h->op == hop->op, SPFD_EINVAL, "bad argument");
         SPFD_CHECK(nrhs >= 1 && nrhs <= h->amg->max_nrhs, SPFD_EINVAL, "nrhs exceeds the hierarchy workspace");
@@ -325,6 +333,7 @@ int spfd_comm_destroy(spfd_comm_t c) {
 }
 
 int spfd_amg_distribute(spfd_amg_t h, spfd_comm_t c, int64_t replicate_below, int64_t *h_range, void *stream) {
+    NvtxRange range_("spfd_amg_distribute");
     return guarded([&] {
         SPFD_CHECK(h && c && h_range, SPFD_EINVAL, "null argument");
         SPFD_CHECK(h->amg->dist == nullptr, SPFD_EINVAL, "hierarchy already distributed");
@@ -398,6 +407,7 @@ int spfd_field_destroy(spfd_field_t f) {
 
 int spfd_coil_field(int64_t n, const double *pts, int nseg, const double *verts, double scale, double *out,
                     void *stream) {
+    NvtxRange range_("spfd_coil_field");
     return guarded([&] {
         SPFD_CHECK(n >= 0 && nseg >= 1 && (n == 0 || (pts && verts && out)), SPFD_EINVAL, "bad argument");
         coil_field(n, pts, nseg, verts, scale, out, S(stream));
@@ -405,6 +415,7 @@ int spfd_coil_field(int64_t n, const double *pts, int nseg, const double *verts,
 }
 
 int spfd_field_interpolate(spfd_field_t f, const spfd_box *lattice, const double *b, double *flux, void *stream) {
+    NvtxRange range_("spfd_field_interpolate");
     return guarded([&] {
         SPFD_CHECK(f && b && flux, SPFD_EINVAL, "null argument");
         check_box(lattice, true);
@@ -420,6 +431,7 @@ int spfd_field_divergence(spfd_field_t f, const double *flux, double *div, void 
 }
 
 int spfd_field_clean(spfd_field_t f, const double *in, double *out, double tol, spfd_clean_info *info, void *stream) {
+    NvtxRange range_("spfd_field_clean");
     return guarded([&] {
         SPFD_CHECK(f && in && out && info, SPFD_EINVAL, "null argument");
         field_clean(*f->f, 1, in, out, tol, info, S(stream));
@@ -428,6 +440,7 @@ int spfd_field_clean(spfd_field_t f, const double *in, double *out, double tol, 
 
 int spfd_field_clean_batch(spfd_field_t f, int nrhs, const double *in, double *out, double tol,
                            spfd_clean_info *info, void *stream) {
+    NvtxRange range_("spfd_field_clean_batch");
     return guarded([&] {
         SPFD_CHECK(f && in && out && info, SPFD_EINVAL, "null argument");
         SPFD_CHECK(nrhs == 1 || nrhs == 2, SPFD_EINVAL, "nrhs must be 1 or 2");
@@ -436,6 +449,7 @@ int spfd_field_clean_batch(spfd_field_t f, int nrhs, const double *in, double *o
 }
 
 int spfd_field_gauge(spfd_field_t f, const double *flux, double *a, double tol, spfd_gauge_info *info, void *stream) {
+    NvtxRange range_("spfd_field_gauge");
     return guarded([&] {
         SPFD_CHECK(f && flux && a && info, SPFD_EINVAL, "null argument");
         field_gauge(*f->f, 0, flux, a, tol, info, S(stream));
@@ -444,6 +458,7 @@ int spfd_field_gauge(spfd_field_t f, const double *flux, double *a, double tol, 
 
 int spfd_field_gauge_tree(spfd_field_t f, int tree, const double *flux, double *a, double tol, spfd_gauge_info *info,
                           void *stream) {
+    NvtxRange range_("spfd_field_gauge_tree");
     return guarded([&] {
         SPFD_CHECK(f && flux && a && info, SPFD_EINVAL, "null argument");
         SPFD_CHECK(tree == 0 || tree == 1, SPFD_EINVAL, "tree must be 0 (comb) or 1 (bfs)");
@@ -461,6 +476,7 @@ int spfd_field_circulation(spfd_field_t f, const double *a, const double *flux, 
 int spfd_exposure_stats(const double *values, int64_t n, double scale, const int64_t *vox_index,
                         const uint16_t *ids_box, int32_t n_ids, double *scaled, int64_t *h_count, double *h_mean,
                         double *h_max, double *h_p99, double *h_global, void *stream) {
+    NvtxRange range_("spfd_exposure_stats");
     return guarded([&] {
         SPFD_CHECK(values && vox_index && ids_box && scaled && h_count && h_mean && h_max && h_p99 && h_global,
                    SPFD_EINVAL, "null argument");

@@ -9,8 +9,18 @@
 #include <vector>
 
 #include "../../include/spfd_b200.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace spfd {
+
+// NVTX range over a C-ABI call (visible in Nsight Systems / ncu --nvtx)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 
 // ---------------------------------------------------------------- errors --
 struct Error : std::runtime_error {
