@@ -61,6 +61,7 @@ struct Dist {
     ListHalo hu, he;
     std::vector<DistLevel> lv;             // index = level (entry 0 unused)
     DevBuf<double> gsend, grecv;           // allgather scratch
+    DevBuf<double> hgather;                // distributed FGMRES: gathered Hessenberg partials
     int64_t dof_b = 0, dof_e = 0, vox_b = 0, vox_e = 0;
     int64_t vrow_b = 0, vrow_e = 0;
     // interior positions [ib, ie): stencil neighbours all owned -> computed on

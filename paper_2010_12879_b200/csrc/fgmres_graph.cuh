@@ -165,12 +165,12 @@ void fg_step(Amg &h, int j, int m, FgDev *st, double *trace, cudaStream_t s) {
     level0_apply<R>(h, 0, false, zj, nullptr, w, s);
     for (int i0 = 0; i0 <= j; i0 += NI2) {
         const int ni = std::min(NI2, j + 1 - i0);
-        k_mdot2<R, NI2><<<nparts, 256, 0, s>>>(n, Vb, i0, ni, w, vj, h.partials.get());
+        k_mdot2<R, NI2><<<nparts, 256, 0, s>>>(n, n, Vb, i0, ni, w, vj, h.partials.get());
         k_mfinal<<<2 * NI2 * R, 256, 0, s>>>(h.partials.get(), nparts, 2 * NI2 * R, sc + SH1 + 2 * i0 * R);
         SPFD_LAUNCH_CHECK();
     }
     k_gram_step<R, NI2><<<1, 256, 0, s>>>(sc + SH1, j, m, h.fg_gram.get(), sc + SH2);
-    k_maxpy<R><<<G, 256, 0, s>>>(n, Vb, j + 1, sc + SH2, w);
+    k_maxpy<R><<<G, 256, 0, s>>>(n, n, Vb, j + 1, sc + SH2, w);
     SPFD_LAUNCH_CHECK();
     dot<R>(h, n, w, w, S_TMP, F_STORE, s);
     k_fg_givens<R><<<1, 32, 0, s>>>(st, sc + SH2, sc + S_TMP, j, sc + SMUL, trace);
@@ -244,7 +244,7 @@ bool fg_graph_build(Amg &h, int m) {
             }
         }
         k_fg_lsq<R><<<1, 32, 0, s>>>(st, h.fg_y.get(), h.fg_jc.get());
-        k_combine_r<R><<<G, 256, 0, s>>>(n, m, h.fg_jc.get(), h.fg_y.get(), h.fg_prec.get(), x);
+        k_combine_r<R><<<G, 256, 0, s>>>(n, n, m, h.fg_jc.get(), h.fg_y.get(), h.fg_prec.get(), x);
         SPFD_LAUNCH_CHECK();
     } catch (const std::exception &e) {
         why = e.what();

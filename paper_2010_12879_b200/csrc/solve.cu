@@ -1900,11 +1900,12 @@ __global__ void __launch_bounds__(256) k_mdot(int64_t n, const double *Vb, int i
 }
 
 // Dual block dot: for k < ni, <V_{i0+k}, w> and <V_{i0+k}, v> (v = the
-// newest basis vector) in one pass over the basis block.  partials layout
-// [cta][2][NI][R].
+// newest basis vector) in one pass over the basis block; n positions, basis
+// vectors ld positions apart (ld > n: a rank's own range of full-length
+// vectors).  partials layout [cta][2][NI][R].
 template <int R, int NI>
-__global__ void __launch_bounds__(256) k_mdot2(int64_t n, const double *Vb, int i0, int ni, const double *w,
-                                               const double *v, double *partials) {
+__global__ void __launch_bounds__(256) k_mdot2(int64_t n, int64_t ld, const double *Vb, int i0, int ni,
+                                               const double *w, const double *v, double *partials) {
     using W = V<R>;
     __shared__ double red[32 * 2 * NI * R];
     double acc[2 * NI * R];
@@ -1915,7 +1916,7 @@ __global__ void __launch_bounds__(256) k_mdot2(int64_t n, const double *Vb, int 
 #pragma unroll
         for (int k = 0; k < NI; ++k) {
             if (k < ni) {
-                const typename W::T b = W::ld(Vb + (int64_t)(i0 + k) * n * R, p);
+                const typename W::T b = W::ld(Vb + (int64_t)(i0 + k) * ld * R, p);
 #pragma unroll
                 for (int c = 0; c < R; ++c) {
                     acc[k * R + c] = fma(W::comp(b, c), W::comp(wv, c), acc[k * R + c]);
@@ -1967,9 +1968,10 @@ __global__ void __launch_bounds__(256) k_mfinal(const double *partials, int nblo
     if (threadIdx.x == 0) out[k] = s[0];
 }
 
-// w -= sum_{i < nv} h[i] V_i  (h: [nv][R] on the device, applied in order i)
+// w -= sum_{i < nv} h[i] V_i  (h: [nv][R] on the device, applied in order i;
+// basis vectors ld positions apart)
 template <int R>
-__global__ void k_maxpy(int64_t n, const double *Vb, int nv, const double *hv, double *w) {
+__global__ void k_maxpy(int64_t n, int64_t ld, const double *Vb, int nv, const double *hv, double *w) {
     using W = V<R>;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         typename W::T acc = W::ld(w, p);
@@ -1977,7 +1979,7 @@ __global__ void k_maxpy(int64_t n, const double *Vb, int nv, const double *hv, d
             double nh[R];
 #pragma unroll
             for (int c = 0; c < R; ++c) nh[c] = -hv[i * R + c];
-            acc = vfma<R>(nh, W::ld(Vb + (int64_t)i * n * R, p), acc);
+            acc = vfma<R>(nh, W::ld(Vb + (int64_t)i * ld * R, p), acc);
         }
         W::st(w, p, acc);
     }
@@ -1998,14 +2000,15 @@ __global__ void k_scale_r(int64_t n, const double *mult, const double *x, double
     }
 }
 
-// x[:, c] += sum_{k < jc[c]} Z_k[:, c] y[c][k]
+// x[:, c] += sum_{k < jc[c]} Z_k[:, c] y[c][k]  (Z_k ld positions apart)
 template <int R>
-__global__ void k_combine_r(int64_t n, int m, const int *jc, const double *y, const double *Zb, double *x) {
+__global__ void k_combine_r(int64_t n, int64_t ld, int m, const int *jc, const double *y, const double *Zb,
+                            double *x) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
         for (int c = 0; c < R; ++c) {
             double acc = 0.0;
-            for (int k = 0; k < jc[c]; ++k) acc += Zb[((int64_t)k * n + p) * R + c] * y[c * m + k];
+            for (int k = 0; k < jc[c]; ++k) acc += Zb[((int64_t)k * ld + p) * R + c] * y[c * m + k];
             x[p * R + c] += acc;
         }
     }
@@ -2099,13 +2102,13 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
             constexpr int NI2 = 4;
             for (int i0 = 0; i0 <= j; i0 += NI2) {
                 const int ni = std::min(NI2, j + 1 - i0);
-                k_mdot2<R, NI2><<<nparts, 256, 0, s>>>(n, Vb, i0, ni, w, vj, h.partials.get());
+                k_mdot2<R, NI2><<<nparts, 256, 0, s>>>(n, n, Vb, i0, ni, w, vj, h.partials.get());
                 k_mfinal<<<2 * NI2 * R, 256, 0, s>>>(h.partials.get(), nparts, 2 * NI2 * R, sc + SH1 + 2 * i0 * R);
                 SPFD_LAUNCH_CHECK();
             }
             // the re-orthogonalisation coefficients and the Gram column on the device
             k_gram_step<R, NI2><<<1, 256, 0, s>>>(sc + SH1, j, m, gram.get(), sc + SH2);
-            k_maxpy<R><<<G, 256, 0, s>>>(n, Vb, j + 1, sc + SH2, w);
+            k_maxpy<R><<<G, 256, 0, s>>>(n, n, Vb, j + 1, sc + SH2, w);
             SPFD_LAUNCH_CHECK();
             dot<R>(h, n, w, w, S_TMP, F_STORE, s);
             std::vector<double> hcol((size_t)(j + 1) * R);
@@ -2167,7 +2170,7 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
         }
         SPFD_CUDA(cudaMemcpyAsync(ydev.get(), y.data(), y.size() * sizeof(double), cudaMemcpyHostToDevice, s));
         SPFD_CUDA(cudaMemcpyAsync(jcdev.get(), jc, R * sizeof(int), cudaMemcpyHostToDevice, s));
-        k_combine_r<R><<<G, 256, 0, s>>>(n, m, jcdev.get(), ydev.get(), Zb, x);
+        k_combine_r<R><<<G, 256, 0, s>>>(n, n, m, jcdev.get(), ydev.get(), Zb, x);
         SPFD_LAUNCH_CHECK();
     }
     // true residual at exit (linsolve.py:296-298)
@@ -2184,6 +2187,184 @@ spfd_report fgmres_batch(Amg &h, const double *b, double *x, const spfd_config &
         if (!(rel <= cfg.rel_tol)) rep.converged = 0;
         itmax = std::max(itmax, its_c[c]);
     }
+    rep.iterations = itmax;
+    return rep;
+}
+
+// Distributed FGMRES(m) (linsolve.py:200-298) over the z-slab ranks: the
+// batched Arnoldi process of fgmres_batch on each rank's own positions of
+// full-length vectors.  The V-cycle and the operator are the distributed ones
+// (halo exchange inside); every inner product -- the dual block dot of the
+// Gram-corrected CGS2 and the norms -- is a per-rank partial, allgathered and
+// summed in rank order, so every rank holds the same Hessenberg column and
+// takes the same Givens / restart decisions on the host.
+template <int R>
+spfd_report fgmres_dist(Amg &h, const double *b, double *x, const spfd_config &cfg, double *h_trace,
+                        cudaStream_t s) {
+    Dist &D = *h.dist;
+    spfd_report rep{};
+    const int64_t n = h.lv[0].nvec;
+    const int64_t no = D.pe - D.pb, off = D.pb * R;
+    const int m = cfg.restart;
+    SPFD_CHECK(m >= 1 && m <= 31, SPFD_EINVAL, "restart must be in [1, 31] for the distributed FGMRES");
+    if (h.fg_m < m || h.fg_R < R) {
+        h.fg_basis.alloc((int64_t)(m + 1) * n * R);
+        h.fg_prec.alloc((int64_t)m * n * R);
+        h.fg_m = m;
+        h.fg_R = R;
+    }
+    constexpr int NI2 = 4;
+    const int raw_max = (m + NI2) / NI2 * 2 * NI2 * R;  // dual-dot values of the largest column
+    if ((int64_t)D.hgather.n < (int64_t)raw_max * D.size) D.hgather.alloc((int64_t)raw_max * D.size);
+    double *Vb = h.fg_basis.get(), *Zb = h.fg_prec.get();
+    double *w = h.kq.get(), *r = h.kr.get();
+    double *sc = h.scal.get();
+    const int G = grid_for(no, 256, 148 * 16);
+    const int SH1 = S_H, SH2 = S_H + 128, SMUL = S_TMP + 2;
+    SPFD_CUDA(cudaMemsetAsync(x, 0, n * R * sizeof(double), s));
+    SPFD_CUDA(cudaMemsetAsync(sc, 0, S_END * sizeof(double), s));
+    dot_dist<R>(h, b, b, S_BB, F_STORE, s);
+    double hb[R];
+    SPFD_CUDA(cudaMemcpyAsync(hb, sc + S_BB, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    double bnorm[R];
+    bool done[R], all = true;
+    for (int c = 0; c < R; ++c) {
+        bnorm[c] = std::sqrt(hb[c]);
+        if (!std::isfinite(bnorm[c])) { rep.status = SPFD_ENONFINITE; return rep; }
+        done[c] = bnorm[c] == 0.0;
+        all = all && done[c];
+    }
+    if (all) { rep.converged = 1; return rep; }
+    std::vector<double> H[R], cs[R], sn[R], g[R];
+    fg_small_alloc(h);
+    for (int c = 0; c < R; ++c) {
+        H[c].assign((size_t)(m + 1) * m, 0.0);
+        cs[c].assign(m, 0.0); sn[c].assign(m, 0.0); g[c].assign(m + 1, 0.0);
+    }
+    int its = 0, its_c[R];
+    for (int c = 0; c < R; ++c) its_c[c] = 0;
+    while (its < cfg.max_iters) {
+        apply_dist<R>(h, 1, false, x, b, r, s);  // r = b - A x (own range)
+        dot_dist<R>(h, r, r, S_TMP, F_STORE, s);
+        double rr[R];
+        SPFD_CUDA(cudaMemcpyAsync(rr, sc + S_TMP, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPFD_CUDA(cudaStreamSynchronize(s));
+        bool active[R], any = false;
+        double mult[R];
+        for (int c = 0; c < R; ++c) {
+            const double beta = std::sqrt(rr[c]);
+            if ((bnorm[c] > 0 ? beta / bnorm[c] : 0.0) <= cfg.rel_tol) done[c] = true;
+            active[c] = !done[c];
+            any = any || active[c];
+            std::fill(H[c].begin(), H[c].end(), 0.0);
+            std::fill(g[c].begin(), g[c].end(), 0.0);
+            g[c][0] = beta;
+            mult[c] = active[c] ? 1.0 / beta : 0.0;
+        }
+        if (!any) break;
+        SPFD_CUDA(cudaMemsetAsync(h.fg_gram.get(), 0, (size_t)R * (m + 1) * (m + 1) * sizeof(double), s));
+        SPFD_CUDA(cudaMemcpyAsync(sc + SMUL, mult, R * sizeof(double), cudaMemcpyHostToDevice, s));
+        k_scale_r<R><<<G, 256, 0, s>>>(no, sc + SMUL, r + off, Vb + off);
+        int jc[R];
+        for (int c = 0; c < R; ++c) jc[c] = 0;
+        int j = 0;
+        while (j < m && its < cfg.max_iters) {
+            double *vj = Vb + (int64_t)j * n * R, *zj = Zb + (int64_t)j * n * R;
+            vcycle_dist_fine<R>(h, vj, zj, s);
+            apply_dist<R>(h, 0, false, zj, nullptr, w, s);
+            // per-rank dual block dots into SH2, gathered and summed in rank
+            // order into SH1 (the layout k_gram_step reads)
+            const int nblk = j / NI2 + 1, nraw = nblk * 2 * NI2 * R;
+            for (int i0 = 0; i0 <= j; i0 += NI2) {
+                const int ni = std::min(NI2, j + 1 - i0);
+                k_mdot2<R, NI2><<<kDotGrid, 256, 0, s>>>(no, n, Vb + off, i0, ni, w + off, vj + off,
+                                                        h.partials.get());
+                k_mfinal<<<2 * NI2 * R, 256, 0, s>>>(h.partials.get(), kDotGrid, 2 * NI2 * R, sc + SH2 + 2 * i0 * R);
+                SPFD_LAUNCH_CHECK();
+            }
+            D.comm->allgather(sc + SH2, D.hgather.get(), nraw * sizeof(double), s);
+            k_rank_sum<<<1, 256, 0, s>>>(D.hgather.get(), D.size, nraw, 1, sc + SH1, nullptr, nullptr);
+            k_gram_step<R, NI2><<<1, 256, 0, s>>>(sc + SH1, j, m, h.fg_gram.get(), sc + SH2);
+            k_maxpy<R><<<G, 256, 0, s>>>(no, n, Vb + off, j + 1, sc + SH2, w + off);
+            SPFD_LAUNCH_CHECK();
+            dot_dist<R>(h, w, w, S_TMP, F_STORE, s);
+            std::vector<double> hcol((size_t)(j + 1) * R);
+            double nn[R];
+            SPFD_CUDA(cudaMemcpyAsync(hcol.data(), sc + SH2, hcol.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SPFD_CUDA(cudaMemcpyAsync(nn, sc + S_TMP, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+            SPFD_CUDA(cudaStreamSynchronize(s));
+            ++its;
+            bool more = false;
+            for (int c = 0; c < R; ++c) {
+                if (!active[c]) { mult[c] = 0.0; continue; }
+                ++its_c[c];
+                const double hn = std::sqrt(nn[c]);
+                if (!std::isfinite(hn)) { rep.status = SPFD_ENONFINITE; rep.iterations = its; return rep; }
+                auto &Hc = H[c];
+                for (int i = 0; i <= j; ++i) Hc[(size_t)i * m + j] = hcol[(size_t)i * R + c];
+                for (int i = 0; i < j; ++i) {
+                    const double t1 = cs[c][i] * Hc[(size_t)i * m + j] + sn[c][i] * Hc[(size_t)(i + 1) * m + j];
+                    const double t2 = -sn[c][i] * Hc[(size_t)i * m + j] + cs[c][i] * Hc[(size_t)(i + 1) * m + j];
+                    Hc[(size_t)i * m + j] = t1;
+                    Hc[(size_t)(i + 1) * m + j] = t2;
+                }
+                const double den = std::hypot(Hc[(size_t)j * m + j], hn);
+                if (den == 0.0) { cs[c][j] = 1.0; sn[c][j] = 0.0; }
+                else { cs[c][j] = Hc[(size_t)j * m + j] / den; sn[c][j] = hn / den; }
+                Hc[(size_t)j * m + j] = cs[c][j] * Hc[(size_t)j * m + j] + sn[c][j] * hn;
+                g[c][j + 1] = -sn[c][j] * g[c][j];
+                g[c][j] = cs[c][j] * g[c][j];
+                jc[c] = j + 1;
+                const double est = std::fabs(g[c][j + 1]) / bnorm[c];
+                if (h_trace && its <= cfg.max_iters) h_trace[(int64_t)(its - 1) * R + c] = est;
+                if (hn == 0.0 || est <= cfg.rel_tol) {
+                    active[c] = false;
+                    mult[c] = 0.0;
+                } else {
+                    mult[c] = 1.0 / hn;
+                    more = true;
+                }
+            }
+            ++j;
+            if (!more) break;
+            if (j < m) {
+                SPFD_CUDA(cudaMemcpyAsync(sc + SMUL, mult, R * sizeof(double), cudaMemcpyHostToDevice, s));
+                k_scale_r<R><<<G, 256, 0, s>>>(no, sc + SMUL, w + off, Vb + (int64_t)j * n * R + off);
+                SPFD_LAUNCH_CHECK();
+            }
+        }
+        std::vector<double> y((size_t)R * m, 0.0);
+        for (int c = 0; c < R; ++c) {
+            const int jj = jc[c];
+            for (int i = jj - 1; i >= 0; --i) {
+                double acc = g[c][i];
+                for (int k = i + 1; k < jj; ++k) acc -= H[c][(size_t)i * m + k] * y[(size_t)c * m + k];
+                y[(size_t)c * m + i] = acc / H[c][(size_t)i * m + i];
+            }
+            for (int i = 0; i < jj; ++i)
+                if (!std::isfinite(y[(size_t)c * m + i])) { rep.status = SPFD_ENONFINITE; rep.iterations = its; return rep; }
+        }
+        SPFD_CUDA(cudaMemcpyAsync(h.fg_y.get(), y.data(), y.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        SPFD_CUDA(cudaMemcpyAsync(h.fg_jc.get(), jc, R * sizeof(int), cudaMemcpyHostToDevice, s));
+        k_combine_r<R><<<G, 256, 0, s>>>(no, n, m, h.fg_jc.get(), h.fg_y.get(), Zb + off, x + off);
+        SPFD_LAUNCH_CHECK();
+    }
+    apply_dist<R>(h, 1, false, x, b, r, s);
+    dot_dist<R>(h, r, r, S_TMP, F_STORE, s);
+    double rr[R];
+    SPFD_CUDA(cudaMemcpyAsync(rr, sc + S_TMP, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPFD_CUDA(cudaStreamSynchronize(s));
+    rep.converged = 1;
+    int itmax = 0;
+    for (int c = 0; c < R; ++c) {
+        const double rel = bnorm[c] > 0 ? std::sqrt(rr[c]) / bnorm[c] : 0.0;
+        rep.rel_residual[c] = rel;
+        if (!(rel <= cfg.rel_tol)) rep.converged = 0;
+        itmax = std::max(itmax, its_c[c]);
+    }
+    // leave x valid on the halo planes too (the E-field reads one plane beyond)
+    range_exchange(D, x, R, s);
     rep.iterations = itmax;
     return rep;
 }
@@ -2480,9 +2661,9 @@ spfd_report krylov_solve(Amg &h, const double *b, double *x, int nrhs, const spf
     SPFD_CUDA(cudaEventCreate(&e1));
     SPFD_CUDA(cudaEventRecord(e0, s));
     spfd_report rep{};
-    SPFD_CHECK(!(h.dist && cfg.method == SPFD_METHOD_FGMRES), SPFD_EINVAL,
-               "the distributed solve supports PCG only");
-    if (cfg.method == SPFD_METHOD_FGMRES) {
+    if (h.dist && cfg.method == SPFD_METHOD_FGMRES) {
+        rep = nrhs == 1 ? fgmres_dist<1>(h, b, x, cfg, h_trace, s) : fgmres_dist<2>(h, b, x, cfg, h_trace, s);
+    } else if (cfg.method == SPFD_METHOD_FGMRES) {
         int64_t n = h.lv[0].nvec;
         // block (Gram-corrected CGS2) Arnoldi unless disabled or the restart
         // exceeds its scalar workspace; else the reference's MGS per rhs

@@ -68,7 +68,7 @@ def test_slab_balancing_rule():
         assert max(counts) - min(counts) <= 50  # balanced to one plane
 
 
-def _solve_worker(rank, size, port, out, name, replicate_below, transport="host"):
+def _solve_worker(rank, size, port, out, name, replicate_below, transport="host", method="pcg"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from paper_2010_12879_b200 import Session, SolveConfig, workloads
@@ -81,7 +81,7 @@ def _solve_worker(rank, size, port, out, name, replicate_below, transport="host"
         torch.cuda.set_device(0)
         _init(rank, size, port)
     w = getattr(workloads, name)()
-    sess = Session(w.model, w.frequency_hz, SolveConfig(rel_tol=1e-10))
+    sess = Session(w.model, w.frequency_hz, SolveConfig(rel_tol=1e-10, method=method))
     a = torch.from_numpy(w.a).cuda()
     comm = Communicator.host() if transport == "host" else Communicator.nccl()
     sess.distribute(comm, replicate_below=replicate_below)
@@ -100,15 +100,19 @@ def _small_layered():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("replicate_below", [1000, 10**9])
-def test_distributed_snapshot_matches_single_gpu(replicate_below):
+@pytest.mark.parametrize("replicate_below,method", [(1000, "pcg"), (10**9, "pcg"), (1000, "fgmres")])
+def test_distributed_snapshot_matches_single_gpu(replicate_below, method):
+    """Two ranks reproduce the single-GPU snapshot; for FGMRES the batched
+    Arnoldi process runs on the ranks' own positions with rank-ordered
+    reductions of every inner product (fgmres_dist)."""
     from paper_2010_12879_b200 import Session, SolveConfig, workloads
     w = workloads.c2(48)
-    sess = Session(w.model, w.frequency_hz, SolveConfig(rel_tol=1e-10))
+    sess = Session(w.model, w.frequency_hz, SolveConfig(rel_tol=1e-10, method=method))
     vox, rep, psi = sess.snapshot(torch.from_numpy(w.a).cuda(), keep_psi=True)
     vox, psi = vox.cpu().numpy(), psi.cpu().numpy()
     with tempfile.TemporaryDirectory() as out:
-        mp.spawn(_solve_worker, args=(2, _port(), out, "c2_small", replicate_below), nprocs=2, join=True)
+        mp.spawn(_solve_worker, args=(2, _port(), out, "c2_small", replicate_below, "host", method), nprocs=2,
+                 join=True)
         parts = [torch.load(os.path.join(out, f"s{r}.pt")) for r in range(2)]
     assert parts[0]["vr"][1] == parts[1]["vr"][0] and parts[1]["vr"][1] == vox.shape[1]
     assert parts[0]["dr"][1] == parts[1]["dr"][0] and parts[1]["dr"][1] == psi.shape[1]
