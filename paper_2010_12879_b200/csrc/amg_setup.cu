@@ -617,20 +617,6 @@ void dense_inverse(const Csr &a, DevBuf<double> &inv, cudaStream_t s) {
 }
 
 // ------------------------------------------------- structured level 0 ----
-__global__ void k_span_rowcnt(const int32_t *pos_to_dof, int64_t L, const int64_t *pptr, int64_t *cnt) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        int d = pos_to_dof[p];
-        cnt[p] = d >= 0 ? pptr[d + 1] - pptr[d] : 0;
-    }
-}
-
-__global__ void k_map_cols(const int32_t *col, int64_t nnz, const int32_t *dof_to_pos, int32_t *out) {
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
-         q += (int64_t)gridDim.x * blockDim.x)
-        out[q] = dof_to_pos[col[q]];
-}
-
 __global__ void k_dofs_to_span_1(const int32_t *pos_to_dof, int64_t L, const double *in, double *out) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < L;
          p += (int64_t)gridDim.x * blockDim.x) {

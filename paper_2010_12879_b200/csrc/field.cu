@@ -85,44 +85,12 @@ __device__ inline AxisParam axis_param(double c, double origin, double spacing, 
     return {i0, __dsub_rn(u, (double)i0), 1};
 }
 
-// fluxes of the faces with normal `a` (_trilinear + interpolate_to_faces,
-// field_source.py:235-272): out = sum over the 8 corners in (dx, dy, dz)
-// order of ((wx*wy)*wz)*corner, then times the face area.
-__global__ void k_interp_faces(Box g, Box lat, int a, const double *__restrict__ b, double area,
-                               double *__restrict__ flux) {
-    int64_t d[3] = {g.n[0], g.n[1], g.n[2]};
-    d[a] += 1;
-    const int64_t nf = d[0] * d[1] * d[2];
-    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = f % d[0], j = (f / d[0]) % d[1], k = f / (d[0] * d[1]);
-        const AxisParam px = axis_param(face_coord(g, a, 0, i), lat.o[0], lat.h[0], lat.n[0]);
-        const AxisParam py = axis_param(face_coord(g, a, 1, j), lat.o[1], lat.h[1], lat.n[1]);
-        const AxisParam pz = axis_param(face_coord(g, a, 2, k), lat.o[2], lat.h[2], lat.n[2]);
-        double out = 0.0;
-#pragma unroll
-        for (int dx = 0; dx < 2; ++dx) {
-            const double wx = dx ? px.t : __dsub_rn(1.0, px.t);
-#pragma unroll
-            for (int dy = 0; dy < 2; ++dy) {
-                const double wy = dy ? py.t : __dsub_rn(1.0, py.t);
-                const double wxy = __dmul_rn(wx, wy);
-#pragma unroll
-                for (int dz = 0; dz < 2; ++dz) {
-                    const double wz = dz ? pz.t : __dsub_rn(1.0, pz.t);
-                    const int64_t p = (px.i0 + dx * px.s) + lat.n[0] * ((py.i0 + dy * py.s) + lat.n[1] * (pz.i0 + dz * pz.s));
-                    out = __dadd_rn(out, __dmul_rn(__dmul_rn(wxy, wz), b[3 * p + a]));
-                }
-            }
-        }
-        flux[f] = __dmul_rn(out, area);
-    }
-}
-
 // The trilinear parameters of a face depend on one coordinate each, so they
 // are tabulated per axis (k_axis_params: d0 + d1 + d2 entries) and the face
-// kernel walks face rows (j, k) with threads along i -- the same values and
-// the same product order as k_interp_faces, without its per-face divisions
-// and 64-bit div/mod.
+// kernel walks face rows (j, k) with threads along i (_trilinear +
+// interpolate_to_faces, field_source.py:235-272: the sum over the 8 corners
+// in (dx, dy, dz) order of ((wx*wy)*wz)*corner, times the face area), without
+// per-face divisions or 64-bit div/mod.
 __global__ void k_axis_params(Box g, Box lat, int a, AxisParam *tab) {
     int64_t d[3] = {g.n[0], g.n[1], g.n[2]};
     d[a] += 1;

@@ -767,7 +767,6 @@ void op_rhs_span(const Operator &op, const double *a, double *rhs_span, int nrhs
 // rhs handled by the caller through interleaved span input).
 __global__ void k_edge_volt(const int4 *rows, EdgeIdx e, int64_t E, const double *a,
                             const double *psi_span, int nrhs, double omega, double *vout) {
-    int64_t ex_n = (int64_t)e.nx * e.NY * (e.nz + 1);
     for (int64_t ed = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ed < E;
          ed += (int64_t)gridDim.x * blockDim.x) {
         int axis;
@@ -776,7 +775,6 @@ __global__ void k_edge_volt(const int4 *rows, EdgeIdx e, int64_t E, const double
         if (ed < e.eoff1) { axis = 0; loc = ed; dx = e.nx; }
         else if (ed < e.eoff2) { axis = 1; loc = ed - e.eoff1; dx = e.NX; }
         else { axis = 2; loc = ed - e.eoff2; dx = e.NX; }
-        (void)ex_n;
         int i = (int)(loc % dx);
         int64_t t = loc / dx;
         int dy = axis == 1 ? e.ny : e.NY;

@@ -256,6 +256,11 @@ __device__ __forceinline__ void span_tile(const SpanView &v, const SpanArgs &a, 
 #ifndef SPFD_SPAN_MINB
 #define SPFD_SPAN_MINB 6
 #endif
+// the SpMV + dot instance spills 8 bytes at 6 CTAs per SM; 5 is spill-free
+// but measured 2% slower at C3 (125.4 vs 122.5 us), so both stay at 6
+#ifndef SPFD_SPMV_MINB
+#define SPFD_SPMV_MINB 6
+#endif
 template <int R, int MODE, bool DOT, bool RANGED = false, bool PF = false, int MINB = SPFD_SPAN_MINB>
 __global__ void __launch_bounds__(kSpanThreads, MINB) k_span(SpanView v, SpanArgs a) {
     __shared__ double red[32 * R];
@@ -937,7 +942,7 @@ void alloc_krylov(Amg &h, int64_t nvec0, int R) {
     int64_t np = kDotGrid;
     if (h.structured) np = std::max<int64_t>(np, h.op->n_tiles);
     np = std::max<int64_t>(np, 148 * 16);
-    np = std::max<int64_t>(np, (int64_t)kDotGrid * 8);  // batched FGMRES block dots (k_mdot, 8 vectors)
+    np = std::max<int64_t>(np, (int64_t)kDotGrid * 8);  // batched FGMRES dual block dots (k_mdot2: 2 x 4 x R)
     h.partials.alloc(np * 2 + 64);
     h.scal.alloc(S_END);
     SPFD_CUDA(cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking));
@@ -1021,9 +1026,10 @@ int launch_fine(const Operator &op, const SpanArgs &a_in, cudaStream_t s) {
         return g;
     }
     int g = (int)op.n_tiles;
+    constexpr int MB = (MODE == 0 && DOT) ? SPFD_SPMV_MINB : SPFD_SPAN_MINB;
     if (g > 0) {
-        if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, false, true><<<g, kSpanThreads, 0, s>>>(v, a);
-        else k_span<R, MODE, DOT><<<g, kSpanThreads, 0, s>>>(v, a);
+        if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, false, true, MB><<<g, kSpanThreads, 0, s>>>(v, a);
+        else k_span<R, MODE, DOT, false, false, MB><<<g, kSpanThreads, 0, s>>>(v, a);
     }
     SPFD_LAUNCH_CHECK();
     return g;
@@ -1122,8 +1128,6 @@ template <int R>
 int vcycle_fine_mf(Amg &h, const double *r, double *z, cudaStream_t s) {
     Level &L = h.lv[0];
     Level &C = h.lv[1];
-    SpanView v = span_view(*h.op);
-    const int g = (int)h.op->n_tiles;
     double *d = L.vd.get(), *t = L.vt.get(), *u = L.vr.get();
     const size_t bytes = (size_t)L.nvec * R * sizeof(double);
     const double *od = L.odinv.get();
@@ -1866,39 +1870,12 @@ __global__ void k_combine(int64_t n, int j, const double *y, const double *zb, d
 // ---- batched FGMRES (both rhs of a pair in one Arnoldi process) ----------
 // Per Arnoldi step: one V-cycle and one SpMV for both rhs (double2), then
 // classical Gram-Schmidt with one re-orthogonalisation (CGS2) as block
-// kernels -- k_mdot (all <V_i, w> for up to 8 basis vectors per launch,
-// fixed-order per-CTA partials), k_mfinal, k_maxpy (w -= sum_i h_i V_i in
-// order i) -- instead of the reference's MGS, which needs 3(j+1) launches
+// kernels -- k_mdot2 (<V_i, w> and <V_i, v_j> for up to 4 basis vectors per
+// launch, fixed-order per-CTA partials), k_mfinal, k_gram_step, k_maxpy
+// (w -= sum_i h_i V_i in order i) -- instead of the reference's MGS, which needs 3(j+1) launches
 // per step and re-reads w for every basis vector.  Givens rotations, the
 // least-squares solve and all convergence decisions stay per rhs on the
 // host, as in fgmres1 (linsolve.py:200-298 semantics per rhs).
-constexpr int kMdotNI = 8;
-
-template <int R, int NI>
-__global__ void __launch_bounds__(256) k_mdot(int64_t n, const double *Vb, int i0, int ni, const double *w,
-                                              double *partials) {
-    using W = V<R>;
-    __shared__ double red[32 * NI * R];
-    double acc[NI * R];
-#pragma unroll
-    for (int k = 0; k < NI * R; ++k) acc[k] = 0.0;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-        const typename W::T wv = W::ld(w, p);
-#pragma unroll
-        for (int k = 0; k < NI; ++k) {
-            if (k < ni) {
-                const typename W::T v = W::ld(Vb + (int64_t)(i0 + k) * n * R, p);
-#pragma unroll
-                for (int c = 0; c < R; ++c) acc[k * R + c] = fma(W::comp(v, c), W::comp(wv, c), acc[k * R + c]);
-            }
-        }
-    }
-    block_sum<NI * R>(acc, red);
-    if (threadIdx.x == 0)
-#pragma unroll
-        for (int k = 0; k < NI * R; ++k) partials[(int64_t)blockIdx.x * NI * R + k] = acc[k];
-}
-
 // Dual block dot: for k < ni, <V_{i0+k}, w> and <V_{i0+k}, v> (v = the
 // newest basis vector) in one pass over the basis block; n positions, basis
 // vectors ld positions apart (ld > n: a rank's own range of full-length
