@@ -21,9 +21,19 @@ static void setup_mark(const char *what, cudaStream_t s) {
     static const bool on = getenv("SPFD_SETUP_TRACE") != nullptr;
     if (!on) return;
     static auto last = std::chrono::steady_clock::now();
+    static cudaEvent_t ev_last = nullptr;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, s);
     cudaStreamSynchronize(s);
+    float gpu_ms = 0.f;
+    if (ev_last) cudaEventElapsedTime(&gpu_ms, ev_last, ev);
+    if (ev_last) cudaEventDestroy(ev_last);
+    ev_last = ev;
     const auto now = std::chrono::steady_clock::now();
-    fprintf(stderr, "[setup] %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+    // wall time since the previous mark, and the stream's time between the two marks
+    fprintf(stderr, "[setup] %-28s %8.1f ms (stream %8.1f ms)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(), gpu_ms);
     last = now;
 }
 

@@ -1,5 +1,6 @@
 // extern "C" boundary of libspfd_b200.so (include/spfd_b200.h).
 #include <atomic>
+#include <chrono>
 #include <cstring>
 #include <string>
 
@@ -176,13 +177,34 @@ static void check_cfg(const spfd_config *c) {
     SPFD_CHECK(c->coarse_cap >= 1 && c->max_levels >= 1, SPFD_EINVAL, "coarse_cap and max_levels must be >= 1");
 }
 
+// Setup peak of library pool memory per fine DOF (temporaries + the
+// hierarchy), measured with SPFD_SETUP_TRACE=1: C3 793 B/DOF.
+constexpr double kSetupPeakBytesPerDof = 800.0;
+
 int spfd_amg_setup_op(spfd_op_t h, const spfd_config *cfg, void *stream, spfd_amg_t *out) {
     NvtxRange range_("spfd_amg_setup_op");
     return guarded([&] {
         SPFD_CHECK(h && out, SPFD_EINVAL, "null argument");
         check_cfg(cfg);
         SPFD_CHECK(h->op->n_dofs >= 1, SPFD_EEMPTY, "empty Poisson system");
+        // reserve the pool for the setup's peak in one step (pool_reserve):
+        // the peak per DOF of the last setup in this process, else a C3/C4
+        // measured figure
+        static double peak_per_dof = kSetupPeakBytesPerDof;
+        const auto t0 = std::chrono::steady_clock::now();
+        const size_t base = pool_used();
+        pool_reserve((size_t)(peak_per_dof * (double)h->op->n_dofs));
+        pool_used_high_reset();
         Amg *a = amg_setup_op(h->op, *cfg, S(stream));
+        const size_t peak = pool_used_high_reset();
+        if (peak > base) peak_per_dof = std::max(peak_per_dof, (double)(peak - base) / (double)h->op->n_dofs);
+        if (getenv("SPFD_SETUP_TRACE"))
+            fprintf(stderr, "[setup] pool peak %.1f MB over %.1f MB in use (%.0f B/DOF)\n", (peak - base) / 1e6,
+                    base / 1e6, (double)(peak - base) / (double)h->op->n_dofs);
+        // setup time = the whole call (pool reservation and the fine-level
+        // CSR export included), on the host clock after the stream drained
+        SPFD_CUDA(cudaStreamSynchronize(S(stream)));
+        a->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         *out = new spfd_amg_s{a, h->op};
         pool_trim();
     });

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <chrono>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -81,6 +82,45 @@ inline cudaMemPool_t lib_pool() {
     return pools[dev];
 }
 
+// Bytes the pool currently hands out / its high-water mark since the last reset.
+inline size_t pool_used() {
+    size_t v = 0;
+    if (cudaMemPool_t pool = lib_pool()) cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &v);
+    return v;
+}
+inline size_t pool_used_high_reset() {
+    size_t v = 0;
+    if (cudaMemPool_t pool = lib_pool()) {
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &v);
+        size_t zero = 0;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
+    }
+    return v;
+}
+
+// Grow the pool in one step so that `bytes` more can be handed out without
+// mapping memory again.  Growing it allocation by allocation is slow and
+// erratic on the B200 driver: single 35-816 MB requests that had to map
+// memory took 5-176 ms each (C3 setup 0.6-2.8 s, SPFD_ALLOC_TRACE=1).
+inline void pool_reserve(size_t bytes) {
+    cudaMemPool_t pool = lib_pool();
+    if (!pool || bytes == 0) return;
+    size_t reserved = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    if (reserved >= used + bytes) return;
+    // (trimming the free blocks first and mapping one block for the whole
+    // estimate measured no steadier)
+    cudaDeviceSynchronize();
+    void *p = nullptr;
+    if (cudaMallocFromPoolAsync(&p, used + bytes - reserved, pool, 0) == cudaSuccess) {
+        cudaFreeAsync(p, 0);
+        cudaStreamSynchronize(0);
+    } else {
+        cudaGetLastError();  // not enough memory for the whole estimate: grow per allocation
+    }
+}
+
 // Return the pool's unused reservations (setup temporaries) to the device,
 // keeping a floor of SPFD_POOL_KEEP_MB (default 4096 MB of the 180 GB) mapped
 // so that the next setup does not pay the page mapping again (C3 repeat
@@ -124,9 +164,19 @@ struct DevBuf {
         release();
         if (count == 0) count = 1;
         cudaMemPool_t pool = lib_pool();
+        static const bool tr = getenv("SPFD_ALLOC_TRACE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         cudaError_t e = pool ? cudaMallocFromPoolAsync((void **)&p, count * sizeof(T), pool, 0)
                              : cudaMallocAsync((void **)&p, count * sizeof(T), 0);
+        const auto t1 = std::chrono::steady_clock::now();
         if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+        if (tr) {
+            const auto t2 = std::chrono::steady_clock::now();
+            const double a_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+            const double s_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+            if (a_ms + s_ms > 5.0)
+                fprintf(stderr, "[alloc] %10.1f MB  malloc %8.1f ms  sync %8.1f ms\n", count * sizeof(T) / 1e6, a_ms, s_ms);
+        }
         if (e != cudaSuccess) {
             p = nullptr;
             throw Error(SPFD_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
@@ -135,8 +185,18 @@ struct DevBuf {
     }
     void release() {
         if (p) {
+            static const bool tr = getenv("SPFD_ALLOC_TRACE") != nullptr;
+            const auto t0 = std::chrono::steady_clock::now();
             cudaDeviceSynchronize();
+            const auto t1 = std::chrono::steady_clock::now();
             cudaFreeAsync(p, 0);
+            if (tr) {
+                const auto t2 = std::chrono::steady_clock::now();
+                const double a_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+                const double f_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+                if (a_ms + f_ms > 5.0)
+                    fprintf(stderr, "[free ] %10.1f MB  sync %8.1f ms  free %8.1f ms\n", n * sizeof(T) / 1e6, a_ms, f_ms);
+            }
         }
         p = nullptr;
         n = 0;

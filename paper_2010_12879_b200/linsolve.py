@@ -18,6 +18,7 @@ symmetric).  All work runs in libspfd_b200.so:
 from __future__ import annotations
 
 import ctypes
+import weakref
 from dataclasses import dataclass, field
 from functools import cached_property
 
@@ -102,8 +103,18 @@ class AmgLevel:
     """Lazy host view of one device level (linsolve.py:56-61)."""
 
     def __init__(self, h: "AmgHierarchy", index: int):
-        self._h = h
+        # a weak reference: the hierarchy owns its levels, and a strong
+        # back-reference would keep the device hierarchy alive until the
+        # cycle collector runs instead of freeing it on the last `del`
+        self._href = weakref.ref(h)
         self.index = index
+
+    @property
+    def _h(self) -> "AmgHierarchy":
+        h = self._href()
+        if h is None:
+            raise ReferenceError("the AmgHierarchy of this level has been released")
+        return h
 
     def _csr(self, which):
         h = self._h
