@@ -102,36 +102,46 @@ __global__ void k_axis_params(Box g, Box lat, int a, AxisParam *tab) {
     }
 }
 
+// One warp per face row (j, k), lanes along i; the four (dy, dz) lattice
+// row offsets and weights are hoisted per row, and index math is 32-bit (the
+// lattice is small).  Same corner order and products as the reference.
 __global__ void __launch_bounds__(256) k_interp_rows(Box g, Box lat, int a, const AxisParam *__restrict__ tab,
                                                      const double *__restrict__ b, double area,
                                                      double *__restrict__ flux) {
     int64_t d[3] = {g.n[0], g.n[1], g.n[2]};
     d[a] += 1;
-    const int64_t nrow = d[1] * d[2];
+    const int nrow = (int)(d[1] * d[2]), n0 = (int)d[0], ny = (int)d[1];
+    const int ln0 = (int)lat.n[0], ln1 = (int)lat.n[1];
     const AxisParam *tx = tab, *ty = tab + d[0], *tz = tab + d[0] + d[1];
-    for (int64_t row = blockIdx.x; row < nrow; row += gridDim.x) {
-        const int64_t j = row % d[1], k = row / d[1];
+    const int lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < nrow; row += warps) {
+        const int j = row % ny, k = row / ny;
         const AxisParam py = ty[j], pz = tz[k];
-        for (int64_t i = threadIdx.x; i < d[0]; i += blockDim.x) {
+        const double wy[2] = {__dsub_rn(1.0, py.t), py.t}, wz[2] = {__dsub_rn(1.0, pz.t), pz.t};
+        int off[2][2];
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+            for (int dz = 0; dz < 2; ++dz)
+                off[dy][dz] = ln0 * ((int)(py.i0 + dy * py.s) + ln1 * (int)(pz.i0 + dz * pz.s));
+        double *frow = flux + (int64_t)row * n0;
+        for (int i = lane; i < n0; i += 32) {
             const AxisParam px = tx[i];
             double out = 0.0;
 #pragma unroll
             for (int dx = 0; dx < 2; ++dx) {
                 const double wx = dx ? px.t : __dsub_rn(1.0, px.t);
+                const int ix = (int)(px.i0 + dx * px.s);
 #pragma unroll
                 for (int dy = 0; dy < 2; ++dy) {
-                    const double wy = dy ? py.t : __dsub_rn(1.0, py.t);
-                    const double wxy = __dmul_rn(wx, wy);
+                    const double wxy = __dmul_rn(wx, wy[dy]);
 #pragma unroll
-                    for (int dz = 0; dz < 2; ++dz) {
-                        const double wz = dz ? pz.t : __dsub_rn(1.0, pz.t);
-                        const int64_t p = (px.i0 + dx * px.s) +
-                                          lat.n[0] * ((py.i0 + dy * py.s) + lat.n[1] * (pz.i0 + dz * pz.s));
-                        out = __dadd_rn(out, __dmul_rn(__dmul_rn(wxy, wz), b[3 * p + a]));
-                    }
+                    for (int dz = 0; dz < 2; ++dz)
+                        out = __dadd_rn(out, __dmul_rn(__dmul_rn(wxy, wz[dz]), b[3 * (ix + off[dy][dz]) + a]));
                 }
             }
-            flux[row * d[0] + i] = __dmul_rn(out, area);
+            frow[i] = __dmul_rn(out, area);
         }
     }
 }
@@ -200,25 +210,26 @@ __global__ void k_divergence(Box g, const double *__restrict__ f, double *__rest
 // ascending cell order like scipy's csc_matvec of div.T.
 __global__ void k_sub_div_transpose(Box g, const double *__restrict__ phi, const double *__restrict__ in,
                                     double *__restrict__ out) {
-    const int64_t nx = g.n[0], ny = g.n[1], nz = g.n[2];
-    const int64_t fx = (nx + 1) * ny * nz, fy = nx * (ny + 1) * nz, fz = nx * ny * (nz + 1);
-    const int64_t nf = fx + fy + fz;
-    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
-        int64_t lo = -1, hi = -1;
+    // 32-bit face / cell indices (the caller checks the box size)
+    const int nx = (int)g.n[0], ny = (int)g.n[1], nz = (int)g.n[2];
+    const int fx = (nx + 1) * ny * nz, fy = nx * (ny + 1) * nz, fz = nx * ny * (nz + 1);
+    const int nf = fx + fy + fz;
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x) {
+        int lo = -1, hi = -1;
         if (f < fx) {
-            const int64_t i = f % (nx + 1), r = f / (nx + 1);          // r = j + ny k
-            const int64_t c = i + nx * r;
+            const int i = f % (nx + 1), r = f / (nx + 1);          // r = j + ny k
+            const int c = i + nx * r;
             if (i > 0) lo = c - 1;
             if (i < nx) hi = c;
         } else if (f < fx + fy) {
-            const int64_t q = f - fx;
-            const int64_t i = q % nx, j = (q / nx) % (ny + 1), k = q / (nx * (ny + 1));
-            const int64_t c = i + nx * (j + ny * k);
+            const int q = f - fx;
+            const int i = q % nx, j = (q / nx) % (ny + 1), k = q / (nx * (ny + 1));
+            const int c = i + nx * (j + ny * k);
             if (j > 0) lo = c - nx;
             if (j < ny) hi = c;
         } else {
-            const int64_t q = f - fx - fy;
-            const int64_t k = q / (nx * ny);
+            const int q = f - fx - fy;
+            const int k = q / (nx * ny);
             if (k > 0) lo = q - nx * ny;
             if (k < nz) hi = q;
         }
@@ -268,69 +279,107 @@ __global__ void k_normal_fill(Box g, const int64_t *__restrict__ ptr, int32_t *_
 // solve to rounding error replaces the reference's AMG-FGMRES at rel_tol
 // <= 1e-12 (field_source.py:315-321): the projection agrees with the
 // reference to its solve tolerance.  The transforms are FP64 tiled
-// products (k_dgemm_strided), the z solves one Thomas sweep per mode.
+// products (k_dgemm_split), the z solves one Thomas sweep per mode.
 
-// C[b](m, n) = sum_k A[b](m, k) B[b](k, n), element strides per operand
+// C(m, n) = sum_k A(m, k) B(k, n) in FP64, k in order (fma chain: the same
+// bits as a plain loop).  The column index n is split as n = lo + nlo * hi
+// with separate strides, so a batch of planes or both rhs run as one wide
+// product: B(k, n) = B[k sBk + lo sBlo + hi sBhi], C(m, n) = C[m sCm + lo sClo + hi sChi].
 struct GemmArgs {
     const double *A, *B;
     double *C;
     int64_t M, N, K;
-    int64_t sAm, sAk, sAb, sBk, sBn, sBb, sCm, sCn, sCb;
+    int64_t sAm, sAk;
+    int64_t sBk, nlo, sBlo, sBhi;
+    int64_t sCm, sClo, sChi;
 };
 
-constexpr int kGBM = 64, kGBN = 64, kGBK = 16, kGTM = 4, kGTN = 4;  // 16 x 16 threads, 4 x 4 outputs each
-
-__global__ void __launch_bounds__(256) k_dgemm_strided(GemmArgs g) {
-    __shared__ double As[kGBK][kGBM + 1];
-    __shared__ double Bs[kGBK][kGBN + 1];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int64_t m0 = (int64_t)blockIdx.x * kGBM, n0 = (int64_t)blockIdx.y * kGBN, b = blockIdx.z;
-    const double *A = g.A + b * g.sAb, *B = g.B + b * g.sBb;
-    double *C = g.C + b * g.sCb;
-    const bool a_mfast = g.sAm <= g.sAk, b_nfast = g.sBn < g.sBk;
-    double acc[kGTM][kGTN];
+// BM x BN tile per CTA of 256 threads, 8 x 8 outputs per thread (TM threads
+// along m, TN along n); BK = 8 k per stage, the next stage prefetched into
+// registers while the current one is multiplied out of shared memory.  The
+// DST matrices are 160 / 112 wide at C3, so BM = 32 wastes no rows on x.
+constexpr int kGBK = 8;
+template <int BM>
+__global__ void __launch_bounds__(256, 1) k_dgemm_split(GemmArgs g) {
+    constexpr int TM = BM / 8, TN = 256 / TM, BN = TN * 8;
+    constexpr int NB = kGBK * BN / 256;       // B elements per thread per stage
+    constexpr int NA = (kGBK * BM + 255) / 256;
+    __shared__ double As[kGBK][BM];
+    __shared__ double Bs[kGBK][BN + 1];
+    __shared__ int64_t boff[BN];
+    const int tid = threadIdx.x, tm = tid % TM, tn = tid / TM;
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    for (int q = tid; q < BN; q += 256) {
+        const int64_t n = n0 + q;
+        boff[q] = n < g.N ? (n % g.nlo) * g.sBlo + (n / g.nlo) * g.sBhi : -1;
+    }
+    __syncthreads();
+    const bool nfast = g.sBlo < g.sBk;
+    double ra[NA], rb[NB];
+    auto load = [&](int64_t k0) {
 #pragma unroll
-    for (int i = 0; i < kGTM; ++i)
-#pragma unroll
-        for (int j = 0; j < kGTN; ++j) acc[i][j] = 0.0;
-    for (int64_t k0 = 0; k0 < g.K; k0 += kGBK) {
-#pragma unroll
-        for (int t = 0; t < (kGBM * kGBK) / 256; ++t) {
-            const int e = threadIdx.x + t * 256;
-            // consecutive threads along the operand's contiguous index
-            const int mm = a_mfast ? e % kGBM : e / kGBK, kk = a_mfast ? e / kGBM : e % kGBK;
+        for (int t = 0; t < NA; ++t) {
+            const int e = tid + t * 256;
+            const int mm = e % BM, kk = e / BM;
             const int64_t m = m0 + mm, k = k0 + kk;
-            As[kk][mm] = (m < g.M && k < g.K) ? A[m * g.sAm + k * g.sAk] : 0.0;
+            ra[t] = (e < kGBK * BM && m < g.M && k < g.K) ? g.A[m * g.sAm + k * g.sAk] : 0.0;
         }
 #pragma unroll
-        for (int t = 0; t < (kGBN * kGBK) / 256; ++t) {
-            const int e = threadIdx.x + t * 256;
-            const int nn = b_nfast ? e % kGBN : e / kGBK, kk = b_nfast ? e / kGBN : e % kGBK;
-            const int64_t n = n0 + nn, k = k0 + kk;
-            Bs[kk][nn] = (n < g.N && k < g.K) ? B[k * g.sBk + n * g.sBn] : 0.0;
+        for (int t = 0; t < NB; ++t) {
+            const int e = tid + t * 256;
+            const int nn = nfast ? e % BN : e / kGBK, kk = nfast ? e / BN : e % kGBK;
+            const int64_t o = boff[nn], k = k0 + kk;
+            rb[t] = (o >= 0 && k < g.K) ? g.B[k * g.sBk + o] : 0.0;
         }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int t = 0; t < NA; ++t) {
+            const int e = tid + t * 256;
+            if (e < kGBK * BM) As[e / BM][e % BM] = ra[t];
+        }
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+            const int e = tid + t * 256;
+            const int nn = nfast ? e % BN : e / kGBK, kk = nfast ? e / BN : e % kGBK;
+            Bs[kk][nn] = rb[t];
+        }
+    };
+    double acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    load(0);
+    for (int64_t k0 = 0; k0 < g.K; k0 += kGBK) {
+        store();
         __syncthreads();
+        if (k0 + kGBK < g.K) load(k0 + kGBK);
 #pragma unroll
         for (int kk = 0; kk < kGBK; ++kk) {
-            double a[kGTM], bb[kGTN];
+            double a[8], b[8];
 #pragma unroll
-            for (int i = 0; i < kGTM; ++i) a[i] = As[kk][tx + 16 * i];
+            for (int i = 0; i < 8; ++i) a[i] = As[kk][tm + TM * i];
 #pragma unroll
-            for (int j = 0; j < kGTN; ++j) bb[j] = Bs[kk][ty + 16 * j];
+            for (int j = 0; j < 8; ++j) b[j] = Bs[kk][tn + TN * j];
 #pragma unroll
-            for (int i = 0; i < kGTM; ++i)
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < kGTN; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+                for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < kGTM; ++i)
+    for (int j = 0; j < 8; ++j) {
+        const int64_t n = n0 + tn + TN * j;
+        if (n >= g.N) continue;
+        const int64_t co = (n % g.nlo) * g.sClo + (n / g.nlo) * g.sChi;
 #pragma unroll
-        for (int j = 0; j < kGTN; ++j) {
-            const int64_t m = m0 + tx + 16 * i, n = n0 + ty + 16 * j;
-            if (m < g.M && n < g.N) C[m * g.sCm + n * g.sCn] = acc[i][j];
+        for (int i = 0; i < 8; ++i) {
+            const int64_t m = m0 + tm + TM * i;
+            if (m < g.M) g.C[m * g.sCm + co] = acc[i][j];
         }
+    }
 }
 
 // The eliminated pivots of every mode's z system depend only on the mode:
@@ -393,10 +442,10 @@ __global__ void k_tridiag_apply(int64_t nx, int64_t ny, int64_t nz, int nrhs, co
 // residual d - (6 phi - sum of neighbours), summed squares per block
 __global__ void k_lap_resid(Box g, const double *__restrict__ phi, const double *__restrict__ d,
                             double *__restrict__ partials) {
-    const int64_t nx = g.n[0], ny = g.n[1], nz = g.n[2], nxy = nx * ny, nc = nxy * nz;
+    const int nx = (int)g.n[0], ny = (int)g.n[1], nz = (int)g.n[2], nxy = nx * ny, nc = nxy * nz;
     double acc = 0.0;
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = c % nx, j = (c / nx) % ny, k = c / nxy;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+        const int i = c % nx, j = (c / nx) % ny, k = c / nxy;
         double s = 6.0 * phi[c];
         if (k > 0) s -= phi[c - nxy];
         if (j > 0) s -= phi[c - nx];
@@ -561,42 +610,48 @@ __global__ void __launch_bounds__(kRedThreads) k_sumsq_partial(int64_t n, const 
 // it: blocks walk face rows (axis, j, k) with threads along i, so the face
 // index needs one division per row instead of 64-bit div/mod per face;
 // per-block partials, summed on the host in block order.
+// Sum of squared circulation defects over every face (gauging.py:167-171):
+// one warp per face row, lanes along the row, 32-bit index math (a box axis
+// holds < 2^31 edges; checked by the caller).
 __global__ void __launch_bounds__(kRedThreads) k_circ_sumsq(Box g, const double *__restrict__ a,
                                                             const double *__restrict__ flux,
                                                             double *__restrict__ part) {
     __shared__ double red[32];
-    const int64_t nx = g.n[0], ny = g.n[1], nz = g.n[2];
-    const int64_t E0 = nx * (ny + 1) * (nz + 1), E1 = (nx + 1) * ny * (nz + 1);
+    const int nx = (int)g.n[0], ny = (int)g.n[1], nz = (int)g.n[2];
+    const int64_t E0 = (int64_t)nx * (ny + 1) * (nz + 1), E1 = (int64_t)(nx + 1) * ny * (nz + 1);
     const int64_t eoff[3] = {0, E0, E0 + E1};
+    const int lane = threadIdx.x & 31;
+    const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), warps = gridDim.x * (blockDim.x >> 5);
     double v[1] = {0.0};
-    int64_t fbase = 0, rbase = 0;
+    int64_t fbase = 0;
     for (int ax = 0; ax < 3; ++ax) {
-        int64_t fd[3] = {nx, ny, nz};
+        int fd[3] = {nx, ny, nz};
         fd[ax] += 1;
-        const int64_t nrow = fd[1] * fd[2];
+        const int nrow = fd[1] * fd[2];
         const int e1 = (ax + 1) % 3, e2 = (ax + 2) % 3;
-        int64_t ed1[3] = {nx + 1, ny + 1, nz + 1}, ed2[3] = {nx + 1, ny + 1, nz + 1};
+        int ed1[3] = {nx + 1, ny + 1, nz + 1}, ed2[3] = {nx + 1, ny + 1, nz + 1};
         ed1[e1] -= 1;
         ed2[e2] -= 1;
-        auto eidx = [&](const int64_t *ed, int64_t i, int64_t j, int64_t k) { return i + ed[0] * (j + ed[1] * k); };
-        for (int64_t row = blockIdx.x; row < nrow; row += gridDim.x) {
-            const int64_t j = row % fd[1], k = row / fd[1];
-            for (int64_t i = threadIdx.x; i < fd[0]; i += blockDim.x) {
-                int64_t c[3] = {i, j, k}, s1[3] = {i, j, k}, s2[3] = {i, j, k};
-                s1[e1] += 1;
-                s2[e2] += 1;
-                double circ = a[eoff[e1] + eidx(ed1, c[0], c[1], c[2])];
-                circ += a[eoff[e2] + eidx(ed2, s1[0], s1[1], s1[2])];
-                circ -= a[eoff[e1] + eidx(ed1, s2[0], s2[1], s2[2])];
-                circ -= a[eoff[e2] + eidx(ed2, c[0], c[1], c[2])];
-                const double d = circ - flux[fbase + row * fd[0] + i];
-                v[0] = fma(d, d, v[0]);
+        // unit steps of the two edge arrays along e1 / e2 and along i
+        const int st1[3] = {1, ed1[0], ed1[0] * ed1[1]}, st2[3] = {1, ed2[0], ed2[0] * ed2[1]};
+        const double *A1 = a + eoff[e1], *A2 = a + eoff[e2];
+        for (int row = warp; row < nrow; row += warps) {
+            const int j = row % fd[1], k = row / fd[1];
+            // edge e1 at c and c + e2, edge e2 at c and c + e1, for c = (0, j, k)
+            const int b1 = ed1[0] * (j + ed1[1] * k), b2 = ed2[0] * (j + ed2[1] * k);
+            const double *frow = flux + fbase + (int64_t)row * fd[0];
+            for (int i = lane; i < fd[0]; i += 32) {
+                const int q1 = b1 + i, q2 = b2 + i;
+                double circ = A1[q1];
+                circ += A2[q2 + st2[e1]];
+                circ -= A1[q1 + st1[e2]];
+                circ -= A2[q2];
+                const double dd = circ - frow[i];
+                v[0] = fma(dd, dd, v[0]);
             }
         }
-        fbase += nrow * fd[0];
-        rbase += nrow;
+        fbase += (int64_t)nrow * fd[0];
     }
-    (void)rbase;
     block_sum<1>(v, red);
     if (threadIdx.x == 0) part[blockIdx.x] = v[0];
 }
@@ -756,9 +811,8 @@ void field_interpolate(Field &F, const spfd_box &lat, const double *b, double *f
             const int64_t nt = d[0] + d[1] + d[2];
             if (F.wt.n < (size_t)nt) F.wt.alloc(nt);
             k_axis_params<<<blocks(nt), 256, 0, s>>>(F.g, L, a, F.wt.get());
-            const int grid = (int)std::min<int64_t>(d[1] * d[2], 148 * 16);
-            k_interp_rows<<<grid, d[0] >= 256 ? 256 : (int)((d[0] + 31) / 32 * 32), 0, s>>>(F.g, L, a, F.wt.get(), b,
-                                                                                           area, flux + off);
+            const int grid = (int)std::min<int64_t>((d[1] * d[2] + 7) / 8, 148 * 16);  // 8 warps = 8 rows
+            k_interp_rows<<<grid, 256, 0, s>>>(F.g, L, a, F.wt.get(), b, area, flux + off);
             SPFD_LAUNCH_CHECK();
         }
         off += nf;
@@ -857,9 +911,124 @@ static void ensure_spectral(Field &F, cudaStream_t s) {
     SPFD_LAUNCH_CHECK();
 }
 
-static void gemm(const GemmArgs &g, int64_t batch, cudaStream_t s) {
-    const dim3 grid((unsigned)((g.M + kGBM - 1) / kGBM), (unsigned)((g.N + kGBN - 1) / kGBN), (unsigned)batch);
-    k_dgemm_strided<<<grid, 256, 0, s>>>(g);
+// The same product on the FP64 tensor cores (mma.sync m8n8k4 f64): a CTA
+// tile of 32 x 256, each of the 8 warps 32 x 32 as 4 x 4 m8n8k4 blocks.  The
+// k order inside an MMA is the hardware's, so the bits can differ from the
+// FFMA chain in the last place (the spectral solve is tolerance-checked).
+__device__ __forceinline__ void dmma_m8n8k4(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const int n = valid ? 8 : 0;  // zero-fill outside the operand
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(valid ? src : dst), "r"(n) : "memory");
+}
+
+// kDmmaStages-deep cp.async pipeline of BK = 8 slices (dynamic shared memory)
+constexpr int kDmmaStages = 4, kDmmaBM = 32, kDmmaBN = 256, kDmmaPA = kDmmaBM + 4, kDmmaPB = kDmmaBN + 4;
+constexpr size_t kDmmaSmem = (size_t)kDmmaStages * kGBK * (kDmmaPA + kDmmaPB) * sizeof(double) + kDmmaBN * sizeof(int64_t);
+
+__global__ void __launch_bounds__(256) k_dgemm_mma(GemmArgs g) {
+    constexpr int BM = kDmmaBM, BN = kDmmaBN, PA = kDmmaPA, PB = kDmmaPB, ST = kDmmaStages;
+    constexpr int NB = kGBK * BN / 256, NA = (kGBK * BM + 255) / 256;
+    extern __shared__ __align__(16) double dsm[];
+    double *As = dsm;                              // [ST][BK][PA]
+    double *Bs = dsm + ST * kGBK * PA;             // [ST][BK][PB]
+    int64_t *boff = reinterpret_cast<int64_t *>(Bs + ST * kGBK * PB);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    for (int q = tid; q < BN; q += 256) {
+        const int64_t n = n0 + q;
+        boff[q] = n < g.N ? (n % g.nlo) * g.sBlo + (n / g.nlo) * g.sBhi : -1;
+    }
+    __syncthreads();
+    const bool nfast = g.sBlo < g.sBk;
+    const int nk = (int)((g.K + kGBK - 1) / kGBK);
+    auto issue = [&](int kt) {
+        if (kt < nk) {
+            const int st = kt % ST;
+            const int64_t k0 = (int64_t)kt * kGBK;
+#pragma unroll
+            for (int t = 0; t < NA; ++t) {
+                const int e = tid + t * 256;
+                if (e < kGBK * BM) {
+                    const int mm = e % BM, kk = e / BM;
+                    const int64_t m = m0 + mm, k = k0 + kk;
+                    const bool ok = m < g.M && k < g.K;
+                    cp_async8(&As[(st * kGBK + kk) * PA + mm], ok ? g.A + m * g.sAm + k * g.sAk : nullptr, ok);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < NB; ++t) {
+                const int e = tid + t * 256;
+                const int nn = nfast ? e % BN : e / kGBK, kk = nfast ? e / BN : e % kGBK;
+                const int64_t o = boff[nn], k = k0 + kk;
+                const bool ok = o >= 0 && k < g.K;
+                cp_async8(&Bs[(st * kGBK + kk) * PB + nn], ok ? g.B + k * g.sBk + o : nullptr, ok);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int fr = lane & 3, fc = lane >> 2;  // fragment row (k) / column (m or n)
+#pragma unroll
+    for (int s0 = 0; s0 < ST - 1; ++s0) issue(s0);
+    for (int kt = 0; kt < nk; ++kt) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2) : "memory");
+        __syncthreads();
+        issue(kt + ST - 1);  // refills the stage computed in iteration kt - 1
+        const double *A = As + (kt % ST) * kGBK * PA, *B = Bs + (kt % ST) * kGBK * PB;
+#pragma unroll
+        for (int kq = 0; kq < kGBK; kq += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = A[(kq + fr) * PA + i * 8 + fc];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = B[(kq + fr) * PB + warp * 32 + j * 8 + fc];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t n = n0 + warp * 32 + j * 8 + fr * 2 + h;
+            if (n >= g.N) continue;
+            const int64_t co = (n % g.nlo) * g.sClo + (n / g.nlo) * g.sChi;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int64_t m = m0 + i * 8 + fc;
+                if (m < g.M) g.C[m * g.sCm + co] = acc[i][j][h];
+            }
+        }
+}
+
+static void gemm(const GemmArgs &g, cudaStream_t s) {
+    constexpr int BM = 32;
+    const bool mma = !(getenv("SPFD_DGEMM_MMA") && std::string(getenv("SPFD_DGEMM_MMA")) == "0");  // read per call
+    const int BN = mma ? 256 : 8 * (256 / (BM / 8));
+    SPFD_CHECK((g.N + BN - 1) / BN <= 65535, SPFD_EINVAL, "grid too large for the spectral solve");
+    const dim3 grid((unsigned)((g.M + BM - 1) / BM), (unsigned)((g.N + BN - 1) / BN));
+    if (mma) {
+        static bool attr = false;
+        if (!attr) {
+            SPFD_CUDA(cudaFuncSetAttribute(k_dgemm_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDmmaSmem));
+            attr = true;
+        }
+        k_dgemm_mma<<<grid, 256, kDmmaSmem, s>>>(g);
+    }
+    else k_dgemm_split<BM><<<grid, 256, 0, s>>>(g);
     SPFD_LAUNCH_CHECK();
 }
 
@@ -867,16 +1036,17 @@ static void gemm(const GemmArgs &g, int64_t batch, cudaStream_t s) {
 static void spectral_solve(Field &F, int na, const double *d, double *phi, cudaStream_t s) {
     ensure_spectral(F, s);
     const int64_t nx = F.g.n[0], ny = F.g.n[1], nz = F.g.n[2], plane = nx * ny, nc = plane * nz;
-    SPFD_CHECK(ny * nz <= (int64_t)65535 * kGBN && nz * na <= 65535, SPFD_EINVAL, "grid too large for the spectral solve");
     double *buf = F.spec_ws.get();
     const double *Sx = F.sx.get(), *Sy = F.sy.get();
     // along x: out(p, col) = sum_i Sx(p, i) in(i, col), col = (j, k)
     auto along_x = [&](const double *in, double *out) {
-        gemm(GemmArgs{Sx, in, out, nx, ny * nz, nx, nx, 1, 0, 1, nx, nc, 1, nx, nc}, na, s);
+        // A = Sx (p, i); B(i, n) = in[i + nx col + nc rhs], n = col + ny nz rhs
+        gemm(GemmArgs{Sx, in, out, nx, ny * nz * na, nx, nx, 1, 1, ny * nz, nx, nc, 1, nx, nc}, s);
     };
-    // along y, per plane: out(i, q) = sum_j in(i, j) Sy(q, j)
+    // along y: out(i, q, kz) = sum_j Sy(q, j) in(i, j, kz) as one product,
+    // A = Sy (q, j); B(j, n) = in[i + nx j + plane kz'], n = i + nx kz' (kz' runs over nz na planes)
     auto along_y = [&](const double *in, double *out) {
-        gemm(GemmArgs{in, Sy, out, nx, ny, ny, 1, nx, plane, 1, ny, 0, 1, nx, plane}, nz * na, s);
+        gemm(GemmArgs{Sy, in, out, ny, nx * nz * na, ny, ny, 1, nx, nx, 1, plane, nx, 1, plane}, s);
     };
     along_x(d, buf);
     along_y(buf, phi);
@@ -908,6 +1078,7 @@ void field_clean(Field &F, int nrhs, const double *in, double *out, double tol, 
                  cudaStream_t s) {
     SPFD_CHECK(nrhs == 1 || nrhs == 2, SPFD_EINVAL, "nrhs must be 1 or 2");
     const int64_t nc = F.n_cells(), nf = F.n_faces();
+    SPFD_CHECK(nf < (int64_t)1 << 30, SPFD_EINVAL, "grid too large for 32-bit face indexing");
     if (F.wc.n < (size_t)(4 * nc)) F.wc.alloc(4 * nc);  // [2][nc] divergences + [nc][2] interleaved
     double *divp = F.wc.get(), *inter = F.wc.get() + 2 * nc;
     double fnorm[2] = {0.0, 0.0};
@@ -917,14 +1088,18 @@ void field_clean(Field &F, int nrhs, const double *in, double *out, double tol, 
         info[c] = spfd_clean_info{};
         const double *ic = in + (int64_t)c * nf;
         double *oc = out + (int64_t)c * nf;
-        if (oc != ic) SPFD_CUDA(cudaMemcpyAsync(oc, ic, nf * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        // a skipped rhs is passed through; a cleaned one is written by
+        // k_sub_div_transpose from `in`, so it needs no copy
+        auto pass = [&] {
+            if (oc != ic) SPFD_CUDA(cudaMemcpyAsync(oc, ic, nf * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        };
         fnorm[c] = std::sqrt(sumsq(F, ic, nf, s));
-        if (fnorm[c] == 0.0 || nc == 0) continue;
+        if (fnorm[c] == 0.0 || nc == 0) { pass(); continue; }
         field_divergence(F, ic, divp + (int64_t)na * nc, s);
         const double rel = std::sqrt(sumsq(F, divp + (int64_t)na * nc, nc, s)) / fnorm[c];
         info[c].rel_before = rel;
         info[c].rel_after = rel;
-        if (rel <= tol) continue;
+        if (rel <= tol) { pass(); continue; }
         rtol = std::min(rtol, std::min(1e-12, 0.25 * tol / rel));
         act[na++] = c;
     }
@@ -1058,6 +1233,8 @@ void field_gauge(Field &F, int tree, const double *flux, double *a, double tol, 
     }
     // postcondition: circulation residual over every face (gauging.py:167-171);
     // the defect array is only materialised to locate the worst face
+    SPFD_CHECK((F.g.n[0] + 1) * (F.g.n[1] + 1) * (F.g.n[2] + 1) < (int64_t)INT32_MAX, SPFD_EINVAL,
+               "grid too large for 32-bit face indexing");
     k_circ_sumsq<<<kRedBlocks, kRedThreads, 0, s>>>(F.g, a, flux, F.part.get());
     SPFD_LAUNCH_CHECK();
     {

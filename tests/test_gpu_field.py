@@ -242,7 +242,7 @@ def test_cleaning_box_level0_matches_csr(g, grid, monkeypatch):
     assert abs(out[0][1] - out[1][1]) <= 1
 
 
-@pytest.mark.parametrize("dims", [(7, 5, 9), (24, 17, 40), (1, 6, 11)])
+@pytest.mark.parametrize("dims", [(7, 5, 9), (24, 17, 40), (1, 6, 11), (70, 45, 33)])
 def test_cleaning_spectral_matches_amg(dims, rng, monkeypatch):
     """The default projection solve (sine transforms in x and y, one
     tridiagonal solve per mode along z) against the reference's method
@@ -255,13 +255,17 @@ def test_cleaning_spectral_matches_amg(dims, rng, monkeypatch):
     nf = sum(int(np.prod([d + (1 if a == ax else 0) for a, d in enumerate(dims)])) for ax in range(3))
     flux = rng.standard_normal((2, nf))
     out = {}
-    for solver in ("spectral", "amg"):
-        monkeypatch.setenv("SPFD_CLEAN_SOLVER", solver)
+    # the sine transforms on the FP64 tensor cores (default) and as FFMA chains
+    for solver, mma in (("spectral", "1"), ("spectral_fma", "0"), ("amg", "1")):
+        monkeypatch.setenv("SPFD_CLEAN_SOLVER", solver.split("_")[0])
+        monkeypatch.setenv("SPFD_DGEMM_MMA", mma)
         ops = FieldOps(grid, SolveConfig())
         c = ops.clean(torch.from_numpy(flux).cuda(), 1e-10).cpu().numpy()
         out[solver] = (c, ops.last_clean)
     c_s, i_s = out["spectral"]
     c_a, i_a = out["amg"]
+    for k in range(2):
+        assert np.linalg.norm(c_s[k] - out["spectral_fma"][0][k]) <= 1e-13 * np.linalg.norm(flux[k])
     for k in range(2):
         fn = np.linalg.norm(flux[k])
         assert np.linalg.norm(c_s[k] - c_a[k]) <= 1e-10 * fn
