@@ -704,7 +704,7 @@ int vcycle_dist_fine(Amg &h, double *r, double *z, cudaStream_t s) {
 template <int R>
 void finalize_dist(Amg &h, int nblocks, int slot, int what, cudaStream_t s) {
     Dist &D = *h.dist;
-    k_finalize<R><<<1, 256, 0, s>>>(h.partials.get(), nblocks, h.scal.get(), S_LOC, F_STORE, 0.0);
+    k_finalize<R><<<1, kFinThreads, 0, s>>>(h.partials.get(), nblocks, h.scal.get(), S_LOC, F_STORE, 0.0);
     SPFD_LAUNCH_CHECK();
     D.comm->allgather(h.scal.get() + S_LOC, D.grecv.get(), R * sizeof(double), s);
     k_rank_finalize<R><<<1, 32, 0, s>>>(D.grecv.get(), D.size, h.scal.get(), slot, what);

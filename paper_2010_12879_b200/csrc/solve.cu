@@ -835,18 +835,33 @@ __global__ void k_xpby(int64_t n, const double *scal, const double *z, double *p
 
 // Sum per-CTA partials in index order; then apply `what`.
 enum { F_STORE = 0, F_ALPHA = 1, F_BETA_INIT = 2, F_BETA = 3, F_BETA_AUTO = 4 };
+// One CTA of kFinThreads: thread t sums partials t, t + T, t + 2T, ... in
+// four interleaved accumulators (coalesced, four loads in flight; a
+// contiguous stripe per thread made this a chain of dependent L2 reads,
+// 11 us for the 8705 fine-level tiles), then a fixed tree -- a fixed order,
+// so the result is reproducible run to run.
+constexpr int kFinThreads = 1024;
 template <int R>
-__global__ void k_finalize(const double *partials, int nblocks, double *scal, int slot, int what, double tol) {
+__global__ void __launch_bounds__(kFinThreads) k_finalize(const double *partials, int nblocks, double *scal, int slot,
+                                                          int what, double tol) {
     __shared__ double red[32 * R];
-    double s[R];
+    double s[R], s4[4][R];
 #pragma unroll
-    for (int c = 0; c < R; ++c) s[c] = 0.0;
-    // each thread sums a contiguous stripe sequentially, then a fixed tree
-    int per = (nblocks + blockDim.x - 1) / blockDim.x;
-    int b0 = threadIdx.x * per, b1 = min(nblocks, b0 + per);
-    for (int b = b0; b < b1; ++b)
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int c = 0; c < R; ++c) s[c] += partials[b * R + c];
+        for (int c = 0; c < R; ++c) s4[u][c] = 0.0;
+    const int T = blockDim.x;
+    int b = threadIdx.x;
+    for (; b + 3 * T < nblocks; b += 4 * T)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int c = 0; c < R; ++c) s4[u][c] += partials[(b + u * T) * R + c];
+    for (; b < nblocks; b += T)
+#pragma unroll
+        for (int c = 0; c < R; ++c) s4[0][c] += partials[b * R + c];
+#pragma unroll
+    for (int c = 0; c < R; ++c) s[c] = (s4[0][c] + s4[1][c]) + (s4[2][c] + s4[3][c]);
     block_sum<R>(s, red);
     if (threadIdx.x == 0) {
         if (what == F_BETA_AUTO) {  // graph PCG: the first iteration after a (re)start initialises rho
@@ -1449,7 +1464,7 @@ void amg_estimate_lmax(Amg &h, cudaStream_t s) {
     auto norm = [&](int64_t n, const double *v) {
         k_dot<1><<<kDotGrid, kDotThreads, 0, s>>>(n, v, v, h.partials.get());
         SPFD_LAUNCH_CHECK();
-        k_finalize<1><<<1, 256, 0, s>>>(h.partials.get(), kDotGrid, sc, S_TMP, F_STORE, 0.0);
+        k_finalize<1><<<1, kFinThreads, 0, s>>>(h.partials.get(), kDotGrid, sc, S_TMP, F_STORE, 0.0);
         SPFD_LAUNCH_CHECK();
         double v2 = 0.0;
         SPFD_CUDA(cudaMemcpyAsync(&v2, sc + S_TMP, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1488,7 +1503,7 @@ namespace {
 
 template <int R>
 void finalize(Amg &h, int nblocks, int slot, int what, cudaStream_t s) {
-    k_finalize<R><<<1, 256, 0, s>>>(h.partials.get(), nblocks, h.scal.get(), slot, what, 0.0);
+    k_finalize<R><<<1, kFinThreads, 0, s>>>(h.partials.get(), nblocks, h.scal.get(), slot, what, 0.0);
     SPFD_LAUNCH_CHECK();
 }
 
