@@ -437,7 +437,8 @@ def main():
              (7, "level1_prolong_post", "k_csr<4,2,6> level-1 prolongation + post-smooth z = od (r + d) + Q e, "
               "Q = P - od A P", 1),
              (8, "pcg_r_update", "k_update_r<2> r -= alpha q (+ r.r)", 1),
-             (9, "pcg_p_update", "k_xpby<2> p = z + beta p", 1)]
+             (9, "pcg_p_update", "k_xpby<2> p = z + beta p" if os.environ.get("SPFD_PCG_FUSE_X") == "0"
+              else "k_xpby_x<2> x += alpha p; p = z + beta p", 1)]
     kernels = {}
     iter_ms = ms / it_mean if it_mean else ms
     for which, key, desc, per_it in table:

@@ -337,6 +337,49 @@ __device__ __forceinline__ void csr_prefetch(const CsrView &m, int64_t row, int 
     l2_prefetch(m.val, q0, q1, 8);
 }
 
+// Row epilogue of the CSR kernels: reduce the G lanes' partial sums with a
+// fixed xor tree (all lanes take part), then the row leader (`lead`) applies
+// MODE to global row gr:
+//   0: y = sum (+ aux = od_aux y)   1/2: y = r - sum   3: y = x + od (r - sum)
+//   4: y = od r + sum   5: y = base + sum   6: y = od (r + base) + sum
+template <int G, int R, int MODE, bool DOT>
+__device__ __forceinline__ void csr_row_out(typename V<R>::T acc, bool lead, int64_t gr, const double *__restrict__ x,
+                                            const double *__restrict__ r, const double *__restrict__ od,
+                                            const double *__restrict__ base, double *__restrict__ y,
+                                            const double *__restrict__ od_aux, double *__restrict__ aux,
+                                            double (&dot)[R]) {
+    using W = V<R>;
+    using T = typename W::T;
+    double ac[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+        ac[c] = W::comp(acc, c);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], o, G);
+    }
+    if (!lead) return;
+    T sum;
+    if constexpr (R == 1) sum = ac[0];
+    else sum = make_double2(ac[0], ac[1]);
+    T out;
+    if (MODE == 0) out = sum;
+    else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(r, gr), sum);
+    else if (MODE == 3) out = W::add(W::ld(x, gr), W::scale(od[gr], W::sub(W::ld(r, gr), sum)));
+    else if (MODE == 4) out = W::add(W::scale(od[gr], W::ld(r, gr)), sum);
+    else if (MODE == 6) out = W::add(W::scale(od[gr], W::add(W::ld(r, gr), W::ld(base, gr))), sum);
+    else out = W::add(W::ld(base, gr), sum);
+    W::st(y, gr, out);
+    if (MODE == 0 && aux) W::st(aux, gr, W::scale(od_aux[gr], out));
+    if (DOT) {
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            if (MODE == 0) dot[c] += W::dot(W::ld(x, gr), out, c);
+            else if (MODE == 3) dot[c] += W::dot(W::ld(r, gr), out, c);
+            else dot[c] += W::dot(out, out, c);
+        }
+    }
+}
+
 template <int G, int R, int MODE, bool DOT>
 __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__restrict__ r,
                       const double *__restrict__ od, const double *__restrict__ base, double *__restrict__ y,
@@ -383,36 +426,8 @@ __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__r
                     if (col[u] >= 0) acc = W::fma_(a[u], xv[u], acc);
             }
         }
-        double ac[R];
-#pragma unroll
-        for (int c = 0; c < R; ++c) {
-            ac[c] = W::comp(acc, c);
-#pragma unroll
-            for (int o = G / 2; o > 0; o >>= 1) ac[c] += __shfl_xor_sync(0xffffffffu, ac[c], o, G);
-        }
-        if (valid && lane == 0) {
-            const int64_t gr = rowmap ? (int64_t)rowmap[row] : row;  // global row (owned-row CSR)
-            T sum;
-            if constexpr (R == 1) sum = ac[0];
-            else sum = make_double2(ac[0], ac[1]);
-            T out;
-            if (MODE == 0) out = sum;
-            else if (MODE == 1 || MODE == 2) out = W::sub(W::ld(r, gr), sum);
-            else if (MODE == 3) out = W::add(W::ld(x, gr), W::scale(od[gr], W::sub(W::ld(r, gr), sum)));
-            else if (MODE == 4) out = W::add(W::scale(od[gr], W::ld(r, gr)), sum);
-            else if (MODE == 6) out = W::add(W::scale(od[gr], W::add(W::ld(r, gr), W::ld(base, gr))), sum);
-            else out = W::add(W::ld(base, gr), sum);
-            W::st(y, gr, out);
-            if (MODE == 0 && aux) W::st(aux, gr, W::scale(od_aux[gr], out));
-            if (DOT) {
-#pragma unroll
-                for (int c = 0; c < R; ++c) {
-                    if (MODE == 0) dot[c] += W::dot(W::ld(x, gr), out, c);
-                    else if (MODE == 3) dot[c] += W::dot(W::ld(r, gr), out, c);
-                    else dot[c] += W::dot(out, out, c);
-                }
-            }
-        }
+        csr_row_out<G, R, MODE, DOT>(acc, valid && lane == 0, (valid && rowmap) ? (int64_t)rowmap[row] : row, x, r, od, base, y,
+                                     od_aux, aux, dot);
     }
     if (DOT) {
         block_sum<R>(dot, red);
@@ -833,6 +848,22 @@ __global__ void k_xpby(int64_t n, const double *scal, const double *z, double *p
     }
 }
 
+// x += alpha p ; p = z + beta p  (alpha of the previous iteration: the graph
+// body's deferred x update fused into the p update -- one read of p, and the
+// same two FMAs per entry as k_update_x followed by k_xpby)
+template <int R>
+__global__ void k_xpby_x(int64_t n, const double *scal, const double *z, double *p, double *x) {
+    using W = V<R>;
+    double a[R], b[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) { a[c] = scal[S_ALPHA + c]; b[c] = scal[S_BETA + c]; }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const typename W::T pv = W::ld(p, i);
+        W::st(x, i, vfma<R>(a, pv, W::ld(x, i)));
+        W::st(p, i, vfma<R>(b, pv, W::ld(z, i)));
+    }
+}
+
 // Sum per-CTA partials in index order; then apply `what`.
 enum { F_STORE = 0, F_ALPHA = 1, F_BETA_INIT = 2, F_BETA = 3, F_BETA_AUTO = 4 };
 // One CTA of kFinThreads: thread t sums partials t, t + T, t + 2T, ... in
@@ -842,10 +873,8 @@ enum { F_STORE = 0, F_ALPHA = 1, F_BETA_INIT = 2, F_BETA = 3, F_BETA_AUTO = 4 };
 // so the result is reproducible run to run.
 constexpr int kFinThreads = 1024;
 template <int R>
-__global__ void __launch_bounds__(kFinThreads) k_finalize(const double *partials, int nblocks, double *scal, int slot,
-                                                          int what, double tol) {
-    __shared__ double red[32 * R];
-    double s[R], s4[4][R];
+__device__ __forceinline__ void fin_sum(const double *partials, int nblocks, double (&s)[R], double *red) {
+    double s4[4][R];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -863,6 +892,14 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(const double *partials
 #pragma unroll
     for (int c = 0; c < R; ++c) s[c] = (s4[0][c] + s4[1][c]) + (s4[2][c] + s4[3][c]);
     block_sum<R>(s, red);
+}
+
+template <int R>
+__global__ void __launch_bounds__(kFinThreads) k_finalize(const double *partials, int nblocks, double *scal, int slot,
+                                                          int what, double tol) {
+    __shared__ double red[32 * R];
+    double s[R];
+    fin_sum<R>(partials, nblocks, s, red);
     if (threadIdx.x == 0) {
         if (what == F_BETA_AUTO) {  // graph PCG: the first iteration after a (re)start initialises rho
             what = scal[S_G_INIT] != 0.0 ? F_BETA_INIT : F_BETA;
@@ -892,7 +929,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(const double *partials
 // the iteration, records the residual estimates, updates the per-rhs active
 // flags and ends the WHILE node on convergence, non-finite residual or the
 // iteration cap.
-__global__ void k_check(double *scal, int R, double *trace, cudaGraphConditionalHandle hnd) {
+__device__ void check_body(double *scal, int R, double *trace, cudaGraphConditionalHandle hnd) {
     const int it = (int)scal[S_G_IT] + 1;
     scal[S_G_IT] = it;
     const double tol = scal[S_G_TOL];
@@ -910,6 +947,25 @@ __global__ void k_check(double *scal, int R, double *trace, cudaGraphConditional
     }
     if (bad) scal[S_G_STATUS] = 1.0;
     if (done || bad || it >= maxit) cudaGraphSetConditional(hnd, 0);
+}
+
+__global__ void k_check(double *scal, int R, double *trace, cudaGraphConditionalHandle hnd) {
+    check_body(scal, R, trace, hnd);
+}
+
+// r.r finalize (F_STORE into S_RR) and the convergence test in one launch:
+// k_finalize's summation order, then k_check's body on thread 0
+template <int R>
+__global__ void __launch_bounds__(kFinThreads) k_finalize_check(const double *partials, int nblocks, double *scal,
+                                                                double *trace, cudaGraphConditionalHandle hnd) {
+    __shared__ double red[32 * R];
+    double s[R];
+    fin_sum<R>(partials, nblocks, s, red);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int c = 0; c < R; ++c) scal[S_RR + c] = s[c];
+        check_body(scal, R, trace, hnd);
+    }
 }
 
 __global__ void k_set_active(double *scal, int R, double tol) {
@@ -1630,30 +1686,47 @@ bool pcg_graph_enabled() {
     return v == 1;
 }
 
+// SPFD_PCG_FUSE_X=0: the graph body's x update as a separate side-stream
+// kernel overlapping the V-cycle instead of fused into the p update
+bool pcg_fuse_x() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_PCG_FUSE_X");
+        v = (e && std::string(e) == "0") ? 0 : 1;
+    }
+    return v == 1;
+}
+
 template <int R>
 void pcg_body(Amg &h, cudaGraphConditionalHandle hnd, cudaStream_t s) {
     const int64_t n = h.lv[0].nvec;
     double *r = h.kr.get(), *z = h.kz.get(), *p = h.kp.get(), *q = h.kq.get(), *x = h.kx.get();
     double *sc = h.scal.get();
-    // x += alpha p with the previous iteration's alpha, overlapping the V-cycle
-    SPFD_CUDA(cudaEventRecord(h.ev_alpha, s));
-    SPFD_CUDA(cudaStreamWaitEvent(h.side, h.ev_alpha, 0));
-    k_update_x<R><<<grid_for(n, 256, 148 * 8), 256, 0, h.side>>>(n, sc, x, p);
-    SPFD_LAUNCH_CHECK();
-    SPFD_CUDA(cudaEventRecord(h.ev_x, h.side));
+    const bool fuse = pcg_fuse_x();
+    if (!fuse) {
+        // x += alpha p with the previous iteration's alpha, overlapping the V-cycle
+        SPFD_CUDA(cudaEventRecord(h.ev_alpha, s));
+        SPFD_CUDA(cudaStreamWaitEvent(h.side, h.ev_alpha, 0));
+        k_update_x<R><<<grid_for(n, 256, 148 * 8), 256, 0, h.side>>>(n, sc, x, p);
+        SPFD_LAUNCH_CHECK();
+        SPFD_CUDA(cudaEventRecord(h.ev_x, h.side));
+    }
     amg_vcycle(h, r, z, R, s);
     if (h.vc_partials > 0) finalize<R>(h, h.vc_partials, S_RZ, F_BETA_AUTO, s);
     else dot<R>(h, n, r, z, S_RZ, F_BETA_AUTO, s);
-    SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
     const int rv = 0;
-    k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, rv);
+    if (fuse) {
+        k_xpby_x<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, x);
+    } else {
+        SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
+        k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, rv);
+    }
     SPFD_LAUNCH_CHECK();
     const int g = level0_apply<R>(h, 0, true, p, nullptr, q, s, true);  // q = A p, p.q
     finalize<R>(h, g, S_PQ, F_ALPHA, s);
     k_update_r<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, r, q, h.partials.get(), rv);
     SPFD_LAUNCH_CHECK();
-    finalize<R>(h, kDotGrid, S_RR, F_STORE, s);
-    k_check<<<1, 1, 0, s>>>(sc, R, h.pcg_trace.get(), hnd);
+    k_finalize_check<R><<<1, kFinThreads, 0, s>>>(h.partials.get(), kDotGrid, sc, h.pcg_trace.get(), hnd);
     SPFD_LAUNCH_CHECK();
 }
 
@@ -2539,7 +2612,8 @@ double coarse_vcycle_bytes(const Amg &h, int l0, double R) {
 double amg_iteration_bytes(const Amg &h, int nrhs) {
     const double R = nrhs;
     const KernelBytes k = kernel_bytes(h, R);
-    double b = k.spmv + 3.0 * k.blas1;  // q = A p; r, x, p updates
+    // q = A p; r, x, p updates (x and p fused: 5 arrays instead of 6)
+    double b = k.spmv + (pcg_fuse_x() ? 1.0 + 5.0 / 3.0 : 3.0) * k.blas1;
     if (h.lv.size() == 1) return b + coarse_vcycle_bytes(h, 0, R);
     const double pos = h.structured ? (double)h.op->L : 0.0;
     if (h.structured)
@@ -2570,7 +2644,7 @@ double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cu
     SPFD_CHECK(which >= 0 && which < 10, SPFD_EINVAL, "unknown kernel");
     const KernelBytes kb = kernel_bytes(h, nrhs);
     const double byt[10] = {kb.spmv, kb.presmooth, kb.postsmooth, 0.0, kb.prolong, kb.aggsum, kb.l1_pre, kb.l1_pp,
-                            kb.blas1, kb.blas1};
+                            kb.blas1, pcg_fuse_x() ? kb.blas1 * 5.0 / 3.0 : kb.blas1};
     auto launch2 = [&](auto rt) {
         constexpr int R = decltype(rt)::value;
         double *p = h.kp.get(), *r = h.kr.get(), *q = h.kq.get(), *z = h.kz.get();
@@ -2615,7 +2689,10 @@ double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cu
                 SPFD_LAUNCH_CHECK();
                 break;
             case 9:
-                k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h.scal.get(), z, p);
+                if (pcg_fuse_x())
+                    k_xpby_x<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h.scal.get(), z, p, h.kx.get());
+                else
+                    k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h.scal.get(), z, p);
                 SPFD_LAUNCH_CHECK();
                 break;
             default: {
@@ -2641,7 +2718,7 @@ double amg_bench_kernel(Amg &h, int which, int reps, int nrhs, double *bytes, cu
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *bytes = byt[which];
-    if (which == 3) *bytes = amg_iteration_bytes(h, nrhs) - kb.spmv - 3.0 * kb.blas1;
+    if (which == 3) *bytes = amg_iteration_bytes(h, nrhs) - kb.spmv - (pcg_fuse_x() ? 1.0 + 5.0 / 3.0 : 3.0) * kb.blas1;
     return ms / reps;
 }
 
