@@ -69,6 +69,7 @@ NcclApi &nccl() {
 
 struct NcclComm : Comm {
     ncclComm_t c = nullptr;
+    bool stream_ordered() const override { return true; }
     struct Op {
         int peer, kind;
         void *buf;

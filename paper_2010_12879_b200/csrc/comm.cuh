@@ -24,6 +24,9 @@ struct Comm {
     virtual void end(cudaStream_t s) = 0;
     // rank-ordered concatenation of `bytes` from every rank into recv
     virtual void allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) = 0;
+    // every operation is stream-ordered (no host synchronisation), so a
+    // sequence of them can be captured into a CUDA graph
+    virtual bool stream_ordered() const { return false; }
 };
 
 Comm *comm_nccl(const void *unique_id, int rank, int size);

@@ -69,7 +69,16 @@ struct Dist {
     int64_t ib = 0, ie = 0;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // distributed PCG: one batch of iterations captured as a CUDA graph per
+    // rhs count (stream-ordered transports only; pcg_dist)
+    cudaGraphExec_t batch_exec[3] = {nullptr, nullptr, nullptr};
+    int batch_nb[3] = {0, 0, 0};
+    const double *batch_trace[3] = {nullptr, nullptr, nullptr};
+    int64_t batch_launches[3] = {0, 0, 0};
+    bool batch_failed[3] = {false, false, false};
     ~Dist() {
+        for (auto &e : batch_exec)
+            if (e) cudaGraphExecDestroy(e);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (side) cudaStreamDestroy(side);
@@ -775,6 +784,71 @@ inline int dist_batch() {
     return v;
 }
 
+// SPFD_DIST_GRAPH=0: queue the distributed iteration batches as individual
+// launches even on a stream-ordered transport
+inline bool dist_graph_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_DIST_GRAPH");
+        v = (e && std::string(e) == "0") ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// One batch of nb iterations (the kernels and transport calls `body` issues
+// on the stream it is given) replayed as a CUDA graph: captured on the
+// hierarchy's private capture stream the first time, ordered after and
+// before the work on s by events.  Returns false (the caller launches the
+// batch itself) when the batch cannot be captured.
+template <int R, class Body>
+bool dist_batch_graph(Amg &h, int nb, Body &&body, cudaStream_t s) {
+    Dist &D = *h.dist;
+    if (D.batch_exec[R] && (D.batch_nb[R] != nb || D.batch_trace[R] != h.pcg_trace.get())) {
+        cudaGraphExecDestroy(D.batch_exec[R]);
+        D.batch_exec[R] = nullptr;
+    }
+    if (!D.batch_exec[R]) {
+        if (D.batch_failed[R]) return false;
+        if (!h.cap) SPFD_CUDA(cudaStreamCreateWithFlags(&h.cap, cudaStreamNonBlocking));
+        const int64_t l0 = launch_count();
+        SPFD_CUDA(cudaStreamBeginCapture(h.cap, cudaStreamCaptureModeRelaxed));
+        std::string why;
+        try {
+            body(nb, h.cap);
+        } catch (const std::exception &e) {
+            why = e.what();
+        }
+        cudaGraph_t g = nullptr;
+        cudaError_t ec = cudaStreamEndCapture(h.cap, &g);
+        cudaGraphExec_t exec = nullptr;
+        if (why.empty() && ec == cudaSuccess) {
+            ec = cudaGraphInstantiate(&exec, g, 0);
+            if (ec != cudaSuccess) why = std::string("instantiate: ") + cudaGetErrorString(ec);
+        } else if (why.empty()) {
+            why = std::string("end capture: ") + cudaGetErrorString(ec);
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();  // clear a sticky capture error
+        if (!why.empty()) {
+            if (getenv("SPFD_DEBUG")) fprintf(stderr, "[spfd] distributed batch capture failed (%s)\n", why.c_str());
+            D.batch_failed[R] = true;
+            return false;
+        }
+        D.batch_exec[R] = exec;
+        D.batch_nb[R] = nb;
+        D.batch_trace[R] = h.pcg_trace.get();
+        D.batch_launches[R] = launch_count() - l0;
+    } else {
+        for (int64_t k = 0; k < D.batch_launches[R]; ++k) count_launch();
+    }
+    SPFD_CUDA(cudaEventRecord(h.ev_alpha, s));
+    SPFD_CUDA(cudaStreamWaitEvent(h.cap, h.ev_alpha, 0));
+    SPFD_CUDA(cudaGraphLaunch(D.batch_exec[R], h.cap));
+    SPFD_CUDA(cudaEventRecord(h.ev_x, h.cap));
+    SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
+    return true;
+}
+
 template <int R>
 spfd_report pcg_dist(Amg &h, const double *b, double *x, const spfd_config &cfg, double *h_trace, cudaStream_t s) {
     Dist &D = *h.dist;
@@ -827,22 +901,29 @@ spfd_report pcg_dist(Amg &h, const double *b, double *x, const spfd_config &cfg,
         // a batch of iterations, the convergence test on the device; the
         // ones queued behind a stop are no-ops (k_dist_check)
         const int nb = std::min(dist_batch(), cfg.max_iters - it);
-        for (int k = 0; k < nb; ++k) {
-            int g = apply_dist<R>(h, 0, true, p, nullptr, q, s);    // q = A p, p.q
-            finalize_dist<R>(h, g, S_PQ, F_ALPHA, s);
-            k_update_xr<R><<<kDotGrid, kDotThreads, 0, s>>>(no, sc, x + off, r + off, p + off, q + off,
-                                                           h.partials.get());
-            SPFD_LAUNCH_CHECK();
-            finalize_dist<R>(h, kDotGrid, S_RR, F_STORE, s);
-            k_dist_check<<<1, 1, 0, s>>>(sc, R, h.pcg_trace.get());
-            SPFD_LAUNCH_CHECK();
-            if (k + 1 == nb) break;  // the host decides what follows the batch's last test
-            int gz = vcycle_dist_fine<R>(h, r, z, s);
-            if (gz > 0) finalize_dist<R>(h, gz, S_RZ, F_BETA, s);
-            else dot_dist<R>(h, r, z, S_RZ, F_BETA, s);
-            k_xpby<R><<<grid_for(no, 256, 148 * 16), 256, 0, s>>>(no, sc, z + off, p + off);
-            SPFD_LAUNCH_CHECK();
-        }
+        auto batch = [&](int nbat, cudaStream_t st) {
+            for (int k = 0; k < nbat; ++k) {
+                int g = apply_dist<R>(h, 0, true, p, nullptr, q, st);    // q = A p, p.q
+                finalize_dist<R>(h, g, S_PQ, F_ALPHA, st);
+                k_update_xr<R><<<kDotGrid, kDotThreads, 0, st>>>(no, sc, x + off, r + off, p + off, q + off,
+                                                                h.partials.get());
+                SPFD_LAUNCH_CHECK();
+                finalize_dist<R>(h, kDotGrid, S_RR, F_STORE, st);
+                k_dist_check<<<1, 1, 0, st>>>(sc, R, h.pcg_trace.get());
+                SPFD_LAUNCH_CHECK();
+                if (k + 1 == nbat) break;  // the host decides what follows the batch's last test
+                int gz = vcycle_dist_fine<R>(h, r, z, st);
+                if (gz > 0) finalize_dist<R>(h, gz, S_RZ, F_BETA, st);
+                else dot_dist<R>(h, r, z, S_RZ, F_BETA, st);
+                k_xpby<R><<<grid_for(no, 256, 148 * 16), 256, 0, st>>>(no, sc, z + off, p + off);
+                SPFD_LAUNCH_CHECK();
+            }
+        };
+        // full batches on a stream-ordered transport (NCCL) replay one
+        // captured graph: no per-kernel launch cost between host reads
+        const bool graphed = nb == dist_batch() && nb > 1 && D.comm->stream_ordered() && dist_graph_enabled() &&
+                             dist_batch_graph<R>(h, nb, batch, s);
+        if (!graphed) batch(nb, s);
         double gs[8];
         SPFD_CUDA(cudaMemcpyAsync(gs, sc + S_G, sizeof gs, cudaMemcpyDeviceToHost, s));
         SPFD_CUDA(cudaStreamSynchronize(s));

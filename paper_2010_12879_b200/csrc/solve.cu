@@ -1090,8 +1090,10 @@ int launch_fine(const Operator &op, const SpanArgs &a_in, cudaStream_t s) {
         b.tile0 = t0;
         int g = t1 - t0;
         if (g > 0) {
-            if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, true, true><<<g, kSpanThreads, 0, s>>>(v, b);
-            else k_span<R, MODE, DOT, true><<<g, kSpanThreads, 0, s>>>(v, b);
+            // 4 CTAs/SM: the range checks cost registers; at 6 (and 5) the ranged
+            // instantiations spilled (the single-GPU kernels keep 6, measured)
+            if (fine_kernel_kind() == 3) k_span<R, MODE, DOT, true, true, 4><<<g, kSpanThreads, 0, s>>>(v, b);
+            else k_span<R, MODE, DOT, true, false, 4><<<g, kSpanThreads, 0, s>>>(v, b);
         }
         SPFD_LAUNCH_CHECK();
         return g;

@@ -158,6 +158,21 @@ def test_nccl_transport_single_rank():
 
 
 @pytest.mark.gpu
+def test_nccl_batch_graph_is_exact(monkeypatch):
+    """On the stream-ordered NCCL transport the distributed PCG replays each
+    full batch of iterations as one captured CUDA graph; it must give the
+    launched batches' iterations and bits (SPFD_DIST_GRAPH=0)."""
+    res = {}
+    for graph in ("0", "1"):
+        monkeypatch.setenv("SPFD_DIST_GRAPH", graph)
+        with tempfile.TemporaryDirectory() as out:
+            mp.spawn(_nccl_single_worker, args=(1, _port(), out), nprocs=1, join=True)
+            res[graph] = torch.load(os.path.join(out, "n.pt"))
+    assert res["0"]["it"] == res["1"]["it"]
+    assert torch.equal(res["0"]["vox"], res["1"]["vox"])
+
+
+@pytest.mark.gpu
 def test_distributed_iteration_batching_is_exact(monkeypatch):
     """The distributed PCG queues several iterations per host read, with the
     convergence test on the device freezing the iterations behind a stop:
