@@ -838,6 +838,9 @@ bool dist_batch_graph(Amg &h, int nb, Body &&body, cudaStream_t s) {
         D.batch_nb[R] = nb;
         D.batch_trace[R] = h.pcg_trace.get();
         D.batch_launches[R] = launch_count() - l0;
+        if (getenv("SPFD_DEBUG"))
+            fprintf(stderr, "[spfd] distributed batch graph captured: %d iterations, %lld launches\n", nb,
+                    (long long)D.batch_launches[R]);
     } else {
         for (int64_t k = 0; k < D.batch_launches[R]; ++k) count_launch();
     }

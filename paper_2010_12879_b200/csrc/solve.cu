@@ -1572,6 +1572,17 @@ void dot(Amg &h, int64_t n, const double *a, const double *b, int slot, int what
     finalize<R>(h, kDotGrid, slot, what, s);
 }
 
+// SPFD_PCG_FUSE_X=0: the x update as a separate side-stream kernel
+// overlapping the V-cycle instead of fused into the next p update
+bool pcg_fuse_x() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_PCG_FUSE_X");
+        v = (e && std::string(e) == "0") ? 0 : 1;
+    }
+    return v == 1;
+}
+
 template <int R>
 spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, double *h_trace, cudaStream_t s) {
     spfd_report rep{};
@@ -1596,6 +1607,7 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
     int it = 0;
     bool restart = true;
     double tol = cfg.rel_tol;
+    const bool fuse = pcg_fuse_x();
     while (true) {
         if (restart) {
             // r = b - A x ; z = M r ; rho = r.z ; p = z
@@ -1611,13 +1623,15 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
         const int rv = 0;
         int g = level0_apply<R>(h, 0, true, p, nullptr, q, s, true);  // q = A p, p.q
         finalize<R>(h, g, S_PQ, F_ALPHA, s);
-        // x += alpha p on the side stream, overlapping the V-cycle (which is
-        // L1/latency-bound and leaves HBM bandwidth idle); joined before p changes
-        SPFD_CUDA(cudaEventRecord(h.ev_alpha, s));
-        SPFD_CUDA(cudaStreamWaitEvent(h.side, h.ev_alpha, 0));
-        k_update_x<R><<<grid_for(n, 256, 148 * 8), 256, 0, h.side>>>(n, sc, x, p);
-        SPFD_LAUNCH_CHECK();
-        SPFD_CUDA(cudaEventRecord(h.ev_x, h.side));
+        if (!fuse) {
+            // x += alpha p on the side stream, overlapping the V-cycle (which is
+            // L1/latency-bound and leaves HBM bandwidth idle); joined before p changes
+            SPFD_CUDA(cudaEventRecord(h.ev_alpha, s));
+            SPFD_CUDA(cudaStreamWaitEvent(h.side, h.ev_alpha, 0));
+            k_update_x<R><<<grid_for(n, 256, 148 * 8), 256, 0, h.side>>>(n, sc, x, p);
+            SPFD_LAUNCH_CHECK();
+            SPFD_CUDA(cudaEventRecord(h.ev_x, h.side));
+        }  // else: x += alpha p rides with the next p update (k_xpby_x), or is flushed below
         k_update_r<R><<<kDotGrid, kDotThreads, 0, s>>>(n, sc, r, q, h.partials.get(), rv);
         SPFD_LAUNCH_CHECK();
         finalize<R>(h, kDotGrid, S_RR, F_STORE, s);
@@ -1634,6 +1648,10 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
         }
         if (done || it >= cfg.max_iters) {
             // true residual check (linsolve.py:296-298 semantics)
+            if (fuse) {
+                k_update_x<R><<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, sc, x, p);
+                SPFD_LAUNCH_CHECK();
+            }
             SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
             int gt = level0_apply<R>(h, 1, true, x, b, q, s);
             finalize<R>(h, gt, S_TMP, F_STORE, s);
@@ -1655,8 +1673,12 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
         amg_vcycle(h, r, z, R, s);
         if (h.vc_partials > 0) finalize<R>(h, h.vc_partials, S_RZ, F_BETA, s);  // r.z fused into the post-smooth
         else dot<R>(h, n, r, z, S_RZ, F_BETA, s);
-        SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));  // x += alpha p done before p changes
-        k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, 0);
+        if (fuse) {
+            k_xpby_x<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, x);
+        } else {
+            SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));  // x += alpha p done before p changes
+            k_xpby<R><<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, sc, z, p, 0);
+        }
         SPFD_LAUNCH_CHECK();
     }
     SPFD_CUDA(cudaStreamWaitEvent(s, h.ev_x, 0));
@@ -1683,17 +1705,6 @@ bool pcg_graph_enabled() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("SPFD_PCG_GRAPH");
-        v = (e && std::string(e) == "0") ? 0 : 1;
-    }
-    return v == 1;
-}
-
-// SPFD_PCG_FUSE_X=0: the graph body's x update as a separate side-stream
-// kernel overlapping the V-cycle instead of fused into the p update
-bool pcg_fuse_x() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SPFD_PCG_FUSE_X");
         v = (e && std::string(e) == "0") ? 0 : 1;
     }
     return v == 1;

@@ -158,16 +158,20 @@ def test_nccl_transport_single_rank():
 
 
 @pytest.mark.gpu
-def test_nccl_batch_graph_is_exact(monkeypatch):
+def test_nccl_batch_graph_is_exact(monkeypatch, capfd):
     """On the stream-ordered NCCL transport the distributed PCG replays each
     full batch of iterations as one captured CUDA graph; it must give the
     launched batches' iterations and bits (SPFD_DIST_GRAPH=0)."""
     res = {}
+    monkeypatch.setenv("SPFD_DEBUG", "1")
     for graph in ("0", "1"):
         monkeypatch.setenv("SPFD_DIST_GRAPH", graph)
+        capfd.readouterr()
         with tempfile.TemporaryDirectory() as out:
             mp.spawn(_nccl_single_worker, args=(1, _port(), out), nprocs=1, join=True)
             res[graph] = torch.load(os.path.join(out, "n.pt"))
+        captured = "distributed batch graph captured" in capfd.readouterr().err
+        assert captured == (graph == "1")
     assert res["0"]["it"] == res["1"]["it"]
     assert torch.equal(res["0"]["vox"], res["1"]["vox"])
 

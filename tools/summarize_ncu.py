@@ -2,6 +2,12 @@
 throughputs, occupancy.  Writes a markdown table and the traffic json."""
 import csv, io, json, subprocess, sys
 rep, out_md, out_json = sys.argv[1], sys.argv[2], sys.argv[3]
+CFG = sys.argv[4] if len(sys.argv) > 4 else "C3"
+# kernel (name prefix in the report) -> bench.py `kernels` key; first launch of each
+KEYS = [("k_span<2, 0, 1", "fine_spmv"), ("k_span<2, 2, 0", "fine_presmooth"), ("k_csr<1, 2, 4", "fine_prolongation"),
+        ("k_span<2, 3, 1", "fine_postsmooth"), ("k_csr<4, 2, 0", "fine_restriction"),
+        ("k_csr<4, 2, 1", "level1_presmooth"), ("k_csr<4, 2, 6", "level1_prolong_post"),
+        ("k_update_r<2>", "pcg_r_update"), ("k_xpby_x<2>", "pcg_p_update")]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h = rows[0]
@@ -32,9 +38,10 @@ for r in rows[2:]:
                  f"{float(r[cols['lts__throughput.avg.pct_of_peak_sustained_elapsed']]):.0f} | "
                  f"{float(r[cols['sm__warps_active.avg.pct_of_peak_sustained_active']]):.0f} | "
                  f"{r[cols['launch__registers_per_thread']]} | {r[cols['launch__grid_size']]} |")
-    if name.startswith("k_span<2, 0, 1") and "C3_fine_spmv_dram_bytes" not in traffic:
-        traffic["C3_fine_spmv_dram_bytes"] = rd + wr
-        traffic["C3_fine_spmv_ncu_us"] = us
+    for prefix, key in KEYS:
+        if name.startswith(prefix) and f"{CFG}_{key}_dram_bytes" not in traffic:
+            traffic[f"{CFG}_{key}_dram_bytes"] = rd + wr
+            traffic[f"{CFG}_{key}_ncu_us"] = us
 open(out_md, "w").write("\n".join(lines) + "\n")
 json.dump(traffic, open(out_json, "w"), indent=1)
 print("\n".join(lines)); print(traffic)
