@@ -491,8 +491,10 @@ def main():
         "config": {
             "workload": f"{args.config} {w.name}: {n_dofs} DOFs, complex (re/im) rhs batched",
             "rel_tol": REL_TOL, "method": "AMG-PCG (SA-AMG V(1,1), reference aggregation)",
-            "parallelism": (f"z-slab decomposition over {world} GPUs (NCCL send/recv halos, allgathered dots; "
-                            f"coarse levels < {args.replicate_below} rows replicated)") if world > 1 else "single GPU",
+            "parallelism": (f"z-slab decomposition over {world} GPUs ("
+                            + ("NCCL send/recv halos, allgathered dots; " if args.transport == "nccl"
+                               else "host (gloo) transport, test mode; ")
+                            + f"coarse levels < {args.replicate_below} rows replicated)") if world > 1 else "single GPU",
             "l2": "inputs larger than L2 (fine-level working set >> 126 MB)",
             "step": "rhs assembly + solve to 1e-8 (both rhs) + fused E-field/voxel average",
         },

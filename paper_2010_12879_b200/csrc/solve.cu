@@ -380,6 +380,10 @@ __device__ __forceinline__ void csr_row_out(typename V<R>::T acc, bool lead, int
     }
 }
 
+#ifndef SPFD_CSR_UNROLL_WIDE
+#define SPFD_CSR_UNROLL_WIDE 4  // entries in flight per lane for groups of >= 8 lanes (8: C3 33.1 vs 32.9 ms)
+#endif
+
 template <int G, int R, int MODE, bool DOT>
 __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__restrict__ r,
                       const double *__restrict__ od, const double *__restrict__ base, double *__restrict__ y,
@@ -402,9 +406,9 @@ __global__ void k_csr(CsrView m, const double *__restrict__ x, const double *__r
         const bool valid = row < m.rows;
         T acc = W::zero();
         if (valid) {
-            // 4 entries per lane in flight (all loads issued before the FMAs,
+            // U entries per lane in flight (all loads issued before the FMAs,
             // which keep the sequential per-lane order)
-            constexpr int U = 4;
+            constexpr int U = G >= 8 ? SPFD_CSR_UNROLL_WIDE : 4;
             const int64_t q1 = m.ptr[row + 1];
             for (int64_t q = m.ptr[row] + lane; q < q1; q += U * G) {
                 int col[U];
@@ -949,12 +953,8 @@ __device__ void check_body(double *scal, int R, double *trace, cudaGraphConditio
     if (done || bad || it >= maxit) cudaGraphSetConditional(hnd, 0);
 }
 
-__global__ void k_check(double *scal, int R, double *trace, cudaGraphConditionalHandle hnd) {
-    check_body(scal, R, trace, hnd);
-}
-
 // r.r finalize (F_STORE into S_RR) and the convergence test in one launch:
-// k_finalize's summation order, then k_check's body on thread 0
+// k_finalize's summation order, then the test (check_body) on thread 0
 template <int R>
 __global__ void __launch_bounds__(kFinThreads) k_finalize_check(const double *partials, int nblocks, double *scal,
                                                                 double *trace, cudaGraphConditionalHandle hnd) {
@@ -1688,9 +1688,9 @@ spfd_report pcg(Amg &h, const double *b, double *x, const spfd_config &cfg, doub
 
 // ---- PCG as one CUDA graph ------------------------------------------------
 // The iteration is rotated so the convergence test ends the body:
-//   x += alpha p (side branch, previous alpha)  |  z = M r, beta (rho on the
-//   first pass after a (re)start)  ->  p = z + beta p  ->  q = A p, alpha  ->
-//   r -= alpha q, r.r  ->  k_check (sets the WHILE condition)
+//   z = M r, beta (rho on the first pass after a (re)start)  ->
+//   x += alpha p (previous alpha), p = z + beta p  ->  q = A p, alpha  ->
+//   r -= alpha q, r.r  ->  k_finalize_check (sets the WHILE condition)
 // which is the host loop's arithmetic in the same order.  The body is
 // captured once per rhs count into the WHILE node of a graph; a solve is
 // restart prologue + one graph launch (+ the last x update), and the host
