@@ -615,11 +615,24 @@ inline int csr_prefetch_enabled() {
     return v;
 }
 
-inline int csr_grid(int64_t rows, int G) {
+// CTAs per SM the grid-stride CSR launches are capped at (SPFD_CSR_GRID_PER_SM,
+// default 8 = one resident wave of 256-thread CTAs: C3 32.91 vs 33.00 ms at
+// 16, 33.2 at 32, 37.6 at 4; launches writing dot partials keep 16, the
+// partials buffer's size).  Rows do not depend on the grid: same bits.
+inline int csr_grid_per_sm() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPFD_CSR_GRID_PER_SM");
+        v = e ? std::max(1, std::min(64, atoi(e))) : 8;
+    }
+    return v;
+}
+
+inline int csr_grid(int64_t rows, int G, int per_sm = 16) {
     int64_t groups = G >= kCsrThreads ? 1 : (int64_t)kCsrThreads / G;
     int64_t g = (rows + groups - 1) / groups;
     if (g < 1) g = 1;
-    if (g > 148 * 16) g = 148 * 16;
+    if (g > 148 * per_sm) g = 148 * per_sm;
     return (int)g;
 }
 
@@ -639,7 +652,7 @@ template <int R, int MODE, bool DOT>
 int launch_csr(const Csr &m, int G, const double *x, const double *r, const double *od, const double *base,
                double *y, double *partials, cudaStream_t s, const double *od_aux = nullptr, double *aux = nullptr,
                const int32_t *rowmap = nullptr) {
-    int grid = csr_grid(m.rows, G);
+    int grid = csr_grid(m.rows, G, DOT ? 16 : csr_grid_per_sm());
     switch (G) {
         case 1: launch_csr_g<1, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
         case 2: launch_csr_g<2, R, MODE, DOT>(m, x, r, od, base, y, partials, s, grid, od_aux, aux, rowmap); break;
